@@ -1,0 +1,247 @@
+"""CPU oracle for the PW-advection hot path — TEST INFRASTRUCTURE ONLY.
+
+This module is the checker, never the thing measured or shipped: only
+`tests/`, `__graft_entry__.smoke()` and `bench.py` (its `cpu_baseline` leg and
+`--impl reference`) may import it. The product package
+`paper_2010_01545_b200` never imports it and has no CPU fallback.
+
+Two independent restatements of the reference algorithm live here:
+
+* `liboracle.so` (oracle/pwadv_oracle.c, plain C, -ffp-contract=off) — the
+  fast one, threaded over X slabs like `run_schedule`'s engines
+  (reference pkg/src/pwadvect/schedules.py:65-75, 207-232).
+* `advect_numpy` — a vectorised numpy transcription of `compute_block`
+  (reference pkg/src/pwadvect/kernel.py:139-185), used to cross-check the C
+  restatement.
+
+Both are pinned against the reference's own golden digests
+(reference pkg/tests/goldens.json) and against fixtures produced by importing
+the reference (tests/golden/make_golden.py → tests/golden/*.json, *.npz).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+_LIB_PATH = _HERE / "_build" / "liboracle.so"
+_lib = None
+
+_D = ctypes.POINTER(ctypes.c_double)
+_I64 = ctypes.c_int64
+
+
+def build() -> Path:
+    """Compile liboracle.so with the committed Makefile (gcc, no FMA)."""
+    subprocess.run(["make", "-s", "-C", str(_HERE)], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            build()
+        L = ctypes.CDLL(str(_LIB_PATH))
+        L.oracle_advect.argtypes = [_D, _D, _D, _D, _D, _D, _I64, _I64, _I64,
+                                    ctypes.c_double, ctypes.c_double, _D, _D, ctypes.c_int]
+        L.oracle_advect.restype = ctypes.c_int
+        L.oracle_advect_slab.argtypes = [_D, _D, _D, _D, _D, _D, _I64, _I64, _I64,
+                                         ctypes.c_double, ctypes.c_double, _D, _D, _I64, _I64]
+        L.oracle_advect_slab.restype = None
+        L.oracle_wrap_halos.argtypes = [_D, _I64, _I64, _I64]
+        L.oracle_wrap_halos.restype = None
+        L.oracle_lcg_doubles.argtypes = [ctypes.c_uint64, ctypes.c_uint64, _I64, _D]
+        L.oracle_lcg_doubles.restype = None
+        L.oracle_fill_random.argtypes = [_D, _D, _D, _I64, _I64, _I64, ctypes.c_uint64, ctypes.c_int]
+        L.oracle_fill_random.restype = None
+        L.oracle_baseline_coefficients.argtypes = [ctypes.c_uint64, _I64, _D, _D, _D, _D]
+        L.oracle_baseline_coefficients.restype = None
+        L.oracle_step.argtypes = [_D, _D, _D, _D, _I64, _I64, _I64, ctypes.c_double,
+                                  ctypes.c_double, _D, _D, ctypes.c_double, ctypes.c_int]
+        L.oracle_step.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_D)
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------------
+# generation (reference grid.py:164-239 + BASELINE mapping)
+
+def lcg_doubles(seed: int, count: int, start: int = 0) -> np.ndarray:
+    out = np.empty(count)
+    if count:
+        lib().oracle_lcg_doubles(seed & (2**64 - 1), start, count, _p(out))
+    return out
+
+
+def fill_random(nx: int, ny: int, nz: int, seed: int, baseline: bool = False):
+    """(u, v, w) padded arrays: reference random fill, optionally BASELINE-mapped."""
+    shape = (nx + 2, ny + 2, nz)
+    u, v, w = (np.empty(shape) for _ in range(3))
+    lib().oracle_fill_random(_p(u), _p(v), _p(w), nx, ny, nz, seed & (2**64 - 1),
+                             1 if baseline else 0)
+    return u, v, w
+
+
+def baseline_coefficients(seed: int, nz: int) -> dict:
+    """tcx=tcy=0.25/50, tzc1/tzc2 (+ recorded tzd1/tzd2) in [1e-3, 5e-3)."""
+    arrs = [np.empty(nz) for _ in range(4)]
+    lib().oracle_baseline_coefficients(seed & (2**64 - 1), nz, *(_p(a) for a in arrs))
+    return {"tcx": 0.25 / 50.0, "tcy": 0.25 / 50.0, "tzc1": arrs[0], "tzc2": arrs[1],
+            "tzd1": arrs[2], "tzd2": arrs[3]}
+
+
+def wrap_halos(a: np.ndarray) -> None:
+    nx, ny, nz = a.shape[0] - 2, a.shape[1] - 2, a.shape[2]
+    lib().oracle_wrap_halos(_p(a), nx, ny, nz)
+
+
+# --------------------------------------------------------------------------
+# the stencil
+
+def advect(u, v, w, tcx, tcy, tzc1, tzc2, engines: int = 1):
+    """C restatement of run_reference (kernel.py:175-185); returns padded su, sv, sw."""
+    nx, ny, nz = u.shape[0] - 2, u.shape[1] - 2, u.shape[2]
+    tzc1 = np.ascontiguousarray(tzc1, dtype=np.float64)
+    tzc2 = np.ascontiguousarray(tzc2, dtype=np.float64)
+    if tzc1.shape != (nz,) or tzc2.shape != (nz,):
+        raise ValueError(f"coefficient length {tzc1.shape} != nz {nz}")
+    outs = [np.zeros_like(u) for _ in range(3)]
+    rc = lib().oracle_advect(_p(u), _p(v), _p(w), *(_p(o) for o in outs), nx, ny, nz,
+                             float(tcx), float(tcy), _p(tzc1), _p(tzc2), int(engines))
+    if rc:
+        raise ValueError("oracle_advect: bad arguments")
+    return tuple(outs)
+
+
+def advect_into(u, v, w, su, sv, sw, tcx, tcy, tzc1, tzc2, engines: int = 1) -> None:
+    """As `advect`, writing into caller-provided (pre-zeroed) outputs."""
+    nx, ny, nz = u.shape[0] - 2, u.shape[1] - 2, u.shape[2]
+    rc = lib().oracle_advect(_p(u), _p(v), _p(w), _p(su), _p(sv), _p(sw), nx, ny, nz,
+                             float(tcx), float(tcy), _p(tzc1), _p(tzc2), int(engines))
+    if rc:
+        raise ValueError("oracle_advect: bad arguments")
+
+
+def advect_numpy(u, v, w, tcx, tcy, tzc1, tzc2):
+    """Vectorised numpy transcription of compute_block/run_reference (kernel.py:139-185)."""
+    nx, ny, nz = u.shape[0] - 2, u.shape[1] - 2, u.shape[2]
+    tzc1 = np.asarray(tzc1, dtype=np.float64)
+    tzc2 = np.asarray(tzc2, dtype=np.float64)
+    F = {"u": u, "v": v, "w": w}
+
+    def r(f, dx, dy, k):
+        return F[f][1 + dx:nx + 1 + dx, 1 + dy:ny + 1 + dy, k]
+
+    outs = []
+    mid = slice(1, nz - 1)
+    km1 = slice(0, nz - 2)
+    kp1 = slice(2, nz)
+    t = nz - 1
+    for name in ("su", "sv", "sw"):
+        s = np.zeros((nx, ny, nz))
+        for ks, kd, kp, top in ((mid, km1, kp1, False), (t, t - 1, t, True)):
+            if not top and nz <= 2:
+                continue
+            c1 = tzc1[ks]
+            c2 = tzc2[ks]
+            if name == "su":
+                X = tcx * (r("u", -1, 0, ks) * (r("u", 0, 0, ks) + r("u", -1, 0, ks))
+                           - r("u", 1, 0, ks) * (r("u", 0, 0, ks) + r("u", 1, 0, ks)))
+                Y = tcy * (r("u", 0, -1, ks) * (r("v", 0, -1, ks) + r("v", 1, -1, ks))
+                           - r("u", 0, 1, ks) * (r("v", 0, 0, ks) + r("v", 1, 0, ks)))
+                A = c1 * r("u", 0, 0, kd) * (r("w", 0, 0, kd) + r("w", 1, 0, kd))
+                if not top:
+                    B = c2 * r("u", 0, 0, kp) * (r("w", 0, 0, ks) + r("w", 1, 0, ks))
+            elif name == "sv":
+                X = tcx * (r("v", -1, 0, ks) * (r("u", -1, 0, ks) + r("u", -1, 1, ks))
+                           - r("v", 1, 0, ks) * (r("u", 0, 0, ks) + r("u", 0, 1, ks)))
+                Y = tcy * (r("v", 0, -1, ks) * (r("v", 0, 0, ks) + r("v", 0, -1, ks))
+                           - r("v", 0, 1, ks) * (r("v", 0, 0, ks) + r("v", 0, 1, ks)))
+                A = c1 * r("v", 0, 0, kd) * (r("w", 0, 0, kd) + r("w", 0, 1, kd))
+                if not top:
+                    B = c2 * r("v", 0, 0, kp) * (r("w", 0, 0, ks) + r("w", 0, 1, ks))
+            else:
+                X = tcx * (r("w", -1, 0, ks) * (r("u", -1, 0, kd) + r("u", -1, 0, ks))
+                           - r("w", 1, 0, ks) * (r("u", 0, 0, kd) + r("u", 0, 0, ks)))
+                Y = tcy * (r("w", 0, -1, ks) * (r("v", 0, -1, kd) + r("v", 0, -1, ks))
+                           - r("w", 0, 1, ks) * (r("v", 0, 0, kd) + r("v", 0, 0, ks)))
+                A = c1 * r("w", 0, 0, kd) * (r("w", 0, 0, ks) + r("w", 0, 0, kd))
+                if not top:
+                    B = c2 * r("w", 0, 0, kp) * (r("w", 0, 0, ks) + r("w", 0, 0, kp))
+            s[..., ks] = (X + Y) + A if top else (X + Y) + (A - B)
+        full = np.zeros_like(u)
+        full[1:-1, 1:-1, 1:] = s[..., 1:]
+        outs.append(full)
+    return tuple(outs)
+
+
+def step(u, v, w, tcx, tcy, tzc1, tzc2, dt: float, steps: int, engines: int = 1):
+    """Composed forward-Euler oracle: in place on u, v, w."""
+    nx, ny, nz = u.shape[0] - 2, u.shape[1] - 2, u.shape[2]
+    scratch = np.zeros((3,) + u.shape)
+    tzc1 = np.ascontiguousarray(tzc1, dtype=np.float64)
+    tzc2 = np.ascontiguousarray(tzc2, dtype=np.float64)
+    for _ in range(steps):
+        rc = lib().oracle_step(_p(u), _p(v), _p(w), _p(scratch), nx, ny, nz, float(tcx),
+                               float(tcy), _p(tzc1), _p(tzc2), float(dt), int(engines))
+        if rc:
+            raise ValueError("oracle_step: bad arguments")
+
+
+# --------------------------------------------------------------------------
+# digests and comparison (reference grid.py:242-249, schedules.py:235-272)
+
+def checksum(padded: np.ndarray) -> str:
+    interior = np.ascontiguousarray(padded[1:-1, 1:-1, :], dtype="<f8")
+    return hashlib.blake2b(interior.tobytes(), digest_size=8).hexdigest()
+
+
+def _ordered_bits(arr):
+    bits = np.ascontiguousarray(arr).reshape(-1).view(np.int64)
+    return np.where(bits >= 0, bits, np.int64(-(2**63)) - bits)
+
+
+def max_ulp(a, b) -> int:
+    oa, ob = _ordered_bits(a), _ordered_bits(b)
+    same = (oa >= 0) == (ob >= 0)
+    worst = 0
+    if same.any():
+        worst = int(np.abs(oa[same] - ob[same]).max())
+    if (~same).any():
+        ua = np.abs(oa[~same]).astype(np.uint64)
+        ub = np.abs(ob[~same]).astype(np.uint64)
+        worst = max(worst, int((ua + ub).max()))
+    return worst
+
+
+def compare(a, b) -> dict:
+    """compare_outputs semantics over full padded arrays (schedules.py:261-272)."""
+    pairs = list(zip(a, b))
+    bitwise = all(np.array_equal(np.ascontiguousarray(x).view(np.int64),
+                                 np.ascontiguousarray(y).view(np.int64)) for x, y in pairs)
+    if bitwise:
+        return {"bitwise_equal": True, "max_abs_diff": 0.0, "max_ulp_diff": 0, "normwise_rel": 0.0}
+    max_abs = max(float(np.abs(x - y).max()) for x, y in pairs)
+    ref_max = max(float(np.abs(x).max()) for x, _ in pairs) or 1.0
+    mu = max(max_ulp(x, y) for x, y in pairs)
+    return {"bitwise_equal": False, "max_abs_diff": max_abs, "max_ulp_diff": max(mu, 1),
+            "normwise_rel": max_abs / ref_max}
