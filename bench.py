@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Benchmark: PW advection grid points/s (fp64) on B200, % of the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl ours|reference]
+
+A "step" is one PW-advection evaluation (su, sv, sw from u, v, w) over the
+whole grid (configs c0-c3), or one forward-Euler step (config c4: exchange +
+fused advect/update). N=1 runs BASELINE.json configs[1] (512x512x64) by
+default. N>1 (torchrun, one rank per GPU, NCCL) runs a px x py x-y
+decomposition with a 1-cell halo exchange before each evaluation, weak
+scaling (the per-GPU block is the config's grid). Device time from CUDA events
+on the launching stream, barrier + synchronize around the timed region, max
+over ranks. Inputs (0.8-13 GB per evaluation) are larger than the 126 MB L2,
+so no L2 flush is needed between steps.
+
+Also reported (one JSON line, rank 0): the dominant kernel's roofline against
+MEASURED_PEAKS.json, the CPU oracle port timed on this host's cores
+(`cpu_baseline`), the end-to-end rate through the reference-facing C-ABI host
+path with H2D/D2H copies inside the timed region (`e2e`), our kernel launch
+count, and SM clocks sampled during the timed region.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+C restatement in oracle/, all host threads; the reference itself is
+numpy-only and cannot be compiled) on the same config and prints the same
+JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "PW advection grid points/sec (fp64)"
+UNIT = "Gpoints/s"
+BYTES_PER_POINT = 48  # 3 fp64 reads + 3 fp64 writes
+SEED = 42
+
+CONFIGS = {
+    "c0": (64, 64, 64, "BASELINE configs[0]: 64x64x64 parity case"),
+    "c1": (512, 512, 64, "BASELINE configs[1]: 512x512x64 single evaluation"),
+    "c2": (1024, 1024, 64, "BASELINE configs[2]: 1024x1024x64 evaluation"),
+    "c3": (2048, 2048, 64, "BASELINE configs[3]: 2048x2048x64 evaluation"),
+    "c4": (4096, 4096, 128, "BASELINE configs[4]: 4096x4096x128 forward-Euler step (dt=0.1)"),
+}
+
+
+def decomposition(n: int) -> tuple[int, int]:
+    """px x py for n ranks (BASELINE: 1x2, 2x2, 2x4; x = i is the slowest axis)."""
+    return {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}.get(n) or _factor(n)
+
+
+def _factor(n):
+    px = int(n ** 0.5)
+    while n % px:
+        px -= 1
+    return px, n // px
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.proc = None
+        self.index = index
+        self.window = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        threading.Thread(target=self._read, daemon=True).start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append((time.perf_counter(), parts))
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        t0, t1 = self.window or (0.0, float("inf"))
+        win = [p for (t, p) in self.samples if t0 <= t <= t1 + 0.06] or [p for _, p in self.samples]
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(p[0]) for p in win if num(p[0]) is not None]
+        reasons = sorted({name for p in win for name, v in zip(self.NAMES, p[3:7])
+                          if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": num(win[0][1]), "power_w_max": max((num(p[2]) or 0) for p in win),
+                "reasons": reasons, "samples": len(win)}
+
+
+# ---------------------------------------------------------------------------
+# helpers
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except (KeyError, ValueError):
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(key: str):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get(key)
+        except ValueError:
+            return None
+    return None
+
+
+def cpu_baseline_arm(nx, ny, nz, reps=3, max_seconds=20.0):
+    """The oracle port (C restatement, oracle/) on all host threads, min of reps."""
+    from oracle import oracle  # checker / CPU baseline only
+    import numpy as np
+    threads = oracle.host_threads()
+    # bounded sample: at most ~8.4M points (a full-column X-slab of the config)
+    sx = max(1, min(nx, (8 * 1024 * 1024) // (ny * nz)))
+    u, v, w = oracle.fill_random(sx, ny, nz, SEED, baseline=True)
+    co = oracle.baseline_coefficients(SEED, nz)
+    outs = [np.zeros_like(u) for _ in range(3)]
+    times = []
+    t_start = time.perf_counter()
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.advect_into(u, v, w, *outs, co["tcx"], co["tcy"], co["tzc1"], co["tzc2"], threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > max_seconds:
+            break
+    pts = sx * ny * nz
+    return {"value": pts / min(times) / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{sx}x{ny}x{nz} X-slab of the config grid ({pts} points), min of "
+                      f"{len(times)} reps, oracle/pwadv_oracle.c on {threads} threads "
+                      f"(X-slab engines as run_schedule), host {os.cpu_count()} cpus"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import paper_2010_01545_b200 as pw
+    from paper_2010_01545_b200 import _lib, device
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    nx, ny, nz, desc = CONFIGS[args.config]
+    px, py = decomposition(ws)
+    stepping = args.config == "c4"
+    if args.config == "c4" and ws == 1 and not args.full_c4:
+        # the 2x4 config's per-GPU block (4096/2 x 4096/4 x 128)
+        nx, ny = 2048, 1024
+        desc = "BASELINE configs[4] per-GPU block 2048x1024x128 (of 4096x4096x128 at 2x4), forward-Euler step"
+    dims = pw.make_grid(nx, ny, nz)  # per-GPU block (weak scaling)
+    opts = device.make_opts(args.variant)
+    stream = torch.cuda.current_stream(dev)
+
+    # inputs generated on the device (K5, reference LCG stream + BASELINE map)
+    gx, gy = px * nx, py * ny
+    if ws == 1:
+        fields = device.fill(dims, pw.GeneratorSpec.baseline(SEED), device=dev)
+    else:
+        from paper_2010_01545_b200 import decomp
+        dec = decomp.Decomposition(pw.make_grid(gx, gy, nz), px, py, rank)
+        fields = dec.fill_local(pw.GeneratorSpec.baseline(SEED), device=dev)
+    co = device.DeviceCoefficients.from_host(pw.baseline_coefficients(SEED, nz), dev)
+    out = device.alloc_fields(dims, dev)
+
+    if ws == 1:
+        if stepping:
+            from paper_2010_01545_b200.stepper import Stepper
+            st = Stepper(fields, co, 0.1, opts=opts)
+
+            def one_step():
+                st._one(stream)
+        else:
+            def one_step():
+                device.advect(*fields, co, out, opts=opts, stream=stream)
+    else:
+        from paper_2010_01545_b200 import decomp
+        exch = decomp.HaloExchanger(dec, dev)
+        if stepping:
+            from paper_2010_01545_b200.stepper import Stepper
+            st = Stepper(fields, co, 0.1, opts=opts,
+                         exchange=lambda f, s=None: exch.exchange(f, stream=s))
+
+            def one_step():
+                st._one(stream)
+        else:
+            def one_step():
+                exch.advect_overlapped(fields, co, out, opts=opts, stream=stream)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _lib.reset_launch_count()
+    t_host0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_host1 = time.perf_counter()
+    launches = _lib.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if sampler:
+        sampler.mark(t_host0, t_host1)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    pts_rank = dims.cells
+    value = pts_rank * ws * args.steps / (ms / 1e3) / 1e9
+
+    # dominant-kernel roofline: per-launch duration of K1/K4 alone (N=1: the
+    # step is exactly one launch; N>1: time the interior kernel separately)
+    if ws == 1 and not stepping:
+        kern_ms = ms_step
+    else:
+        torch.cuda.synchronize()
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nk = max(5, min(args.steps, 50))
+        k0.record(stream)
+        for _ in range(nk):
+            if stepping:
+                device.step(*fields, co, 0.1, out, opts=opts, stream=stream)
+            else:
+                device.advect(*fields, co, out, opts=opts, stream=stream)
+        k1.record(stream)
+        torch.cuda.synchronize()
+        kern_ms = k0.elapsed_time(k1) / nk
+    peak, peak_src = measured_peak()
+    achieved = BYTES_PER_POINT * pts_rank / (kern_ms / 1e3) / 1e9
+    key = f"{args.config}:{args.variant}:{nx}x{ny}x{nz}"
+    traffic = ncu_traffic(key)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": peak_src, "kernel_ms": round(kern_ms, 5),
+                "algorithmic_bytes_per_launch": BYTES_PER_POINT * pts_rank,
+                "bytes_per_point": BYTES_PER_POINT,
+                "frac_of_8TBs_spec": round(achieved / 8000.0, 4)}
+
+    # parity spot check of the timed output (bounded: two X slabs vs oracle)
+    parity = None
+    if rank == 0 and ws == 1 and not stepping:
+        from oracle import oracle  # checker only
+        ok = True
+        for x0, x1 in ((1, 3), (dims.nx - 1, dims.nx + 1)):
+            ins = [f[x0 - 1:x1 + 1].cpu().numpy() for f in fields]
+            want = oracle.advect(*ins, co.tcx, co.tcy, co.tz[0].cpu().numpy(), co.tz[1].cpu().numpy(),
+                                 engines=oracle.host_threads())
+            for o, wnt in zip(out, want):
+                ok &= o[x0:x1].cpu().numpy().tobytes() == wnt[1:-1].tobytes()
+        parity = {"bitwise_equal_slabs": bool(ok), "checked": "planes 1-2 and nx-1..nx vs oracle"}
+
+    clocks = sampler.stop() if sampler else None
+
+    # end-to-end through the reference-facing C-ABI host path (N=1)
+    e2e = None
+    if ws == 1 and not stepping and not args.no_e2e:
+        ctx = device.HostContext(dims, local)
+        hin = [torch.empty(dims.padded_shape, dtype=torch.float64, pin_memory=True) for _ in range(3)]
+        hout = [torch.empty(dims.padded_shape, dtype=torch.float64, pin_memory=True) for _ in range(3)]
+        for h, f in zip(hin, fields):
+            h.copy_(f)
+        tz = [co.tz[0].cpu().numpy(), co.tz[1].cpu().numpy()]
+        ke = max(3, min(args.steps, args.e2e_steps))
+        for _ in range(2):
+            ctx.advect_host(*hin, *hout, co.tcx, co.tcy, *tz, chunks=args.chunks)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            h2d, d2h = ctx.advect_host(*hin, *hout, co.tcx, co.tcy, *tz, chunks=args.chunks)
+        t1 = time.perf_counter()
+        ctx.close()
+        same = all(torch.equal(a.view(torch.int64), b.cpu().view(torch.int64)) for a, b in zip(hout, out))
+        e2e = {"value": dims.cells * ke / (t1 - t0) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": ke, "chunks": args.chunks,
+               "api": "pwadv_ctx_advect_host (C ABI; pinned host buffers; H2D/K1/D2H pipelined)",
+               "bitwise_equal_to_device_run": bool(same)}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_baseline_arm(nx, ny, nz)
+
+    if rank == 0:
+        plan = device.describe_plan(dims, None, opts, local)
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: reference Knuth-MMIX LCG stream (seed 42) mapped to [-10,10], "
+                    "w=0 at k=0 and k=nz-1, tzc in [1e-3,5e-3), tcx=tcy=0.005 (BASELINE.json)",
+            "config": {"workload": desc, "nx": nx, "ny": ny, "nz": nz,
+                       "global_grid": f"{gx}x{gy}x{nz}", "points_per_gpu": pts_rank,
+                       "decomposition": f"{px}x{py}", "variant": args.variant,
+                       "bit_exact": not args.variant.endswith("_fma"),
+                       "l2": f"inputs larger than L2 ({3 * dims.padded_len * 8 / 1e6:.0f} MB read per "
+                             f"step vs 126 MB L2); no flush", "plan": plan},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks, "parity": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    nx, ny, nz, desc = CONFIGS[args.config]
+    from oracle import oracle  # the reference algorithm's CPU implementation (port)
+    import numpy as np
+    threads = oracle.host_threads()
+    sx = max(1, min(nx, (8 * 1024 * 1024) // (ny * nz)))  # bounded X-slab sample
+    u, v, w = oracle.fill_random(sx, ny, nz, SEED, baseline=True)
+    co = oracle.baseline_coefficients(SEED, nz)
+    outs = [np.zeros_like(u) for _ in range(3)]
+    run = lambda: oracle.advect_into(u, v, w, *outs, co["tcx"], co["tcy"], co["tzc1"], co["tzc2"], threads)  # noqa: E731
+    for _ in range(min(args.warmup, 2)):
+        run()
+    steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run()
+    dt = time.perf_counter() - t0
+    pts = sx * ny * nz
+    value = pts * steps / dt / 1e9
+    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": ws, "steps": steps,
+            "warmup": min(args.warmup, 2), "ms_per_step": round(dt / steps * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (same generator as our arm)", "impl": "reference",
+            "config": {"workload": desc, "nx": nx, "ny": ny, "nz": nz, "sample_nx": sx},
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{sx}x{ny}x{nz} X-slab per step ({pts} points), "
+                                       "oracle/pwadv_oracle.c (C restatement of the numpy reference, "
+                                       "which cannot be compiled), X-slab engine threads"},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--variant", default="xmarch",
+                    choices=("xmarch", "simple", "xmarch_fma", "simple_fma"))
+    ap.add_argument("--chunks", type=int, default=16, help="X-slab chunks of the e2e pipeline")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--full-c4", action="store_true", help="c4 on one GPU at the full 4096x4096x128")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

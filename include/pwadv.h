@@ -1,0 +1,185 @@
+/*
+ * pwadv.h — C ABI of the B200-native PW-advection hot path (libpwadv.so).
+ *
+ * This is the drop-in boundary for the reference's hot path (pwadvect 0.1.0,
+ * /root/reference). The reference has no FFI of its own: its
+ * interface is the Python function
+ *     run_reference(fields: FieldSet, coeffs: AdvectionCoefficients) -> SourceSet
+ * (pkg/src/pwadvect/kernel.py:175-185) and the dispatcher
+ *     run_schedule(fields, coeffs, ScheduleSpec) -> (SourceSet, TrafficReport, wall)
+ * (pkg/src/pwadvect/schedules.py:207-232). The entry points below are what a
+ * ctypes/cffi binding of that interface calls; the Python mirror in
+ * paper_2010_01545_b200/ (and INTEGRATION.md) shows the binding.
+ *
+ * Data contract (pkg/src/pwadvect/grid.py:30-130, docs/model-notes.md §1):
+ *   every field is a C-order float64 array of shape (nx+2, ny+2, nz), k fastest,
+ *   halo width 1 in X and Y only; flat offset of [i, j, k] = (i*(ny+2)+j)*nz + k.
+ *   Outputs su/sv/sw: interior columns are written at every level (level 0 is
+ *   +0.0, kernel.py:151); halo columns are never written (the caller zeroes the
+ *   output buffers once, as zeros_sources does, grid.py:129-130).
+ *
+ * Conventions:
+ *   - All functions return 0 on success or a negative PWADV_E* code; the
+ *     message of the last failure on the calling thread is pwadv_last_error().
+ *   - Device-pointer functions are asynchronous on `stream` (a cudaStream_t;
+ *     NULL = legacy default stream) and never retain caller memory.
+ *   - No global mutable state besides a lazily initialised per-device attribute
+ *     cache; safe to call from several host threads on different streams/devices.
+ *   - Arithmetic is bit-exact with the reference (IEEE binary64, no FMA
+ *     contraction, the reference's association order)
+ *     unless PWADV_FLAG_FMA is passed.
+ */
+#ifndef PWADV_H_
+#define PWADV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PWADV_ABI_VERSION 1
+
+enum {
+    PWADV_OK = 0,
+    PWADV_E_DIMS = -1,      /* nx < 1, ny < 1 or nz < 2 (grid.py:52-58 GridError) */
+    PWADV_E_NULL = -2,      /* null pointer argument */
+    PWADV_E_RANGE = -3,     /* sub-box outside the interior / bad slab */
+    PWADV_E_CUDA = -4,      /* CUDA launch or runtime error */
+    PWADV_E_ARG = -5,       /* other invalid argument (mode, tuning) */
+    PWADV_E_ALIGN = -6      /* pointer not 8-byte aligned */
+};
+
+/* flags for pwadv_opts.flags */
+#define PWADV_FLAG_FMA 1u           /* contract into DFMA (not bit-exact; <=1e-12 normwise) */
+#define PWADV_FLAG_SIMPLE 2u        /* force the one-thread-per-point kernel */
+#define PWADV_FLAG_NO_STREAMING 4u  /* plain stores instead of st.global.cs */
+
+/* Optional tuning / variant selection; pass NULL for defaults. */
+typedef struct pwadv_opts {
+    uint32_t flags;
+    int32_t tile_j;        /* columns per CTA strip for the X-march kernel (0 = auto) */
+    int32_t stages;        /* smem plane-ring depth (0 = auto) */
+    int32_t grid;          /* CTAs (0 = auto: SMs x resident CTAs) */
+    int32_t max_threads;   /* X-march CTA thread budget: 512, 384 or 256 (0 = auto) */
+} pwadv_opts;
+
+int pwadv_abi_version(void);
+const char *pwadv_last_error(void);
+
+/* Launch-count instrumentation: kernels launched by this library on the
+ * calling thread since the last reset (bench.py reports it as gpu_launches). */
+uint64_t pwadv_launch_count(void);
+void pwadv_reset_launch_count(void);
+
+/*
+ * K1 — one PW-advection evaluation, device pointers, whole interior.
+ * Replaces run_reference (kernel.py:175-185) -> compute_block (:139-162) ->
+ * su/sv/sw_formula (:73-112). tzc1/tzc2: device arrays of nz doubles.
+ */
+int pwadv_advect_f64(const double *u, const double *v, const double *w,
+                     double *su, double *sv, double *sw,
+                     int64_t nx, int64_t ny, int64_t nz,
+                     double tcx, double tcy,
+                     const double *tzc1, const double *tzc2,
+                     const pwadv_opts *opts, void *stream);
+
+/*
+ * K1 on a sub-box of interior columns: i in [x_begin, x_end), j in
+ * [y_begin, y_end) (1-based interior indices, as Slab in schedules.py:53-62).
+ * The reference's X-slab engine (schedules.py:131-135, 194-204) is the case
+ * y_begin=1, y_end=ny+1. Used for the interior/rim split of the multi-GPU
+ * overlap.
+ */
+int pwadv_advect_box_f64(const double *u, const double *v, const double *w,
+                         double *su, double *sv, double *sw,
+                         int64_t nx, int64_t ny, int64_t nz,
+                         double tcx, double tcy,
+                         const double *tzc1, const double *tzc2,
+                         int64_t x_begin, int64_t x_end, int64_t y_begin, int64_t y_end,
+                         const pwadv_opts *opts, void *stream);
+
+/* Launch plan the library would use for K1 on this box (for reports/benches). */
+typedef struct pwadv_plan_info {
+    int32_t kernel;        /* 1 = X-march (bulk-copy plane ring), 2 = one-thread-per-point */
+    int32_t tile_j, threads_per_column, stages, threads, grid;
+    int64_t smem_bytes, strips;
+} pwadv_plan_info;
+int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz,
+                        int64_t x_begin, int64_t x_end, int64_t y_begin, int64_t y_end,
+                        const pwadv_opts *opts, int device, pwadv_plan_info *out);
+
+/*
+ * K4 — fused forward step on a sub-box: f_new = f + dt*s_f (mul then add) for
+ * f in {u, v, w}, with s computed as K1 from (u, v, w). Writes interior
+ * columns of u_new/v_new/w_new in the box (all levels); halos are not written
+ * (wrap or exchange afterwards). No reference counterpart; the
+ * composed oracle is run_reference + numpy f + dt*s + wrap_halos.
+ */
+int pwadv_step_box_f64(const double *u, const double *v, const double *w,
+                       double *u_new, double *v_new, double *w_new,
+                       int64_t nx, int64_t ny, int64_t nz,
+                       double tcx, double tcy,
+                       const double *tzc1, const double *tzc2, double dt,
+                       int64_t x_begin, int64_t x_end, int64_t y_begin, int64_t y_end,
+                       const pwadv_opts *opts, void *stream);
+
+/* K2 — periodic halo wrap in place (grid.py:203-208: X then Y semantics). */
+int pwadv_wrap_halos_f64(double *f, int64_t nx, int64_t ny, int64_t nz, void *stream);
+/* K2 on three fields in one launch. */
+int pwadv_wrap_halos3_f64(double *u, double *v, double *w,
+                          int64_t nx, int64_t ny, int64_t nz, void *stream);
+
+/*
+ * K5 — device field generator (grid.py:133-239), bit-identical to the
+ * reference's fill_fields. Fills the interiors of u, v, w and wraps halos.
+ *   mode 0: GeneratorSpec.random(seed): one Knuth-MMIX LCG stream, u then v
+ *           then w interior in C order, value (state>>11)*2^-53.
+ *   mode 1: BASELINE.json distribution: mode 0 value x mapped
+ *           to x*20.0-10.0 (no FMA); w = 0 at levels 0 and nz-1.
+ *   mode 2: GeneratorSpec.uniform(a, b, c): u=a, v=b, w=c everywhere.
+ */
+int pwadv_fill_f64(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
+                   int32_t mode, uint64_t seed, double a, double b, double c, void *stream);
+
+/* Halo exchange helpers (multi-GPU x-y decomposition).
+ * Y faces are (nx+2) runs of nz doubles at stride (ny+2)*nz: pack the column
+ * j (all i in 0..nx+1) of u, v, w into buf[3][nx+2][nz], or unpack into it. */
+int pwadv_pack_yface3_f64(const double *u, const double *v, const double *w, double *buf,
+                          int64_t nx, int64_t ny, int64_t nz, int64_t j, void *stream);
+int pwadv_unpack_yface3_f64(double *u, double *v, double *w, const double *buf,
+                            int64_t nx, int64_t ny, int64_t nz, int64_t j, void *stream);
+/* X faces: plane i (all j in 0..ny+1) of u, v, w <-> buf[3][ny+2][nz]. */
+int pwadv_pack_xface3_f64(const double *u, const double *v, const double *w, double *buf,
+                          int64_t nx, int64_t ny, int64_t nz, int64_t i, void *stream);
+int pwadv_unpack_xface3_f64(double *u, double *v, double *w, const double *buf,
+                            int64_t nx, int64_t ny, int64_t nz, int64_t i, void *stream);
+/* Local periodic copy of one axis (an undivided axis of the decomposition):
+ * axis 0 = X faces (planes), axis 1 = Y faces (columns, all i incl. halos). */
+int pwadv_wrap_axis3_f64(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
+                         int32_t axis, void *stream);
+
+/*
+ * Host-buffer entry (end-to-end drop-in): u/v/w/su/sv/sw/tzc1/tzc2 are HOST
+ * pointers (pinned or pageable). The context owns device buffers for one grid
+ * shape and three streams; the call pipelines X-slab chunks so the H2D copy of
+ * chunk c+1, the K1 launch on chunk c and the D2H copy of chunk c-1 overlap
+ * (the paper's proposed future work). Synchronous: returns after
+ * the outputs are in host memory. Output halos and level 0 are +0.0.
+ */
+typedef struct pwadv_ctx pwadv_ctx;
+int pwadv_ctx_create(pwadv_ctx **out, int device, int64_t nx, int64_t ny, int64_t nz);
+int pwadv_ctx_destroy(pwadv_ctx *ctx);
+int pwadv_ctx_advect_host(pwadv_ctx *ctx,
+                          const double *u, const double *v, const double *w,
+                          double *su, double *sv, double *sw,
+                          double tcx, double tcy, const double *tzc1, const double *tzc2,
+                          int32_t chunks, const pwadv_opts *opts);
+/* Bytes moved host->device and device->host by the last ctx_advect_host call. */
+int pwadv_ctx_last_bytes(const pwadv_ctx *ctx, uint64_t *h2d, uint64_t *d2h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PWADV_H_ */

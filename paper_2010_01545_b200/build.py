@@ -1,0 +1,63 @@
+"""Build libpwadv.so in-tree with nvcc for sm_100a (no JIT cache, travels with gpurun)."""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libpwadv.so"
+SOURCES = ["pwadv_advect.cu", "pwadv_aux.cu", "pwadv_api.cu"]
+HEADERS = ["pwadv_device.cuh", "pwadv_internal.h"]
+
+
+def nvcc_path() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def nvcc_flags(verbose: bool = False) -> list[str]:
+    flags = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+             # bit-exact build: no FMA contraction anywhere (the formulas use
+             # explicit __d*_rn intrinsics as well; the FMA variant uses
+             # explicit __fma_rn and is selected at run time)
+             "--fmad=false",
+             "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+             "-I", str(PKG.parent / "include")]
+    if verbose:
+        flags += ["-Xptxas", "-v"]
+    return flags
+
+
+def stale() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [PKG.parent / "include" / "pwadv.h"]
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not stale():
+        return LIB
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [nvcc_path(), *nvcc_flags(verbose), "-shared", "-o", str(tmp),
+           *[str(CSRC / s) for s in SOURCES]]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    print(LIB)

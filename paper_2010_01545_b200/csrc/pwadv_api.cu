@@ -1,0 +1,437 @@
+// pwadv_api.cu — the extern "C" boundary of libpwadv.so (include/pwadv.h).
+//
+// Argument checks mirror the reference's error behaviour so the Python shim can
+// raise the same exceptions (GridError/ValueError before any compute,
+// grid.py:52-58, kernel.py:178-179, schedules.py:65-68); here they come back
+// as negative codes with a message in pwadv_last_error().
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "pwadv_internal.h"
+
+namespace pwadv {
+
+static thread_local char g_err[512] = "";
+static thread_local uint64_t g_launches = 0;
+
+int set_error(int code, const char *fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int set_cuda_error(const char *what, cudaError_t e)
+{
+    return set_error(PWADV_E_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+void count_launch() { ++g_launches; }
+
+static constexpr int kMaxDevices = 64;
+static DeviceInfo g_devs[kMaxDevices];
+static std::once_flag g_dev_once[kMaxDevices];
+
+const DeviceInfo *device_info()
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return nullptr;
+    std::call_once(g_dev_once[dev], [dev]() {
+        DeviceInfo d;
+        d.device = dev;
+        d.sms = 148;
+        d.smem_optin = 227 * 1024;
+        cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        g_devs[dev] = d;
+    });
+    return &g_devs[dev];
+}
+
+static int check_dims(int64_t nx, int64_t ny, int64_t nz)
+{
+    if (nx < 1 || ny < 1)
+        return set_error(PWADV_E_DIMS, "horizontal extents must be >= 1, got %lldx%lld",
+                         (long long)nx, (long long)ny);
+    if (nz < 2)
+        return set_error(PWADV_E_DIMS, "nz must be >= 2 (column stencil starts at k=2), got %lld",
+                         (long long)nz);
+    return PWADV_OK;
+}
+
+static int check_ptrs(std::initializer_list<const void *> ps)
+{
+    for (const void *p : ps) {
+        if (!p) return set_error(PWADV_E_NULL, "null pointer argument");
+        if ((uintptr_t)p & 7) return set_error(PWADV_E_ALIGN, "pointer %p is not 8-byte aligned", p);
+    }
+    return PWADV_OK;
+}
+
+static int run_box(const double *u, const double *v, const double *w, double *o0, double *o1,
+                   double *o2, int64_t nx, int64_t ny, int64_t nz, double tcx, double tcy,
+                   const double *tzc1, const double *tzc2, double dt, bool step, int64_t x0,
+                   int64_t x1, int64_t y0, int64_t y1, const pwadv_opts *opts, void *stream)
+{
+    int rc = check_dims(nx, ny, nz);
+    if (rc) return rc;
+    rc = check_ptrs({u, v, w, o0, o1, o2, tzc1, tzc2});
+    if (rc) return rc;
+    if (x0 < 1 || x1 > nx + 1 || x0 > x1 || y0 < 1 || y1 > ny + 1 || y0 > y1)
+        return set_error(PWADV_E_RANGE, "box [%lld,%lld)x[%lld,%lld) outside interior %lldx%lld",
+                         (long long)x0, (long long)x1, (long long)y0, (long long)y1,
+                         (long long)nx, (long long)ny);
+    BoxLaunch L;
+    L.u = u;
+    L.v = v;
+    L.w = w;
+    L.o0 = o0;
+    L.o1 = o1;
+    L.o2 = o2;
+    L.tzc1 = tzc1;
+    L.tzc2 = tzc2;
+    L.nx = nx;
+    L.ny = ny;
+    L.nz = nz;
+    L.tcx = tcx;
+    L.tcy = tcy;
+    L.dt = dt;
+    L.x0 = x0;
+    L.x1 = x1;
+    L.y0 = y0;
+    L.y1 = y1;
+    L.step = step;
+    L.flags = opts ? opts->flags : 0u;
+    L.tile_j = opts ? opts->tile_j : 0;
+    L.stages = opts ? opts->stages : 0;
+    L.grid = opts ? opts->grid : 0;
+    L.max_threads = opts ? opts->max_threads : 0;
+    if (L.tile_j < 0 || L.stages < 0 || L.grid < 0 || L.max_threads < 0)
+        return set_error(PWADV_E_ARG, "negative tuning value");
+    return launch_box(L, (cudaStream_t)stream);
+}
+
+}  // namespace pwadv
+
+using namespace pwadv;
+
+namespace {
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+}  // namespace
+
+extern "C" {
+
+int pwadv_abi_version(void) { return PWADV_ABI_VERSION; }
+const char *pwadv_last_error(void) { return g_err; }
+uint64_t pwadv_launch_count(void) { return g_launches; }
+void pwadv_reset_launch_count(void) { g_launches = 0; }
+
+int pwadv_advect_f64(const double *u, const double *v, const double *w, double *su, double *sv,
+                     double *sw, int64_t nx, int64_t ny, int64_t nz, double tcx, double tcy,
+                     const double *tzc1, const double *tzc2, const pwadv_opts *opts, void *stream)
+{
+    return run_box(u, v, w, su, sv, sw, nx, ny, nz, tcx, tcy, tzc1, tzc2, 0.0, false, 1, nx + 1,
+                   1, ny + 1, opts, stream);
+}
+
+int pwadv_advect_box_f64(const double *u, const double *v, const double *w, double *su,
+                         double *sv, double *sw, int64_t nx, int64_t ny, int64_t nz, double tcx,
+                         double tcy, const double *tzc1, const double *tzc2, int64_t x_begin,
+                         int64_t x_end, int64_t y_begin, int64_t y_end, const pwadv_opts *opts,
+                         void *stream)
+{
+    return run_box(u, v, w, su, sv, sw, nx, ny, nz, tcx, tcy, tzc1, tzc2, 0.0, false, x_begin,
+                   x_end, y_begin, y_end, opts, stream);
+}
+
+int pwadv_step_box_f64(const double *u, const double *v, const double *w, double *u_new,
+                       double *v_new, double *w_new, int64_t nx, int64_t ny, int64_t nz,
+                       double tcx, double tcy, const double *tzc1, const double *tzc2, double dt,
+                       int64_t x_begin, int64_t x_end, int64_t y_begin, int64_t y_end,
+                       const pwadv_opts *opts, void *stream)
+{
+    if (u == u_new || v == v_new || w == w_new)
+        return set_error(PWADV_E_ARG, "fused step needs distinct (ping-pong) output buffers");
+    return run_box(u, v, w, u_new, v_new, w_new, nx, ny, nz, tcx, tcy, tzc1, tzc2, dt, true,
+                   x_begin, x_end, y_begin, y_end, opts, stream);
+}
+
+int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz, int64_t x0, int64_t x1, int64_t y0,
+                        int64_t y1, const pwadv_opts *opts, int device, pwadv_plan_info *out)
+{
+    int rc = check_dims(nx, ny, nz);
+    if (rc) return rc;
+    if (!out) return set_error(PWADV_E_NULL, "null out");
+    DeviceGuard g(device);
+    const DeviceInfo *dev = device_info();
+    if (!dev) return set_error(PWADV_E_CUDA, "no CUDA device");
+    BoxLaunch L{};
+    // nominal 256-byte aligned pointers: the plan only depends on alignment
+    L.u = L.v = L.w = reinterpret_cast<const double *>(256);
+    L.o0 = L.o1 = L.o2 = reinterpret_cast<double *>(256);
+    L.nx = nx;
+    L.ny = ny;
+    L.nz = nz;
+    L.x0 = x0;
+    L.x1 = x1;
+    L.y0 = y0;
+    L.y1 = y1;
+    L.flags = opts ? opts->flags : 0u;
+    L.tile_j = opts ? opts->tile_j : 0;
+    L.stages = opts ? opts->stages : 0;
+    L.grid = opts ? opts->grid : 0;
+    L.max_threads = opts ? opts->max_threads : 0;
+    XmarchPlan p{};
+    *out = pwadv_plan_info{};
+    if (plan_xmarch(L, *dev, &p)) {
+        out->kernel = 1;
+        out->tile_j = p.tj;
+        out->threads_per_column = p.kp;
+        out->stages = p.stages;
+        out->threads = p.threads;
+        out->grid = p.grid;
+        out->smem_bytes = (int64_t)p.smem;
+        out->strips = p.nstrips;
+    } else {
+        out->kernel = 2;
+        out->threads = 256;
+    }
+    return PWADV_OK;
+}
+
+int pwadv_wrap_halos_f64(double *f, int64_t nx, int64_t ny, int64_t nz, void *stream)
+{
+    int rc = check_dims(nx, ny, nz);
+    if (rc) return rc;
+    if ((rc = check_ptrs({f}))) return rc;
+    return launch_wrap3(f, nullptr, nullptr, 1, nx, ny, nz, (cudaStream_t)stream);
+}
+
+int pwadv_wrap_halos3_f64(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
+                          void *stream)
+{
+    int rc = check_dims(nx, ny, nz);
+    if (rc) return rc;
+    if ((rc = check_ptrs({u, v, w}))) return rc;
+    return launch_wrap3(u, v, w, 3, nx, ny, nz, (cudaStream_t)stream);
+}
+
+int pwadv_wrap_axis3_f64(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
+                         int32_t axis, void *stream)
+{
+    int rc = check_dims(nx, ny, nz);
+    if (rc) return rc;
+    if ((rc = check_ptrs({u, v, w}))) return rc;
+    if (axis != 0 && axis != 1) return set_error(PWADV_E_ARG, "axis must be 0 or 1");
+    return launch_wrap_axis3(u, v, w, nx, ny, nz, axis, (cudaStream_t)stream);
+}
+
+int pwadv_fill_f64(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
+                   int32_t mode, uint64_t seed, double a, double b, double c, void *stream)
+{
+    int rc = check_dims(nx, ny, nz);
+    if (rc) return rc;
+    if ((rc = check_ptrs({u, v, w}))) return rc;
+    if (mode < 0 || mode > 2) return set_error(PWADV_E_ARG, "unknown generator mode %d", mode);
+    return launch_fill(u, v, w, nx, ny, nz, mode, seed, a, b, c, (cudaStream_t)stream);
+}
+
+static int face(const double *u, const double *v, const double *w, double *buf, int64_t nx,
+                int64_t ny, int64_t nz, int axis, int64_t index, bool pack, void *stream)
+{
+    int rc = check_dims(nx, ny, nz);
+    if (rc) return rc;
+    if ((rc = check_ptrs({u, v, w, buf}))) return rc;
+    const int64_t lim = axis == 0 ? nx + 1 : ny + 1;
+    if (index < 0 || index > lim)
+        return set_error(PWADV_E_RANGE, "face index %lld outside 0..%lld", (long long)index,
+                         (long long)lim);
+    return launch_face3(const_cast<double *>(u), const_cast<double *>(v), const_cast<double *>(w),
+                        buf, nx, ny, nz, axis, index, pack, (cudaStream_t)stream);
+}
+
+int pwadv_pack_yface3_f64(const double *u, const double *v, const double *w, double *buf,
+                          int64_t nx, int64_t ny, int64_t nz, int64_t j, void *stream)
+{
+    return face(u, v, w, buf, nx, ny, nz, 1, j, true, stream);
+}
+
+int pwadv_unpack_yface3_f64(double *u, double *v, double *w, const double *buf, int64_t nx,
+                            int64_t ny, int64_t nz, int64_t j, void *stream)
+{
+    return face(u, v, w, const_cast<double *>(buf), nx, ny, nz, 1, j, false, stream);
+}
+
+int pwadv_pack_xface3_f64(const double *u, const double *v, const double *w, double *buf,
+                          int64_t nx, int64_t ny, int64_t nz, int64_t i, void *stream)
+{
+    return face(u, v, w, buf, nx, ny, nz, 0, i, true, stream);
+}
+
+int pwadv_unpack_xface3_f64(double *u, double *v, double *w, const double *buf, int64_t nx,
+                            int64_t ny, int64_t nz, int64_t i, void *stream)
+{
+    return face(u, v, w, const_cast<double *>(buf), nx, ny, nz, 0, i, false, stream);
+}
+
+// ---------------------------------------------------------------------------
+// host-buffer context: pipelined H2D / K1 / D2H over X-slab chunks
+
+struct pwadv_ctx {
+    int device;
+    int64_t nx, ny, nz;
+    double *d_in[3];
+    double *d_out[3];
+    double *d_tz;
+    cudaStream_t s_h2d, s_cmp, s_d2h;
+    std::vector<cudaEvent_t> ev_in, ev_cmp;
+    uint64_t last_h2d, last_d2h;
+};
+
+
+int pwadv_ctx_create(pwadv_ctx **out, int device, int64_t nx, int64_t ny, int64_t nz)
+{
+    if (!out) return set_error(PWADV_E_NULL, "null ctx out pointer");
+    *out = nullptr;
+    int rc = check_dims(nx, ny, nz);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    pwadv_ctx *c = new pwadv_ctx();
+    c->device = device;
+    c->nx = nx;
+    c->ny = ny;
+    c->nz = nz;
+    const size_t n = (size_t)(nx + 2) * (ny + 2) * nz;
+    cudaError_t e = cudaSuccess;
+    for (int m = 0; m < 3 && e == cudaSuccess; ++m) e = cudaMalloc(&c->d_in[m], n * sizeof(double));
+    for (int m = 0; m < 3 && e == cudaSuccess; ++m) e = cudaMalloc(&c->d_out[m], n * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_tz, 2 * (size_t)nz * sizeof(double));
+    for (int m = 0; m < 3 && e == cudaSuccess; ++m) e = cudaMemset(c->d_out[m], 0, n * sizeof(double));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_cmp, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        pwadv_ctx_destroy(c);
+        return set_cuda_error("pwadv_ctx_create", e);
+    }
+    *out = c;
+    return PWADV_OK;
+}
+
+int pwadv_ctx_destroy(pwadv_ctx *c)
+{
+    if (!c) return PWADV_OK;
+    DeviceGuard g(c->device);
+    for (int m = 0; m < 3; ++m) {
+        if (c->d_in[m]) cudaFree(c->d_in[m]);
+        if (c->d_out[m]) cudaFree(c->d_out[m]);
+    }
+    if (c->d_tz) cudaFree(c->d_tz);
+    if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+    if (c->s_cmp) cudaStreamDestroy(c->s_cmp);
+    if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+    for (auto ev : c->ev_in) cudaEventDestroy(ev);
+    for (auto ev : c->ev_cmp) cudaEventDestroy(ev);
+    delete c;
+    return PWADV_OK;
+}
+
+int pwadv_ctx_last_bytes(const pwadv_ctx *c, uint64_t *h2d, uint64_t *d2h)
+{
+    if (!c || !h2d || !d2h) return set_error(PWADV_E_NULL, "null argument");
+    *h2d = c->last_h2d;
+    *d2h = c->last_d2h;
+    return PWADV_OK;
+}
+
+int pwadv_ctx_advect_host(pwadv_ctx *c, const double *u, const double *v, const double *w,
+                          double *su, double *sv, double *sw, double tcx, double tcy,
+                          const double *tzc1, const double *tzc2, int32_t chunks,
+                          const pwadv_opts *opts)
+{
+    if (!c) return set_error(PWADV_E_NULL, "null ctx");
+    if (!u || !v || !w || !su || !sv || !sw || !tzc1 || !tzc2)
+        return set_error(PWADV_E_NULL, "null pointer argument");
+    DeviceGuard g(c->device);
+    const int64_t nx = c->nx, ny = c->ny, nz = c->nz;
+    if (chunks < 1) chunks = 1;
+    if (chunks > nx) chunks = (int32_t)nx;
+    while ((int)c->ev_in.size() < chunks) {
+        cudaEvent_t a, b;
+        cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+        c->ev_in.push_back(a);
+        c->ev_cmp.push_back(b);
+    }
+    const size_t plane = (size_t)(ny + 2) * nz;  // doubles per i-plane
+    const size_t pb = plane * sizeof(double);
+    const double *hin[3] = {u, v, w};
+    double *hout[3] = {su, sv, sw};
+    uint64_t h2d = 0, d2h = 0;
+    cudaError_t e;
+    e = cudaMemcpyAsync(c->d_tz, tzc1, nz * sizeof(double), cudaMemcpyHostToDevice, c->s_h2d);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(c->d_tz + nz, tzc2, nz * sizeof(double), cudaMemcpyHostToDevice,
+                            c->s_h2d);
+    if (e != cudaSuccess) return set_cuda_error("coefficient upload", e);
+    h2d += 2 * nz * sizeof(double);
+    pwadv_opts o = opts ? *opts : pwadv_opts{0u, 0, 0, 0, 0};
+    int64_t copied = 0;  // input planes [0, copied) are on the device
+    int64_t base = nx / chunks, rem = nx % chunks, x = 1;
+    for (int ch = 0; ch < chunks; ++ch) {
+        const int64_t x0 = x, x1 = x + base + (ch < rem ? 1 : 0);
+        x = x1;
+        const int64_t need = (ch == chunks - 1) ? nx + 2 : x1 + 1;  // planes up to x1 inclusive
+        if (need > copied) {
+            for (int m = 0; m < 3; ++m) {
+                e = cudaMemcpyAsync(c->d_in[m] + copied * plane, hin[m] + copied * plane,
+                                    (need - copied) * pb, cudaMemcpyHostToDevice, c->s_h2d);
+                if (e != cudaSuccess) return set_cuda_error("H2D", e);
+            }
+            h2d += 3 * (uint64_t)(need - copied) * pb;
+            copied = need;
+        }
+        cudaEventRecord(c->ev_in[ch], c->s_h2d);
+        cudaStreamWaitEvent(c->s_cmp, c->ev_in[ch], 0);
+        int rc = pwadv_advect_box_f64(c->d_in[0], c->d_in[1], c->d_in[2], c->d_out[0],
+                                      c->d_out[1], c->d_out[2], nx, ny, nz, tcx, tcy, c->d_tz,
+                                      c->d_tz + nz, x0, x1, 1, ny + 1, &o, c->s_cmp);
+        if (rc) return rc;
+        cudaEventRecord(c->ev_cmp[ch], c->s_cmp);
+        cudaStreamWaitEvent(c->s_d2h, c->ev_cmp[ch], 0);
+        // output planes of this chunk; the first/last chunk also returns the
+        // all-zero halo planes 0 / nx+1 so host outputs match zeros_sources
+        const int64_t o0 = (ch == 0) ? 0 : x0;
+        const int64_t o1 = (ch == chunks - 1) ? nx + 2 : x1;
+        for (int m = 0; m < 3; ++m) {
+            e = cudaMemcpyAsync(hout[m] + o0 * plane, c->d_out[m] + o0 * plane, (o1 - o0) * pb,
+                                cudaMemcpyDeviceToHost, c->s_d2h);
+            if (e != cudaSuccess) return set_cuda_error("D2H", e);
+        }
+        d2h += 3 * (uint64_t)(o1 - o0) * pb;
+    }
+    e = cudaStreamSynchronize(c->s_d2h);
+    if (e != cudaSuccess) return set_cuda_error("ctx_advect_host sync", e);
+    c->last_h2d = h2d;
+    c->last_d2h = d2h;
+    return PWADV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// pwadv_internal.h — shared declarations between the libpwadv translation units.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/pwadv.h"
+
+namespace pwadv {
+
+struct DeviceInfo {
+    int device;
+    int sms;
+    int smem_optin;
+};
+
+// One K1/K4 launch over an interior box.
+struct BoxLaunch {
+    const double *u, *v, *w;
+    double *o0, *o1, *o2;
+    const double *tzc1, *tzc2;
+    int64_t nx, ny, nz;
+    double tcx, tcy, dt;
+    int64_t x0, x1, y0, y1;
+    bool step;
+    uint32_t flags;
+    int tile_j, stages, grid, max_threads;
+};
+
+struct XmarchPlan {
+    int maxt, tj, kp, stages, threads, grid;
+    size_t smem;
+    int64_t nstrips;
+};
+
+// cached attributes of the current device (lazily filled, thread-safe)
+const DeviceInfo *device_info();
+
+int set_error(int code, const char *fmt, ...);
+int set_cuda_error(const char *what, cudaError_t e);
+void count_launch();
+
+bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p);
+int launch_box(const BoxLaunch &L, cudaStream_t stream);
+
+// auxiliary kernels (pwadv_aux.cu)
+int launch_wrap3(double *u, double *v, double *w, int nf, int64_t nx, int64_t ny, int64_t nz,
+                 cudaStream_t s);
+int launch_wrap_axis3(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
+                      int axis, cudaStream_t s);
+int launch_fill(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz, int mode,
+                uint64_t seed, double a, double b, double c, cudaStream_t s);
+int launch_face3(double *u, double *v, double *w, double *buf, int64_t nx, int64_t ny,
+                 int64_t nz, int axis, int64_t index, bool pack, cudaStream_t s);
+
+}  // namespace pwadv

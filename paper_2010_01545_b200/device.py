@@ -1,0 +1,259 @@
+"""Device-resident API: the hot path on torch CUDA tensors, no host copies.
+
+Fields are torch.float64 CUDA tensors of shape (nx+2, ny+2, nz), C-contiguous,
+k fastest — byte-for-byte the reference's `Field3D.data` layout
+(pkg/src/pwadvect/grid.py:61-88), so there are no transposes at the boundary.
+torch only allocates memory and supplies streams; every kernel is ours
+(libpwadv.so through `_lib`). This is the API the benchmark times.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .layout import GeneratorSpec, GridDims, GridError, make_grid
+
+__all__ = ["DeviceCoefficients", "make_opts", "advect", "step", "wrap_halos", "fill",
+           "describe_plan", "HostContext", "dims_of", "alloc_fields"]
+
+
+def _stream_handle(stream, device) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _p(t: torch.Tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def dims_of(t: torch.Tensor) -> GridDims:
+    if t.dim() != 3:
+        raise GridError(f"fields are 3-D (nx+2, ny+2, nz), got shape {tuple(t.shape)}")
+    return make_grid(t.shape[0] - 2, t.shape[1] - 2, t.shape[2])
+
+
+def _check_field(t: torch.Tensor, dims: GridDims, name: str) -> None:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch tensor")
+    if tuple(t.shape) != dims.padded_shape:
+        raise GridError(f"{name} shape {tuple(t.shape)} != padded {dims.padded_shape}")
+    if t.dtype != torch.float64:
+        raise GridError(f"fields are float64, got {t.dtype} for {name}")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (the PW path has no CPU fallback)")
+    if not t.is_contiguous():
+        raise GridError(f"{name} must be C-contiguous (k fastest)")
+
+
+def alloc_fields(dims: GridDims, device=None, zero: bool = True):
+    """Three padded float64 fields on `device` (zeroed: +0.0 halos, as zeros_sources)."""
+    mk = torch.zeros if zero else torch.empty
+    return tuple(mk(dims.padded_shape, dtype=torch.float64, device=device) for _ in range(3))
+
+
+@dataclass
+class DeviceCoefficients:
+    """tcx/tcy scalars + tzc1/tzc2 resident on the device (tz[0] = tzc1, tz[1] = tzc2)."""
+
+    tcx: float
+    tcy: float
+    tz: torch.Tensor  # (2, nz) float64 CUDA
+
+    @property
+    def nz(self) -> int:
+        return int(self.tz.shape[1])
+
+    @classmethod
+    def from_host(cls, coeffs, device=None) -> "DeviceCoefficients":
+        """From a (reference or mirror) AdvectionCoefficients-like object."""
+        tz = np.stack([np.asarray(coeffs.tzc1, dtype=np.float64),
+                       np.asarray(coeffs.tzc2, dtype=np.float64)])
+        t = torch.from_numpy(np.ascontiguousarray(tz)).to(device or "cuda")
+        return cls(float(coeffs.tcx), float(coeffs.tcy), t)
+
+
+def _as_device_coeffs(coeffs, device) -> DeviceCoefficients:
+    if isinstance(coeffs, DeviceCoefficients):
+        if coeffs.tz.device != device:
+            return DeviceCoefficients(coeffs.tcx, coeffs.tcy, coeffs.tz.to(device))
+        return coeffs
+    return DeviceCoefficients.from_host(coeffs, device)
+
+
+def make_opts(variant: str = "xmarch", *, tile_j: int = 0, stages: int = 0, grid: int = 0,
+              max_threads: int = 0, streaming: bool = True) -> _lib.Opts:
+    """Kernel selection: "xmarch" (bulk-copy plane ring, default), "simple"
+    (one thread per point); suffix "_fma" for the DFMA (not bit-exact) build."""
+    flags = 0
+    base = variant
+    if variant.endswith("_fma"):
+        flags |= _lib.FLAG_FMA
+        base = variant[:-4]
+    if base == "simple":
+        flags |= _lib.FLAG_SIMPLE
+    elif base != "xmarch":
+        raise ValueError(f"unknown kernel variant {variant!r}")
+    if not streaming:
+        flags |= _lib.FLAG_NO_STREAMING
+    return _lib.Opts(flags, tile_j, stages, grid, max_threads)
+
+
+def _box(dims: GridDims, box):
+    if box is None:
+        return 1, dims.nx + 1, 1, dims.ny + 1
+    x0, x1, y0, y1 = (int(b) for b in box)
+    if not (1 <= x0 <= x1 <= dims.nx + 1 and 1 <= y0 <= y1 <= dims.ny + 1):
+        raise ValueError(f"box {box} outside interior {dims.nx}x{dims.ny}")
+    return x0, x1, y0, y1
+
+
+def advect(u, v, w, coeffs, out=None, *, box=None, opts: _lib.Opts | None = None,
+           stream=None):
+    """K1: su, sv, sw = PW advection of (u, v, w); returns the output tensors.
+
+    `out` (su, sv, sw) must be zero-initialised once by the caller (halo
+    columns are never written); allocated with +0.0 halos when None.
+    `box` = (x_begin, x_end, y_begin, y_end) restricts to interior columns
+    (1-based, half-open), like the reference's X slabs (schedules.py:53-75).
+    """
+    dims = dims_of(u)
+    for t, n in ((u, "u"), (v, "v"), (w, "w")):
+        _check_field(t, dims, n)
+    dc = _as_device_coeffs(coeffs, u.device)
+    if dc.nz != dims.nz:
+        raise ValueError(f"coefficient length {dc.nz} != nz {dims.nz}")
+    if out is None:
+        out = alloc_fields(dims, u.device)
+    for t, n in zip(out, ("su", "sv", "sw")):
+        _check_field(t, dims, n)
+    x0, x1, y0, y1 = _box(dims, box)
+    L = _lib.lib()
+    _lib.check(L.pwadv_advect_box_f64(_p(u), _p(v), _p(w), _p(out[0]), _p(out[1]), _p(out[2]),
+                                      dims.nx, dims.ny, dims.nz, dc.tcx, dc.tcy, _p(dc.tz[0]),
+                                      _p(dc.tz[1]), x0, x1, y0, y1, _lib.opts_ptr(opts),
+                                      _stream_handle(stream, u.device)))
+    return out
+
+
+def step(u, v, w, coeffs, dt: float, out, *, box=None, opts: _lib.Opts | None = None,
+         stream=None):
+    """K4: out = (u, v, w) + dt*(su, sv, sw) on interior columns (halos untouched)."""
+    dims = dims_of(u)
+    for t, n in ((u, "u"), (v, "v"), (w, "w")):
+        _check_field(t, dims, n)
+    for t, n in zip(out, ("u_new", "v_new", "w_new")):
+        _check_field(t, dims, n)
+    dc = _as_device_coeffs(coeffs, u.device)
+    if dc.nz != dims.nz:
+        raise ValueError(f"coefficient length {dc.nz} != nz {dims.nz}")
+    x0, x1, y0, y1 = _box(dims, box)
+    _lib.check(_lib.lib().pwadv_step_box_f64(
+        _p(u), _p(v), _p(w), _p(out[0]), _p(out[1]), _p(out[2]), dims.nx, dims.ny, dims.nz,
+        dc.tcx, dc.tcy, _p(dc.tz[0]), _p(dc.tz[1]), float(dt), x0, x1, y0, y1,
+        _lib.opts_ptr(opts), _stream_handle(stream, u.device)))
+    return out
+
+
+def wrap_halos(*fields, stream=None) -> None:
+    """K2: periodic halo wrap in place (reference grid.py:203-208)."""
+    if not fields:
+        return
+    dims = dims_of(fields[0])
+    for t in fields:
+        _check_field(t, dims, "field")
+    L = _lib.lib()
+    h = _stream_handle(stream, fields[0].device)
+    if len(fields) == 3:
+        _lib.check(L.pwadv_wrap_halos3_f64(_p(fields[0]), _p(fields[1]), _p(fields[2]),
+                                           dims.nx, dims.ny, dims.nz, h))
+    else:
+        for t in fields:
+            _lib.check(L.pwadv_wrap_halos_f64(_p(t), dims.nx, dims.ny, dims.nz, h))
+
+
+def fill(dims: GridDims, spec: GeneratorSpec, device=None, stream=None, out=None):
+    """K5: (u, v, w) on the device, bit-identical to the reference fill_fields."""
+    if spec.mode == "trig":
+        raise ValueError("the trig test pattern is host-generated (layout.fill_fields)")
+    code = {"random": 0, "baseline": 1, "uniform": 2}[spec.mode]
+    if out is None:
+        out = alloc_fields(dims, device or "cuda", zero=False)
+    for t, n in zip(out, "uvw"):
+        _check_field(t, dims, n)
+    _lib.check(_lib.lib().pwadv_fill_f64(_p(out[0]), _p(out[1]), _p(out[2]), dims.nx, dims.ny,
+                                         dims.nz, code, int(spec.seed) & (2**64 - 1),
+                                         float(spec.a), float(spec.b), float(spec.c),
+                                         _stream_handle(stream, out[0].device)))
+    return out
+
+
+def describe_plan(dims: GridDims, box=None, opts: _lib.Opts | None = None, device: int = 0) -> dict:
+    x0, x1, y0, y1 = _box(dims, box)
+    info = _lib.PlanInfo()
+    _lib.check(_lib.lib().pwadv_describe_plan(dims.nx, dims.ny, dims.nz, x0, x1, y0, y1,
+                                              _lib.opts_ptr(opts), int(device), ctypes.byref(info)))
+    return {"kernel": {1: "xmarch", 2: "simple"}[info.kernel], "tile_j": info.tile_j,
+            "threads_per_column": info.threads_per_column, "stages": info.stages,
+            "threads": info.threads, "grid": info.grid, "smem_bytes": info.smem_bytes,
+            "strips": info.strips}
+
+
+class HostContext:
+    """pwadv_ctx: device buffers + 3 streams for host-buffer (end-to-end) calls."""
+
+    def __init__(self, dims: GridDims, device: int = 0):
+        self.dims = dims
+        self.device = int(device)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().pwadv_ctx_create(ctypes.byref(h), self.device, dims.nx, dims.ny,
+                                               dims.nz))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.lib().pwadv_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _hp(a) -> ctypes.c_void_p:
+        if isinstance(a, torch.Tensor):
+            if a.is_cuda or a.dtype != torch.float64 or not a.is_contiguous():
+                raise ValueError("host buffers must be contiguous float64 CPU tensors")
+            return ctypes.c_void_p(a.data_ptr())
+        if a.dtype != np.float64 or not a.flags.c_contiguous:
+            raise GridError("host buffers must be C-contiguous float64 arrays")
+        return ctypes.c_void_p(a.ctypes.data)
+
+    def advect_host(self, u, v, w, su, sv, sw, tcx, tcy, tzc1, tzc2, chunks: int = 0,
+                    opts: _lib.Opts | None = None) -> tuple[int, int]:
+        """Host in, host out: pipelined H2D / K1 / D2H. Returns (h2d, d2h) bytes."""
+        d = self.dims
+        for a in (u, v, w, su, sv, sw):
+            if tuple(a.shape) != d.padded_shape:
+                raise GridError(f"field shape {tuple(a.shape)} != padded {d.padded_shape}")
+        tz1 = np.ascontiguousarray(tzc1, dtype=np.float64)
+        tz2 = np.ascontiguousarray(tzc2, dtype=np.float64)
+        if tz1.shape != (d.nz,) or tz2.shape != (d.nz,):
+            raise ValueError(f"coefficient length {tz1.shape} != nz {d.nz}")
+        if chunks <= 0:
+            # pipeline only when transfers are large enough to overlap
+            chunks = 1 if d.padded_len * 8 < (32 << 20) else min(16, d.nx)
+        _lib.check(_lib.lib().pwadv_ctx_advect_host(
+            self._h, self._hp(u), self._hp(v), self._hp(w), self._hp(su), self._hp(sv),
+            self._hp(sw), float(tcx), float(tcy), ctypes.c_void_p(tz1.ctypes.data),
+            ctypes.c_void_p(tz2.ctypes.data), int(chunks), _lib.opts_ptr(opts)))
+        a, b = ctypes.c_uint64(), ctypes.c_uint64()
+        _lib.check(_lib.lib().pwadv_ctx_last_bytes(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return int(a.value), int(b.value)

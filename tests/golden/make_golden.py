@@ -34,7 +34,8 @@ sys.path.insert(0, str(REF / "src"))
 
 from pwadvect.grid import (FieldSet, Field3D, GeneratorSpec, checksum,  # noqa: E402
                            fill_fields, lcg_doubles, make_grid, wrap_halos)
-from pwadvect.kernel import AdvectionCoefficients, run_reference  # noqa: E402
+from pwadvect.kernel import (COMPUTE_ROLES, AdvectionCoefficients,  # noqa: E402
+                             operation_census, reads_per_point, run_reference)
 
 OUT = Path(__file__).resolve().parent
 
@@ -137,7 +138,11 @@ def main():
     (OUT / "cases.json").write_text(json.dumps({
         "generated_by": "tests/golden/make_golden.py (imports reference pwadvect 0.1.0)",
         "reference_goldens_json": goldens,
-        "cases": cases}, indent=1))
+        "cases": cases,
+        "compute_roles": [list(r) for r in COMPUTE_ROLES],
+        "operation_census": {"mid": operation_census(False), "top": operation_census(True),
+                             "reads_mid": reads_per_point(False),
+                             "reads_top": reads_per_point(True)}}, indent=1))
     np.savez_compressed(OUT / "small.npz", **small)
 
     # 6. composed time stepping: f <- f + dt*s, then wrap
