@@ -54,7 +54,11 @@ enum {
 /* flags for pwadv_opts.flags */
 #define PWADV_FLAG_FMA 1u           /* contract into DFMA (not bit-exact; <=1e-12 normwise) */
 #define PWADV_FLAG_SIMPLE 2u        /* force the one-thread-per-point kernel */
-#define PWADV_FLAG_NO_STREAMING 4u  /* plain stores instead of st.global.cs */
+/* ablation switches for profiling only (results are NOT the PW sources):
+ * skip the arithmetic / skip waiting for staged planes */
+#define PWADV_FLAG_DEBUG_NO_COMPUTE 0x100u
+#define PWADV_FLAG_DEBUG_NO_WAIT 0x200u
+#define PWADV_FLAG_DEBUG_NO_STORE 0x400u
 
 /* Optional tuning / variant selection; pass NULL for defaults. */
 typedef struct pwadv_opts {
@@ -62,7 +66,10 @@ typedef struct pwadv_opts {
     int32_t tile_j;        /* columns per CTA strip for the X-march kernel (0 = auto) */
     int32_t stages;        /* smem plane-ring depth (0 = auto) */
     int32_t grid;          /* CTAs (0 = auto: SMs x resident CTAs) */
-    int32_t max_threads;   /* X-march CTA thread budget: 512, 384 or 256 (0 = auto) */
+    int32_t max_threads;   /* X-march CTA thread budget: 512, 448, 384 or 256 (0 = auto) */
+    int32_t chunks;        /* X chunks per strip (work unit = chunk x strip; 0 = auto) */
+    void *trace;           /* profiling only: device buffer of 2x4096 u64 for CTA 0's
+                              per-plane copy-issue / arrival %globaltimer stamps; NULL = off */
 } pwadv_opts;
 
 int pwadv_abi_version(void);
@@ -105,6 +112,7 @@ typedef struct pwadv_plan_info {
     int32_t kernel;        /* 1 = X-march (bulk-copy plane ring), 2 = one-thread-per-point */
     int32_t tile_j, threads_per_column, stages, threads, grid;
     int64_t smem_bytes, strips;
+    int32_t chunks, reserved;
 } pwadv_plan_info;
 int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz,
                         int64_t x_begin, int64_t x_end, int64_t y_begin, int64_t y_end,

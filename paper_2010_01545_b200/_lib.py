@@ -32,7 +32,6 @@ PWADV_E_ALIGN = -6
 
 FLAG_FMA = 1
 FLAG_SIMPLE = 2
-FLAG_NO_STREAMING = 4
 
 
 class Opts(ctypes.Structure):
@@ -40,7 +39,8 @@ class Opts(ctypes.Structure):
 
     _fields_ = [("flags", ctypes.c_uint32), ("tile_j", ctypes.c_int32),
                 ("stages", ctypes.c_int32), ("grid", ctypes.c_int32),
-                ("max_threads", ctypes.c_int32)]
+                ("max_threads", ctypes.c_int32), ("chunks", ctypes.c_int32),
+                ("trace", ctypes.c_void_p)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -49,7 +49,8 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [("kernel", ctypes.c_int32), ("tile_j", ctypes.c_int32),
                 ("threads_per_column", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("threads", ctypes.c_int32), ("grid", ctypes.c_int32),
-                ("smem_bytes", ctypes.c_int64), ("strips", ctypes.c_int64)]
+                ("smem_bytes", ctypes.c_int64), ("strips", ctypes.c_int64),
+                ("chunks", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 # name -> (restype, argtypes); every symbol include/pwadv.h declares

@@ -29,6 +29,8 @@
 #include "pwadv_device.cuh"
 #include "pwadv_internal.h"
 
+#include <type_traits>
+
 namespace pwadv {
 
 struct BoxArgs {
@@ -43,15 +45,40 @@ struct BoxArgs {
     int64_t nx, ny, nz;
     double tcx, tcy, dt;
     int64_t x0, x1, y0, y1;  // interior box, 1-based, half-open
+    unsigned long long *trace;  // profiling only: per-plane issue/arrival timestamps (CTA 0)
 };
 
 struct TileCfg {
     int tj;           // columns per strip
     int kp;           // threads per column (= nz/2)
     int stages;       // ring depth
-    int streaming;    // st.global.cs for outputs
+    int nchunks;      // X chunks per strip; work unit = (chunk, strip)
+    int debug;        // ablation bits (PWADV_FLAG_DEBUG_*): 1 = no compute, 2 = no data waits,
+                      // 4 = no stores
     int64_t nstrips;  // ceil((y1-y0)/tj)
 };
+
+// Work units are (chunk, strip) pairs numbered chunk-major,
+// u = chunk * nstrips + strip, dealt round-robin to the CTAs: CTA b runs units
+// b, b+G, b+2G, ... All CTAs start a round together and march at the same
+// rate, so CTAs on adjacent strips stand on the same X planes at the same
+// time and each strip's two halo columns (the neighbours' edge columns) are
+// served from L2 instead of HBM; the plane before a chunk was streamed by the
+// previous round for the same strip and is an L2 hit as well.
+struct Unit {
+    int64_t strip, ib, ie;  // outputs i in [ib, ie) of this strip
+};
+
+__device__ __forceinline__ Unit unit_at(const BoxArgs &a, const TileCfg &t, int64_t u)
+{
+    const int64_t chunk = u / t.nstrips;
+    const int64_t nxr = a.x1 - a.x0;
+    Unit w;
+    w.strip = u - chunk * t.nstrips;
+    w.ib = a.x0 + (nxr * chunk) / t.nchunks;
+    w.ie = a.x0 + (nxr * (chunk + 1)) / t.nchunks;
+    return w;
+}
 
 // ---------------------------------------------------------------------------
 // simple kernel
@@ -113,24 +140,84 @@ __global__ void __launch_bounds__(256) k_advect_simple(BoxArgs a)
 // X-march kernel
 
 // value at k0-1 of the thread's pair: the previous lane's k1, or (across a
-// warp boundary inside a column) straight from the shared plane.
+// warp boundary inside a column, FIX only) straight from the shared plane.
+template <bool FIX>
 __device__ __forceinline__ double nbr_m(double2 p, const double *colp, int k0, bool fix)
 {
     double m = __shfl_up_sync(0xffffffffu, p.y, 1);
-    if (fix) m = colp[k0 - 1];
+    if constexpr (FIX) {
+        if (fix) m = colp[k0 - 1];
+    }
     return m;
 }
 
 // value at k0+2: the next lane's k0, or from the shared plane.
+template <bool FIX>
 __device__ __forceinline__ double nbr_q(double2 p, const double *colp, int k0, bool fix)
 {
     double q = __shfl_down_sync(0xffffffffu, p.x, 1);
-    if (fix) q = colp[k0 + 2];
+    if constexpr (FIX) {
+        if (fix) q = colp[k0 + 2];
+    }
     return q;
 }
 
-template <bool FMA, bool STEP, int MAXT>
-__global__ void __launch_bounds__(MAXT, 1) k_advect_xmarch(BoxArgs a, TileCfg t)
+// Per-CTA ring bookkeeping in shared memory. Planes are numbered by a CTA-
+// local sequence number q (the order the CTA consumes them); plane q lives in
+// stage q % S. Unit k of this CTA (global unit blockIdx.x + k*gridDim.x)
+// streams planes first[k] .. first[k+1]-1 = its chunk plus one plane each side.
+constexpr int kMaxUnitsPerCta = 64;
+
+struct RingState {
+    int total;                        // planes this CTA streams
+    int nunits;                       // units of this CTA
+    int first[kMaxUnitsPerCta + 1];   // first sequence number of each unit
+    uint32_t bytes[kMaxUnitsPerCta];  // bytes per field per plane of each unit
+    int64_t src[kMaxUnitsPerCta];     // element offset of the unit's first plane tile
+    int released[16];                 // per stage: warps done with its current plane
+};
+
+__device__ __forceinline__ unsigned long long gtime()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Issue the bulk copies of plane q (3 fields, one contiguous run each) into
+// stage st, completing on full[st]. A table lookup and one multiply-add: the
+// warp that issues must not fall behind the others (it gates the next refill).
+__device__ __forceinline__ void issue_plane(const RingState *rs, const BoxArgs &a, int q, int st,
+                                            int CS, double *ring, uint64_t *full)
+{
+    if (a.trace && blockIdx.x == 0 && q < 4096) a.trace[2 * q] = gtime();
+    int k = 0;
+    while (rs->first[k + 1] <= q) ++k;
+    const uint32_t bytes = rs->bytes[k];
+    const int64_t off = rs->src[k] + (int64_t)(q - rs->first[k]) * ((a.ny + 2) * a.nz);
+    mbar_arrive_expect_tx(&full[st], 3 * bytes);
+    double *dst = ring + (size_t)st * 3 * CS;
+    bulk_g2s(dst, a.u + off, bytes, &full[st]);
+    bulk_g2s(dst + CS, a.v + off, bytes, &full[st]);
+    bulk_g2s(dst + 2 * CS, a.w + off, bytes, &full[st]);
+}
+
+// X-march kernel. Register slots U0[3], V0[3], ... hold plane p in slot p % 3
+// (relative to the unit start), so the x-1/x/x+1 window rotates by renaming —
+// the step body is instantiated for the three rotations and unrolled, with no
+// register moves.
+//
+// Ring protocol (no producer warp): each warp, once it has read everything it
+// needs from plane q, bumps released[q % S]; the warp that completes the count
+// resets it and immediately issues plane q+S into the freed stage. Refills
+// happen in sequence order (every warp releases q before q+1), and no single
+// warp paces the pipeline. Planes q+1 .. q+S-1 are resident or in flight
+// when q is released.
+// resident CTAs per SM for a thread budget (each CTA keeps <= 168 registers)
+__host__ __device__ constexpr int ctas_per_sm(int maxt) { return maxt <= 128 ? 3 : (maxt <= 192 ? 2 : 1); }
+
+template <bool FMA, bool STEP, int MAXT, bool FIX>
+__global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT)) k_advect_xmarch(BoxArgs a, TileCfg t)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int S = t.stages, TJ = t.tj, KP = t.kp;
@@ -138,7 +225,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_advect_xmarch(BoxArgs a, TileCfg t)
     const int CS = (TJ + 2) * nz;  // doubles per field per tile-plane
     double *ring = reinterpret_cast<double *>(smem_raw);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)S * 3 * CS * sizeof(double));
-    uint64_t *empty = full + S;
+    RingState *rs = reinterpret_cast<RingState *>(full + S);
 
     const int tid = threadIdx.x, lane = tid & 31;
     const int nwarps = blockDim.x >> 5;
@@ -146,8 +233,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_advect_xmarch(BoxArgs a, TileCfg t)
     const int c = in_tile ? tid / KP : TJ - 1;
     const int kp = in_tile ? tid - (tid / KP) * KP : 0;
     const int k0 = 2 * kp, k1 = k0 + 1;
-    const bool fixM = (lane == 0) && kp > 0;
-    const bool fixQ = (lane == 31) && kp < KP - 1;
+    const bool fixM = FIX && (lane == 0) && kp > 0;
+    const bool fixQ = FIX && (lane == 31) && kp < KP - 1;
     const bool top_b = (k1 == nz - 1);
     const bool lvl0 = (k0 == 0);
 
@@ -156,138 +243,169 @@ __global__ void __launch_bounds__(MAXT, 1) k_advect_xmarch(BoxArgs a, TileCfg t)
     const double c2a = __ldg(a.tzc2 + k0), c2b = __ldg(a.tzc2 + k1);
 
     const int64_t ny2 = a.ny + 2;
-    const int64_t nxr = a.x1 - a.x0;
-    const int64_t W = t.nstrips * nxr;
-    const int64_t wb = (W * (int64_t)blockIdx.x) / gridDim.x;
-    const int64_t we = (W * (int64_t)(blockIdx.x + 1)) / gridDim.x;
-    if (wb >= we) return;
-    const int64_t sb0 = wb / nxr, sb1 = (we - 1) / nxr;
-    const int total = (int)((we - wb) + 2 * (sb1 - sb0 + 1));  // planes this CTA streams
+    const int64_t nunits = t.nstrips * t.nchunks;
+    const int64_t G = gridDim.x;
+    if ((int64_t)blockIdx.x >= nunits) return;
 
     if (tid == 0) {
+        int q = 0, k = 0;
+        for (int64_t u = blockIdx.x; u < nunits && k < kMaxUnitsPerCta; u += G, ++k) {
+            const Unit w = unit_at(a, t, u);
+            const int64_t j0 = a.y0 + w.strip * TJ;
+            const int64_t tjs = (a.y1 - j0) < TJ ? (a.y1 - j0) : TJ;
+            rs->first[k] = q;
+            rs->bytes[k] = (uint32_t)((tjs + 2) * nz * sizeof(double));
+            rs->src[k] = ((w.ib - 1) * ny2 + (j0 - 1)) * nz;
+            q += (int)(w.ie - w.ib + 2);
+        }
+        rs->first[k] = q;
+        rs->total = q;
+        rs->nunits = k;
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], nwarps);
+            rs->released[s] = 0;
         }
         fence_mbar_init();
+        const int n0 = q < S ? q : S;
+        for (int n = 0; n < n0; ++n) issue_plane(rs, a, n, n, CS, ring, full);
     }
     __syncthreads();
+    const int total = rs->total;
+    const int my_units = rs->nunits;
 
-    // ---- producer state (thread 0 only) --------------------------------
-    int pseq = 0;
-    int64_t p_strip = sb0, p_plane = 0, p_end = 0;
-    auto seg_ib = [&](int64_t s) { return a.x0 + (wb - s * nxr > 0 ? wb - s * nxr : 0); };
-    auto seg_ie = [&](int64_t s) { return a.x0 + (we - s * nxr < nxr ? we - s * nxr : nxr); };
-    if (tid == 0) {
-        p_plane = seg_ib(sb0) - 1;
-        p_end = seg_ie(sb0);
-    }
-    auto issue = [&]() {
-        const int st = (int)(pseq % S);
-        if (pseq >= S) mbar_wait(&empty[st], (uint32_t)(((pseq / S) - 1) & 1));
-        const int64_t j0 = a.y0 + p_strip * TJ;
-        const int64_t tjs = (a.y1 - j0) < TJ ? (a.y1 - j0) : TJ;
-        const uint32_t bytes = (uint32_t)((tjs + 2) * nz * sizeof(double));
-        mbar_arrive_expect_tx(&full[st], 3 * bytes);
-        const int64_t off = (p_plane * ny2 + (j0 - 1)) * nz;
-        double *dst = ring + (size_t)st * 3 * CS;
-        bulk_g2s(dst, a.u + off, bytes, &full[st]);
-        bulk_g2s(dst + CS, a.v + off, bytes, &full[st]);
-        bulk_g2s(dst + 2 * CS, a.w + off, bytes, &full[st]);
-        ++pseq;
-        if (++p_plane > p_end) {
-            ++p_strip;
-            if (p_strip <= sb1) {
-                p_plane = seg_ib(p_strip) - 1;
-                p_end = seg_ie(p_strip);
+    // consumer ring position: sequence number, stage and parity of the
+    // plane to wait for next
+    int cseq = 0, cst = 0;
+    uint32_t cph = 0;
+    const int toff = (c + 1) * nz + k0;  // this thread's pair in a field tile-plane
+
+    auto release = [&](int seq, int st) {
+        __syncwarp();
+        if (lane == 0) {
+            __threadfence_block();  // this warp's reads of the stage happen before the refill
+            const int done = atomicAdd(&rs->released[st], 1);
+            if (done == nwarps - 1) {
+                rs->released[st] = 0;
+                if (seq + S < total) {
+                    fence_proxy_async();
+                    issue_plane(rs, a, seq + S, st, CS, ring, full);
+                }
             }
         }
     };
-    if (tid == 0) {
-        const int n0 = total < S ? total : S;
-        for (int n = 0; n < n0; ++n) issue();
-    }
-    // warp 0 releases planes in sequence order; after each release thread 0
-    // refills the stage released one step earlier (keeps S-3 planes in flight
-    // beyond the next one without stalling on the slowest warp).
-    auto release = [&](int seq) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[seq % S]);
-        if (tid == 0) {
-            while (pseq < total && pseq <= seq - 1 + S) issue();
+    auto wait_next = [&]() -> const double * {
+        if (!(t.debug & 2)) mbar_wait(&full[cst], cph);
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && cseq < 4096) a.trace[2 * cseq + 1] = gtime();
+        return ring + (size_t)cst * 3 * CS;
+    };
+    auto advance = [&]() {
+        ++cseq;
+        if (++cst == S) {
+            cst = 0;
+            cph ^= 1u;
         }
     };
-    auto wait_full = [&](int seq) -> const double * {
-        const int st = (int)(seq % S);
-        mbar_wait(&full[st], (uint32_t)((seq / S) & 1));
-        return ring + (size_t)st * 3 * CS;
-    };
-    // pair (k0, k0+1) of field f, column offset dy, in a staged plane
     auto P = [&](const double *pl, int f, int dy) -> double2 {
-        return *reinterpret_cast<const double2 *>(pl + f * CS + (c + 1 + dy) * nz + k0);
+        return *reinterpret_cast<const double2 *>(pl + f * CS + dy * nz + toff);
     };
     auto colp = [&](const double *pl, int f, int dy) -> const double * {
         return pl + f * CS + (c + 1 + dy) * nz;
     };
 
-    int cseq = 0;
-    for (int64_t s = sb0; s <= sb1; ++s) {
-        const int64_t ib = seg_ib(s), ie = seg_ie(s);
-        const int64_t j0 = a.y0 + s * TJ;
+    double2 U0[3], V0[3], W0[3], U1[3], VM[3];
+    double U0M[3], W0M[3];
+
+    for (int k = 0; k < my_units; ++k) {
+        const Unit wu = unit_at(a, t, (int64_t)blockIdx.x + (int64_t)k * G);
+        const int64_t ib = wu.ib, ie = wu.ie;
+        const int64_t j0 = a.y0 + wu.strip * TJ;
         const int64_t tjs = (a.y1 - j0) < TJ ? (a.y1 - j0) : TJ;
         const bool active = in_tile && c < tjs;
 
-        // plane ib-1: the x-1 window
-        const double *pl = wait_full(cseq);
-        double2 u0m = P(pl, 0, 0), u1m = P(pl, 0, 1), v0m = P(pl, 1, 0), w0m = P(pl, 2, 0);
-        double u0mM = nbr_m(u0m, colp(pl, 0, 0), k0, fixM);
-        release(cseq);
-        ++cseq;
-        // plane ib: the x window (leading items)
-        pl = wait_full(cseq);
-        double2 u0c = P(pl, 0, 0), v0c = P(pl, 1, 0), w0c = P(pl, 2, 0), vmc = P(pl, 1, -1);
-        double w0cM = nbr_m(w0c, colp(pl, 2, 0), k0, fixM);
-        ++cseq;
+        // plane ib-1 -> slot 2 (the x-1 window of the first step)
+        {
+            const double *pl = wait_next();
+            U0[2] = P(pl, 0, 0);
+            U1[2] = P(pl, 0, 1);
+            V0[2] = P(pl, 1, 0);
+            W0[2] = P(pl, 2, 0);
+            U0M[2] = nbr_m<FIX>(U0[2], colp(pl, 0, 0), k0, fixM);
+            release(cseq, cst);
+            advance();
+        }
+        // plane ib -> slot 0 (items read from the leading plane)
+        int pst = cst;  // stage of the current x plane, released one step later
+        {
+            const double *pl = wait_next();
+            U0[0] = P(pl, 0, 0);
+            V0[0] = P(pl, 1, 0);
+            W0[0] = P(pl, 2, 0);
+            VM[0] = P(pl, 1, -1);
+            W0M[0] = nbr_m<FIX>(W0[0], colp(pl, 2, 0), k0, fixM);
+            advance();
+        }
 
-        int64_t obase = (ib * ny2 + (j0 + c)) * (int64_t)nz + k0;
+        double *o0 = a.o0 + (ib * ny2 + (j0 + c)) * (int64_t)nz + k0;
+        double *o1 = a.o1 + (ib * ny2 + (j0 + c)) * (int64_t)nz + k0;
+        double *o2 = a.o2 + (ib * ny2 + (j0 + c)) * (int64_t)nz + k0;
         const int64_t ostep = ny2 * nz;
-        const int nsteps = (int)(ie - ib);
-        for (int n = 0; n < nsteps; ++n, obase += ostep) {
-            const double *L = wait_full(cseq);                       // plane i+1
-            const double *C = ring + (size_t)((cseq - 1) % S) * 3 * CS;  // plane i
-            const double2 u0p = P(L, 0, 0), v0p = P(L, 1, 0), w0p = P(L, 2, 0), vmp = P(L, 1, -1);
-            const double w0pM = nbr_m(w0p, colp(L, 2, 0), k0, fixM);
-            const double2 u1c = P(C, 0, 1), umc = P(C, 0, -1), v1c = P(C, 1, 1);
-            const double2 w1c = P(C, 2, 1), wmc = P(C, 2, -1);
-            const double w1cM = nbr_m(w1c, colp(C, 2, 1), k0, fixM);
-            const double u0cM = nbr_m(u0c, colp(C, 0, 0), k0, fixM);
-            const double u0cQ = nbr_q(u0c, colp(C, 0, 0), k0, fixQ);
-            const double v0cM = nbr_m(v0c, colp(C, 1, 0), k0, fixM);
-            const double v0cQ = nbr_q(v0c, colp(C, 1, 0), k0, fixQ);
-            const double w0cQ = nbr_q(w0c, colp(C, 2, 0), k0, fixQ);
-            const double vmcM = nbr_m(vmc, colp(C, 1, -1), k0, fixM);
-            release(cseq - 1);  // plane i fully consumed by this warp
 
-            // level k0 (never the top; level 0 is identically zero)
-            double su_a = su_formula<FMA>(tcx, tcy, c1a, c2a, u0c.x, u0m.x, u0p.x, umc.x, u1c.x,
-                                          u0cM, u0c.y, vmc.x, vmp.x, v0c.x, v0p.x, w0cM, w0pM,
-                                          w0c.x, w0p.x, false);
-            double sv_a = sv_formula<FMA>(tcx, tcy, c1a, c2a, v0c.x, v0m.x, v0p.x, vmc.x, v1c.x,
-                                          v0cM, v0c.y, u0m.x, u1m.x, u0c.x, u1c.x, w0cM, w1cM,
-                                          w0c.x, w1c.x, false);
-            double sw_a = sw_formula<FMA>(tcx, tcy, c1a, c2a, w0c.x, w0m.x, w0p.x, wmc.x, w1c.x,
-                                          w0cM, w0c.y, u0mM, u0m.x, u0cM, u0c.x, vmcM, vmc.x,
-                                          v0cM, v0c.x, false);
-            // level k1 (the top when k1 == nz-1)
-            double su_b = su_formula<FMA>(tcx, tcy, c1b, c2b, u0c.y, u0m.y, u0p.y, umc.y, u1c.y,
-                                          u0c.x, u0cQ, vmc.y, vmp.y, v0c.y, v0p.y, w0c.x, w0p.x,
-                                          w0c.y, w0p.y, top_b);
-            double sv_b = sv_formula<FMA>(tcx, tcy, c1b, c2b, v0c.y, v0m.y, v0p.y, vmc.y, v1c.y,
-                                          v0c.x, v0cQ, u0m.y, u1m.y, u0c.y, u1c.y, w0c.x, w1c.x,
-                                          w0c.y, w1c.y, top_b);
-            double sw_b = sw_formula<FMA>(tcx, tcy, c1b, c2b, w0c.y, w0m.y, w0p.y, wmc.y, w1c.y,
-                                          w0c.x, w0cQ, u0m.x, u0m.y, u0c.x, u0c.y, vmc.x, vmc.y,
-                                          v0c.x, v0c.y, top_b);
+        auto body = [&](auto R) {
+            constexpr int r = decltype(R)::value;
+            constexpr int rm = (r + 2) % 3, rp = (r + 1) % 3;
+            const int lst = cst;
+            const double *L = wait_next();                           // plane i+1
+            const double *C = ring + (size_t)pst * 3 * CS;           // plane i
+            U0[rp] = P(L, 0, 0);
+            V0[rp] = P(L, 1, 0);
+            W0[rp] = P(L, 2, 0);
+            VM[rp] = P(L, 1, -1);
+            W0M[rp] = nbr_m<FIX>(W0[rp], colp(L, 2, 0), k0, fixM);
+            U1[r] = P(C, 0, 1);
+            const double2 umc = P(C, 0, -1), v1c = P(C, 1, 1), w1c = P(C, 2, 1), wmc = P(C, 2, -1);
+            const double w1cM = nbr_m<FIX>(w1c, colp(C, 2, 1), k0, fixM);
+            U0M[r] = nbr_m<FIX>(U0[r], colp(C, 0, 0), k0, fixM);
+            const double u0cQ = nbr_q<FIX>(U0[r], colp(C, 0, 0), k0, fixQ);
+            const double v0cM = nbr_m<FIX>(V0[r], colp(C, 1, 0), k0, fixM);
+            const double v0cQ = nbr_q<FIX>(V0[r], colp(C, 1, 0), k0, fixQ);
+            const double w0cQ = nbr_q<FIX>(W0[r], colp(C, 2, 0), k0, fixQ);
+            const double vmcM = nbr_m<FIX>(VM[r], colp(C, 1, -1), k0, fixM);
+            release(cseq - 1, pst);  // plane i fully consumed by this warp
+
+            const double2 u0m = U0[rm], u0c = U0[r], u0p = U0[rp];
+            const double2 v0m = V0[rm], v0c = V0[r], v0p = V0[rp];
+            const double2 w0m = W0[rm], w0c = W0[r], w0p = W0[rp];
+            const double2 u1m = U1[rm], u1c = U1[r], vmc = VM[r], vmp = VM[rp];
+            const double u0mM = U0M[rm], u0cM = U0M[r], w0cM = W0M[r], w0pM = W0M[rp];
+
+            double su_a, sv_a, sw_a, su_b, sv_b, sw_b;
+            if (t.debug & 1) {  // ablation: touch every staged operand, no PW arithmetic
+                su_a = sv_a = sw_a = su_b = sv_b = sw_b =
+                    (u0c.x + u0p.x) + (umc.x + u1c.x) + (v1c.x + w1c.x) + (wmc.x + vmp.x) +
+                    (v0m.x + w0m.y) + (u1m.y + vmc.y) + (w0cM + w0pM) + (u0cQ + v0cQ) +
+                    (w0cQ + vmcM) + (v0cM + w1cM) + (u0mM + u0cM) + (v0p.y + w0p.x);
+            } else {
+    // level k0 (never the top; level 0 is identically zero)
+                su_a = su_formula<FMA>(tcx, tcy, c1a, c2a, u0c.x, u0m.x, u0p.x, umc.x, u1c.x,
+                                              u0cM, u0c.y, vmc.x, vmp.x, v0c.x, v0p.x, w0cM, w0pM,
+                                              w0c.x, w0p.x, false);
+                sv_a = sv_formula<FMA>(tcx, tcy, c1a, c2a, v0c.x, v0m.x, v0p.x, vmc.x, v1c.x,
+                                              v0cM, v0c.y, u0m.x, u1m.x, u0c.x, u1c.x, w0cM, w1cM,
+                                              w0c.x, w1c.x, false);
+                sw_a = sw_formula<FMA>(tcx, tcy, c1a, c2a, w0c.x, w0m.x, w0p.x, wmc.x, w1c.x,
+                                              w0cM, w0c.y, u0mM, u0m.x, u0cM, u0c.x, vmcM, vmc.x,
+                                              v0cM, v0c.x, false);
+                // level k1 (the top when k1 == nz-1)
+                su_b = su_formula<FMA>(tcx, tcy, c1b, c2b, u0c.y, u0m.y, u0p.y, umc.y, u1c.y,
+                                              u0c.x, u0cQ, vmc.y, vmp.y, v0c.y, v0p.y, w0c.x, w0p.x,
+                                              w0c.y, w0p.y, top_b);
+                sv_b = sv_formula<FMA>(tcx, tcy, c1b, c2b, v0c.y, v0m.y, v0p.y, vmc.y, v1c.y,
+                                              v0c.x, v0cQ, u0m.y, u1m.y, u0c.y, u1c.y, w0c.x, w1c.x,
+                                              w0c.y, w1c.y, top_b);
+                sw_b = sw_formula<FMA>(tcx, tcy, c1b, c2b, w0c.y, w0m.y, w0p.y, wmc.y, w1c.y,
+                                              w0c.x, w0cQ, u0m.x, u0m.y, u0c.x, u0c.y, vmc.x, vmc.y,
+                                              v0c.x, v0c.y, top_b);
+            }
             if (lvl0) {
                 su_a = 0.0;
                 sv_a = 0.0;
@@ -301,25 +419,39 @@ __global__ void __launch_bounds__(MAXT, 1) k_advect_xmarch(BoxArgs a, TileCfg t)
                 sw_a = fwd_update(w0c.x, dt, sw_a);
                 sw_b = fwd_update(w0c.y, dt, sw_b);
             }
-            if (active) {
-                store2(a.o0 + obase, su_a, su_b, t.streaming);
-                store2(a.o1 + obase, sv_a, sv_b, t.streaming);
-                store2(a.o2 + obase, sw_a, sw_b, t.streaming);
+            if (active && !(t.debug & 4)) {
+                store2(o0, su_a, su_b);
+                store2(o1, sv_a, sv_b);
+                store2(o2, sw_a, sw_b);
             }
-            // roll the x window
-            u0m = u0c;
-            u0mM = u0cM;
-            u0c = u0p;
-            u1m = u1c;
-            v0m = v0c;
-            v0c = v0p;
-            w0m = w0c;
-            w0c = w0p;
-            w0cM = w0pM;
-            vmc = vmp;
-            ++cseq;
+            o0 += ostep;
+            o1 += ostep;
+            o2 += ostep;
+            pst = lst;
+            advance();
+        };
+
+        using R0 = std::integral_constant<int, 0>;
+        using R1 = std::integral_constant<int, 1>;
+        using R2 = std::integral_constant<int, 2>;
+        const int nsteps = (int)(ie - ib);
+        int n = 0;
+        for (; n + 3 <= nsteps; n += 3) {
+            body(R0{});
+            body(R1{});
+            body(R2{});
         }
-        release(cseq - 1);  // plane ie was only read as the x+1 plane
+        if (n < nsteps) {
+            body(R0{});
+            if (n + 1 < nsteps) body(R1{});
+        }
+        release(cseq - 1, pst);  // plane ie was only read as the x+1 plane
+    }
+    if (t.debug & 2) {  // ablation: drain the copies still in flight before exit
+        for (int n = 0; n < S && n < total; ++n) {
+            const int q = total - 1 - n;
+            mbar_wait(&full[q % S], (uint32_t)((q / S) & 1));
+        }
     }
 }
 
@@ -349,6 +481,7 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
     a.x1 = L.x1;
     a.y0 = L.y0;
     a.y1 = L.y1;
+    a.trace = reinterpret_cast<unsigned long long *>(L.trace);
     const bool fma = (L.flags & PWADV_FLAG_FMA) != 0;
     const int64_t nbx = L.x1 - L.x0, nby = L.y1 - L.y0;
     if (nbx <= 0 || nby <= 0) return PWADV_OK;
@@ -363,19 +496,28 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         t.tj = plan.tj;
         t.kp = plan.kp;
         t.stages = plan.stages;
-        t.streaming = (L.flags & PWADV_FLAG_NO_STREAMING) ? 0 : 1;
+        t.nchunks = plan.nchunks;
+        t.debug = (int)((L.flags >> 8) & 7u);
         t.nstrips = plan.nstrips;
         void (*kern)(BoxArgs, TileCfg) = nullptr;
-#define PWADV_PICK(MT)                                                                      \
-    if (plan.maxt == MT) {                                                                  \
-        if (L.step)                                                                         \
-            kern = fma ? k_advect_xmarch<true, true, MT> : k_advect_xmarch<false, true, MT>; \
-        else                                                                                \
-            kern = fma ? k_advect_xmarch<true, false, MT> : k_advect_xmarch<false, false, MT>; \
+        const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
+#define PWADV_PICK(MT, FX)                                                       \
+    if (plan.maxt == MT && fix == FX) {                                          \
+        if (L.step)                                                              \
+            kern = fma ? k_advect_xmarch<true, true, MT, FX>                     \
+                       : k_advect_xmarch<false, true, MT, FX>;                   \
+        else                                                                     \
+            kern = fma ? k_advect_xmarch<true, false, MT, FX>                    \
+                       : k_advect_xmarch<false, false, MT, FX>;                  \
     }
-        PWADV_PICK(512)
-        PWADV_PICK(384)
-        PWADV_PICK(256)
+        PWADV_PICK(384, false)
+        PWADV_PICK(384, true)
+        PWADV_PICK(256, false)
+        PWADV_PICK(256, true)
+        PWADV_PICK(192, false)
+        PWADV_PICK(192, true)
+        PWADV_PICK(128, false)
+        PWADV_PICK(128, true)
 #undef PWADV_PICK
         if (!kern) return set_error(PWADV_E_ARG, "unsupported thread budget %d", plan.maxt);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -420,20 +562,23 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     // thread budget per CTA (register file / CTA): 384 by default, which
     // leaves ~168 registers per thread for the rolled x-window
     int maxt = L.max_threads > 0 ? L.max_threads : 384;
-    if (maxt != 512 && maxt != 384 && maxt != 256) return false;
+    if (maxt != 384 && maxt != 256 && maxt != 192 && maxt != 128) return false;
+    const int per_sm = ctas_per_sm(maxt);
     if (kp > maxt) return false;
     int tj = L.tile_j > 0 ? L.tile_j : maxt / kp;
     if (tj > maxt / kp) tj = maxt / kp;
     if (tj < 1) return false;
     if (tj > nby) tj = (int)nby;
-    const size_t bar_bytes = 2 * 16 * sizeof(uint64_t);
-    const size_t smem_cap = (size_t)dev.smem_optin - bar_bytes - 1024;
+    const size_t bar_bytes = 16 * sizeof(uint64_t) + sizeof(RingState);
+    // shared memory per CTA: the SM's 228 KB split between resident CTAs
+    size_t smem_cap = (size_t)dev.smem_optin - bar_bytes - 1024;
+    if (per_sm > 1) smem_cap = (size_t)(228 * 1024) / per_sm - bar_bytes - 1024 - 1024;
     int stages = 0;
     for (;;) {
         const size_t stage_bytes = (size_t)3 * (tj + 2) * nz * sizeof(double);
         int smax = (int)(smem_cap / stage_bytes);
-        if (smax > 8) smax = 8;
-        stages = L.stages > 0 ? (L.stages < smax ? L.stages : smax) : smax;
+        if (smax > 16) smax = 16;  // RingState::released
+        stages = L.stages > 0 ? (L.stages < smax ? L.stages : smax) : (smax < 8 ? smax : 8);
         if (stages >= 3) break;
         if (tj == 1) return false;
         tj = tj / 2;
@@ -443,14 +588,34 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     p->kp = kp;
     p->stages = stages;
     p->threads = round_up(tj * kp, 32);
-    p->smem = (size_t)stages * 3 * (tj + 2) * nz * sizeof(double) + 2 * stages * sizeof(uint64_t);
+    p->smem = (size_t)stages * 3 * (tj + 2) * nz * sizeof(double) + stages * sizeof(uint64_t) +
+              sizeof(RingState);
     p->nstrips = (nby + tj - 1) / tj;
-    const int64_t work = p->nstrips * nbx;
-    int64_t grid = L.grid > 0 ? L.grid : (int64_t)dev.sms;  // one resident CTA per SM
-    const int64_t min_planes = 4;
-    int64_t cap = (work + min_planes - 1) / min_planes;
-    if (L.grid <= 0 && grid > cap) grid = cap;
-    if (grid > work) grid = work;
+    // X chunking of the (chunk, strip) work units dealt round-robin to the
+    // grid: minimise rounds x (planes per unit + 2 boundary planes at half
+    // cost, they are L2 hits), i.e. balance the last round against the
+    // per-unit prologue.
+    const int64_t g0 = L.grid > 0 ? L.grid : (int64_t)dev.sms * per_sm;  // one wave of resident CTAs
+    int64_t best_nch = 1;
+    double best_cost = 1e300;
+    const int64_t nch_max = nbx < 4096 ? nbx : 4096;
+    for (int64_t nch = L.chunks > 0 ? (L.chunks < nch_max ? L.chunks : nch_max) : 1; nch <= nch_max;
+         ++nch) {
+        const int64_t units = p->nstrips * nch;
+        const int64_t g = units < g0 ? units : g0;
+        const int64_t rounds = (units + g - 1) / g;
+        if (rounds > kMaxUnitsPerCta) break;
+        const int64_t lmax = (nbx + nch - 1) / nch;
+        const double cost = (double)rounds * ((double)lmax + 1.0);
+        if (cost < best_cost * 0.999) {
+            best_cost = cost;
+            best_nch = nch;
+        }
+        if (L.chunks > 0) break;
+    }
+    p->nchunks = (int)best_nch;
+    const int64_t units = p->nstrips * best_nch;
+    int64_t grid = units < g0 ? units : g0;
     if (grid < 1) grid = 1;
     p->grid = (int)grid;
     return true;

@@ -111,7 +111,9 @@ static int run_box(const double *u, const double *v, const double *w, double *o0
     L.stages = opts ? opts->stages : 0;
     L.grid = opts ? opts->grid : 0;
     L.max_threads = opts ? opts->max_threads : 0;
-    if (L.tile_j < 0 || L.stages < 0 || L.grid < 0 || L.max_threads < 0)
+    L.chunks = opts ? opts->chunks : 0;
+    L.trace = opts ? opts->trace : nullptr;
+    if (L.tile_j < 0 || L.stages < 0 || L.grid < 0 || L.max_threads < 0 || L.chunks < 0)
         return set_error(PWADV_E_ARG, "negative tuning value");
     return launch_box(L, (cudaStream_t)stream);
 }
@@ -197,6 +199,7 @@ int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz, int64_t x0, int64_t 
     L.stages = opts ? opts->stages : 0;
     L.grid = opts ? opts->grid : 0;
     L.max_threads = opts ? opts->max_threads : 0;
+    L.chunks = opts ? opts->chunks : 0;
     XmarchPlan p{};
     *out = pwadv_plan_info{};
     if (plan_xmarch(L, *dev, &p)) {
@@ -208,6 +211,7 @@ int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz, int64_t x0, int64_t 
         out->grid = p.grid;
         out->smem_bytes = (int64_t)p.smem;
         out->strips = p.nstrips;
+        out->chunks = p.nchunks;
     } else {
         out->kernel = 2;
         out->threads = 256;
@@ -392,7 +396,7 @@ int pwadv_ctx_advect_host(pwadv_ctx *c, const double *u, const double *v, const 
                             c->s_h2d);
     if (e != cudaSuccess) return set_cuda_error("coefficient upload", e);
     h2d += 2 * nz * sizeof(double);
-    pwadv_opts o = opts ? *opts : pwadv_opts{0u, 0, 0, 0, 0};
+    pwadv_opts o = opts ? *opts : pwadv_opts{0u, 0, 0, 0, 0, 0, nullptr};
     int64_t copied = 0;  // input planes [0, copied) are on the device
     int64_t base = nx / chunks, rem = nx % chunks, x = 1;
     for (int ch = 0; ch < chunks; ++ch) {

@@ -159,12 +159,10 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, u
         : "memory");
 }
 
-__device__ __forceinline__ void store2(double *p, double a, double b, bool streaming)
+// outputs are written once and not re-read by this kernel: evict-first stores
+__device__ __forceinline__ void store2(double *p, double a, double b)
 {
-    if (streaming)
-        __stcs(reinterpret_cast<double2 *>(p), make_double2(a, b));
-    else
-        *reinterpret_cast<double2 *>(p) = make_double2(a, b);
+    __stcs(reinterpret_cast<double2 *>(p), make_double2(a, b));
 }
 
 }  // namespace pwadv

@@ -25,11 +25,12 @@ struct BoxLaunch {
     int64_t x0, x1, y0, y1;
     bool step;
     uint32_t flags;
-    int tile_j, stages, grid, max_threads;
+    int tile_j, stages, grid, max_threads, chunks;
+    void *trace;
 };
 
 struct XmarchPlan {
-    int maxt, tj, kp, stages, threads, grid;
+    int maxt, tj, kp, stages, threads, grid, nchunks;
     size_t smem;
     int64_t nstrips;
 };

@@ -87,7 +87,7 @@ def _as_device_coeffs(coeffs, device) -> DeviceCoefficients:
 
 
 def make_opts(variant: str = "xmarch", *, tile_j: int = 0, stages: int = 0, grid: int = 0,
-              max_threads: int = 0, streaming: bool = True) -> _lib.Opts:
+              max_threads: int = 0, chunks: int = 0) -> _lib.Opts:
     """Kernel selection: "xmarch" (bulk-copy plane ring, default), "simple"
     (one thread per point); suffix "_fma" for the DFMA (not bit-exact) build."""
     flags = 0
@@ -99,9 +99,7 @@ def make_opts(variant: str = "xmarch", *, tile_j: int = 0, stages: int = 0, grid
         flags |= _lib.FLAG_SIMPLE
     elif base != "xmarch":
         raise ValueError(f"unknown kernel variant {variant!r}")
-    if not streaming:
-        flags |= _lib.FLAG_NO_STREAMING
-    return _lib.Opts(flags, tile_j, stages, grid, max_threads)
+    return _lib.Opts(flags, tile_j, stages, grid, max_threads, chunks, None)
 
 
 def _box(dims: GridDims, box):
@@ -201,7 +199,7 @@ def describe_plan(dims: GridDims, box=None, opts: _lib.Opts | None = None, devic
     return {"kernel": {1: "xmarch", 2: "simple"}[info.kernel], "tile_j": info.tile_j,
             "threads_per_column": info.threads_per_column, "stages": info.stages,
             "threads": info.threads, "grid": info.grid, "smem_bytes": info.smem_bytes,
-            "strips": info.strips}
+            "strips": info.strips, "chunks": info.chunks}
 
 
 class HostContext:

@@ -117,19 +117,14 @@ def plan_traffic(dims: GridDims, box, plan: dict) -> TrafficReport:
         # 27 distinct operands per point at k >= 1 (9 per field), via L1/L2
         tr.external_reads = 27 * nbx * nby * (nz - 1)
         return tr
-    tj, g = plan["tile_j"], plan["grid"]
+    tj, g, nch = plan["tile_j"], plan["grid"], plan.get("chunks", 1)
     nstrips = plan["strips"]
-    W = nstrips * nbx
     widths = [min(tj, nby - s * tj) for s in range(nstrips)]
     planes = 0
-    for b in range(g):
-        wb, we = W * b // g, W * (b + 1) // g
-        if wb >= we:
-            continue
-        for s in range(wb // nbx, (we - 1) // nbx + 1):
-            ib = max(wb - s * nbx, 0)
-            ie = min(we - s * nbx, nbx)
-            planes += (ie - ib + 2) * (widths[s] + 2)
+    for u in range(nstrips * nch):  # (chunk, strip) units, each streams its chunk + 2 planes
+        chunk, s = divmod(u, nstrips)
+        ib, ie = nbx * chunk // nch, nbx * (chunk + 1) // nch
+        planes += (ie - ib + 2) * (widths[s] + 2)
     tr.external_reads = 3 * nz * planes
     tr.local_writes = tr.external_reads
     # 9 paired shared loads per thread per plane step (2 points) = 9 per point

@@ -159,18 +159,21 @@ def test_dual_oracle_property_loop(variant):
         assert_bitwise(got, oracle.advect(u, v, w, *co), (nx, ny, nz))
 
 
-@pytest.mark.parametrize("tile_j,stages,grid,maxt", [(0, 0, 0, 0), (1, 3, 7, 0), (3, 4, 0, 256),
-                                                     (5, 3, 1, 512), (2, 0, 300, 384)])
-def test_xmarch_tilings_bitwise(tile_j, stages, grid, maxt):
-    # every tiling / ring depth / grid split gives identical bits (segments
-    # crossing strip boundaries, partial strips, single-CTA and over-split grids)
-    for (nx, ny, nz, seed) in ((37, 29, 64, 3), (13, 40, 8, 9), (6, 5, 2, 1), (20, 18, 128, 5)):
+@pytest.mark.parametrize("tile_j,stages,grid,maxt,chunks", [
+    (0, 0, 0, 0, 0), (1, 3, 7, 0, 0), (3, 4, 0, 256, 1), (5, 3, 1, 192, 3), (2, 0, 300, 384, 0),
+    (0, 0, 5, 128, 7), (4, 5, 2, 0, 40), (0, 3, 0, 0, 1000), (0, 0, 0, 192, 0)])
+def test_xmarch_tilings_bitwise(tile_j, stages, grid, maxt, chunks):
+    # every tiling / ring depth / grid / chunking gives identical bits (units
+    # dealt round-robin, CTAs running several units, partial strips, single-CTA
+    # grids, more chunks than planes)
+    for (nx, ny, nz, seed) in ((37, 29, 64, 3), (13, 40, 8, 9), (6, 5, 2, 1), (20, 18, 128, 5),
+                               (9, 30, 6, 2)):
         u, v, w = oracle.fill_random(nx, ny, nz, seed, baseline=True)
         co = oracle.baseline_coefficients(seed, nz)
         args = (co["tcx"], co["tcy"], co["tzc1"], co["tzc2"])
         got, dims = gpu_advect(u, v, w, *args, "xmarch", tile_j=tile_j, stages=stages, grid=grid,
-                               max_threads=maxt)
-        assert_bitwise(got, oracle.advect(u, v, w, *args), (nx, ny, nz, tile_j, stages, grid))
+                               max_threads=maxt, chunks=chunks)
+        assert_bitwise(got, oracle.advect(u, v, w, *args), (nx, ny, nz, tile_j, stages, grid, chunks))
 
 
 def test_bottom_level_zero_and_translation_equivariance():

@@ -208,7 +208,8 @@ def test_compare_outputs_semantics():
 
 def test_plan_traffic_accounting():
     dims = pw.make_grid(512, 512, 64)
-    plan = {"kernel": "xmarch", "tile_j": 12, "grid": 148, "strips": 43, "smem_bytes": 200000}
+    plan = {"kernel": "xmarch", "tile_j": 12, "grid": 148, "strips": 43, "smem_bytes": 200000,
+            "chunks": 10}
     tr = plan_traffic(dims, (1, 513, 1, 513), plan)
     interior_in = 3 * 512 * 512 * 64
     # staged input traffic is within (1 + halo columns + boundary planes) of the interior

@@ -1,0 +1,91 @@
+"""Tuning sweep for K1/K4 on one GPU: prints one JSON line per variant.
+
+    python tools/sweep.py [--config c1] [--reps 50]
+"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import torch  # noqa: E402
+
+import paper_2010_01545_b200 as pw  # noqa: E402
+from paper_2010_01545_b200 import device  # noqa: E402
+
+SHAPES = {"c1": (512, 512, 64), "c2": (1024, 1024, 64), "c3": (2048, 2048, 64),
+          "c4blk": (2048, 1024, 128), "c0": (64, 64, 64)}
+
+
+def time_it(fn, reps):
+    for _ in range(5):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c1")
+    ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--ablate", action="store_true")
+    args = ap.parse_args()
+    nx, ny, nz = SHAPES[args.config]
+    dims = pw.make_grid(nx, ny, nz)
+    fields = device.fill(dims, pw.GeneratorSpec.baseline(42))
+    co = device.DeviceCoefficients.from_host(pw.baseline_coefficients(42, nz), fields[0].device)
+    out = device.alloc_fields(dims, fields[0].device)
+    ref = None
+    variants = [dict(variant="xmarch")]
+    for ch in (1, 2, 4, 8, 16, 32):
+        variants.append(dict(variant="xmarch", chunks=ch))
+    for maxt, stages in ((384, 3), (384, 4), (384, 6), (384, 10), (256, 0), (256, 12)):
+        variants.append(dict(variant="xmarch", max_threads=maxt, stages=stages))
+    for tj in (8, 10, 11):
+        variants.append(dict(variant="xmarch", tile_j=tj))
+    variants += [dict(variant="xmarch_fma"), dict(variant="simple"), dict(variant="simple_fma")]
+    if args.ablate:
+        variants = [dict(variant="xmarch"), dict(variant="xmarch", debug=1)]
+        for st in (3, 4, 6, 8, 10):
+            variants += [dict(variant="xmarch", stages=st, debug=5), dict(variant="xmarch", stages=st, debug=4)]
+        for mt in (192, 128):
+            variants += [dict(variant="xmarch", max_threads=mt, debug=5)]
+    for v in variants:
+        kw = dict(v)
+        name = kw.pop("variant")
+        dbg = kw.pop("debug", 0)
+        opts = device.make_opts(name, **kw)
+        opts.flags |= dbg << 8
+        try:
+            plan = device.describe_plan(dims, None, opts)
+            ms = time_it(lambda: device.advect(*fields, co, out, opts=opts), args.reps)
+        except Exception as e:  # noqa: BLE001
+            print(json.dumps({"variant": v, "error": str(e)}))
+            continue
+        snap = [o.clone() for o in out]
+        if ref is None:
+            ref = snap
+        same = all(torch.equal(a.view(torch.int64), b.view(torch.int64)) for a, b in zip(ref, snap))
+        gbs = 48 * dims.cells / (ms / 1e3) / 1e9
+        print(json.dumps({"config": args.config, "variant": v, "ms": round(ms, 4),
+                          "gpts": round(dims.cells / ms / 1e6, 2), "GBs": round(gbs, 1),
+                          "bitwise_same_as_first": same, "plan": plan}), flush=True)
+    # fused step K4
+    nxt = device.alloc_fields(dims, fields[0].device)
+    ms = time_it(lambda: device.step(*fields, co, 0.1, nxt), args.reps)
+    print(json.dumps({"config": args.config, "variant": "step_k4", "ms": round(ms, 4),
+                      "gpts": round(dims.cells / ms / 1e6, 2),
+                      "GBs": round(48 * dims.cells / (ms / 1e3) / 1e9, 1)}), flush=True)
+    ms = time_it(lambda: device.wrap_halos(*fields), args.reps)
+    print(json.dumps({"config": args.config, "variant": "wrap3", "ms": round(ms, 4)}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
