@@ -592,26 +592,25 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
               sizeof(RingState);
     p->nstrips = (nby + tj - 1) / tj;
     // X chunking of the (chunk, strip) work units dealt round-robin to the
-    // grid: minimise rounds x (planes per unit + 2 boundary planes at half
-    // cost, they are L2 hits), i.e. balance the last round against the
-    // per-unit prologue.
+    // grid. Measured on B200 (tools/sweep.py, profiles/): long units stream
+    // faster per plane than short ones, so take the fewest chunks whose
+    // units fill >= 90% of the grid's CTA slots over all rounds (C1 -> 10
+    // chunks, 2048-plane grids -> 4); if none does, the best filling one.
     const int64_t g0 = L.grid > 0 ? L.grid : (int64_t)dev.sms * per_sm;  // one wave of resident CTAs
     int64_t best_nch = 1;
-    double best_cost = 1e300;
+    double best_fill = -1.0;
     const int64_t nch_max = nbx < 4096 ? nbx : 4096;
     for (int64_t nch = L.chunks > 0 ? (L.chunks < nch_max ? L.chunks : nch_max) : 1; nch <= nch_max;
          ++nch) {
         const int64_t units = p->nstrips * nch;
-        const int64_t g = units < g0 ? units : g0;
-        const int64_t rounds = (units + g - 1) / g;
+        const int64_t rounds = (units + g0 - 1) / g0;
         if (rounds > kMaxUnitsPerCta) break;
-        const int64_t lmax = (nbx + nch - 1) / nch;
-        const double cost = (double)rounds * ((double)lmax + 1.0);
-        if (cost < best_cost * 0.999) {
-            best_cost = cost;
+        const double fill = (double)units / (double)(rounds * g0);
+        if (fill > best_fill + 1e-9) {
+            best_fill = fill;
             best_nch = nch;
         }
-        if (L.chunks > 0) break;
+        if (L.chunks > 0 || fill >= 0.9) break;
     }
     p->nchunks = (int)best_nch;
     const int64_t units = p->nstrips * best_nch;

@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--config", default="c1")
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--ablate", action="store_true")
+    ap.add_argument("--variants", default="", help="JSON list of variant dicts (overrides)")
     args = ap.parse_args()
     nx, ny, nz = SHAPES[args.config]
     dims = pw.make_grid(nx, ny, nz)
@@ -51,6 +52,8 @@ def main():
     for tj in (8, 10, 11):
         variants.append(dict(variant="xmarch", tile_j=tj))
     variants += [dict(variant="xmarch_fma"), dict(variant="simple"), dict(variant="simple_fma")]
+    if args.variants:
+        variants = json.loads(args.variants)
     if args.ablate:
         variants = [dict(variant="xmarch"), dict(variant="xmarch", debug=1)]
         for st in (3, 4, 6, 8, 10):
