@@ -236,8 +236,7 @@ def run_ours(args):
         exch = decomp.HaloExchanger(dec, dev)
         if stepping:
             from paper_2010_01545_b200.stepper import Stepper
-            st = Stepper(fields, co, 0.1, opts=opts,
-                         exchange=lambda f, s=None: exch.exchange(f, stream=s))
+            st = Stepper(fields, co, 0.1, opts=opts, exchanger=exch)
 
             def one_step():
                 st._one(stream)

@@ -151,6 +151,14 @@ int pwadv_wrap_halos3_f64(double *u, double *v, double *w,
 int pwadv_fill_f64(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
                    int32_t mode, uint64_t seed, double a, double b, double c, void *stream);
 
+/* K5 on one block of an x-y decomposition: fills the interior columns of the
+ * local (nx, ny, nz) arrays with global columns (x_off+1 .. x_off+nx,
+ * y_off+1 .. y_off+ny) of the (gnx, gny, nz) grid's stream. Halos are left
+ * for the halo exchange. */
+int pwadv_fill_box_f64(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
+                       int64_t gnx, int64_t gny, int64_t x_off, int64_t y_off, int32_t mode,
+                       uint64_t seed, double a, double b, double c, void *stream);
+
 /* Halo exchange helpers (multi-GPU x-y decomposition).
  * Y faces are (nx+2) runs of nz doubles at stride (ny+2)*nz: pack the column
  * j (all i in 0..nx+1) of u, v, w into buf[3][nx+2][nz], or unpack into it. */

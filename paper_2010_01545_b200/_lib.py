@@ -70,6 +70,8 @@ SIGNATURES = {
     "pwadv_wrap_axis3_f64": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, ctypes.c_int32, _P]),
     "pwadv_fill_f64": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, ctypes.c_int32,
                                       ctypes.c_uint64, _D, _D, _D, _P]),
+    "pwadv_fill_box_f64": (ctypes.c_int, [_P, _P, _P] + [_I64] * 7 + [ctypes.c_int32, ctypes.c_uint64,
+                                                                      _D, _D, _D, _P]),
     "pwadv_pack_yface3_f64": (ctypes.c_int, [_P] * 4 + [_I64] * 4 + [_P]),
     "pwadv_unpack_yface3_f64": (ctypes.c_int, [_P] * 4 + [_I64] * 4 + [_P]),
     "pwadv_pack_xface3_f64": (ctypes.c_int, [_P] * 4 + [_I64] * 4 + [_P]),

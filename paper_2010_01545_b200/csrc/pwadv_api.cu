@@ -256,6 +256,22 @@ int pwadv_fill_f64(double *u, double *v, double *w, int64_t nx, int64_t ny, int6
     return launch_fill(u, v, w, nx, ny, nz, mode, seed, a, b, c, (cudaStream_t)stream);
 }
 
+int pwadv_fill_box_f64(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
+                       int64_t gnx, int64_t gny, int64_t x_off, int64_t y_off, int32_t mode,
+                       uint64_t seed, double a, double b, double c, void *stream)
+{
+    int rc = check_dims(nx, ny, nz);
+    if (rc) return rc;
+    if ((rc = check_ptrs({u, v, w}))) return rc;
+    if (mode < 0 || mode > 2) return set_error(PWADV_E_ARG, "unknown generator mode %d", mode);
+    if (x_off < 0 || y_off < 0 || x_off + nx > gnx || y_off + ny > gny)
+        return set_error(PWADV_E_RANGE, "block [%lld,+%lld)x[%lld,+%lld) outside global %lldx%lld",
+                         (long long)x_off, (long long)nx, (long long)y_off, (long long)ny,
+                         (long long)gnx, (long long)gny);
+    return launch_fill_box(u, v, w, nx, ny, nz, gnx, gny, x_off, y_off, mode, seed, a, b, c,
+                           (cudaStream_t)stream);
+}
+
 static int face(const double *u, const double *v, const double *w, double *buf, int64_t nx,
                 int64_t ny, int64_t nz, int axis, int64_t index, bool pack, void *stream)
 {

@@ -138,10 +138,15 @@ __device__ __forceinline__ uint64_t lcg_skip(uint64_t seed, uint64_t steps)
 
 static constexpr int kFillRun = 8;  // consecutive stream values per thread
 
+// Fill the interior columns of a local (nx, ny) block whose interior column
+// (i, j) is global column (x_off + i, y_off + j) of a (gnx, gny) grid: the
+// stream index of a value is that of the global grid, so every block of a
+// decomposition holds exactly its part of the global fields.
 __global__ void k_fill_lcg(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
-                           uint64_t seed, int baseline)
+                           int64_t gnx, int64_t gny, int64_t x_off, int64_t y_off, uint64_t seed,
+                           int baseline)
 {
-    const int64_t cells = nx * ny * nz;
+    const int64_t cells = gnx * gny * nz;
     const int64_t runs_per_col = (nz + kFillRun - 1) / kFillRun;
     const int64_t total = 3 * nx * ny * runs_per_col;
     double *fs[3] = {u, v, w};
@@ -153,7 +158,8 @@ __global__ void k_fill_lcg(double *u, double *v, double *w, int64_t nx, int64_t 
         const int64_t q = col - m * nx * ny;      // interior column, C order over (i, j)
         const int64_t i = 1 + q / ny, j = 1 + q % ny;
         const int64_t kb = r * kFillRun;
-        const int64_t n0 = m * cells + q * nz + kb;  // stream index of the first value
+        const int64_t gq = (x_off + i - 1) * gny + (y_off + j - 1);  // global interior column
+        const int64_t n0 = m * cells + gq * nz + kb;  // stream index of the first value
         uint64_t s = lcg_skip(seed, (uint64_t)n0);
         double *dst = fs[m] + (i * (ny + 2) + j) * nz;
         for (int t = 0; t < kFillRun; ++t) {
@@ -230,6 +236,15 @@ int launch_face3(double *u, double *v, double *w, double *buf, int64_t nx, int64
 int launch_fill(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz, int mode,
                 uint64_t seed, double a, double b, double c, cudaStream_t s)
 {
+    int rc = launch_fill_box(u, v, w, nx, ny, nz, nx, ny, 0, 0, mode, seed, a, b, c, s);
+    if (rc || mode == 2) return rc;
+    return launch_wrap3(u, v, w, 3, nx, ny, nz, s);
+}
+
+int launch_fill_box(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
+                    int64_t gnx, int64_t gny, int64_t x_off, int64_t y_off, int mode, uint64_t seed,
+                    double a, double b, double c, cudaStream_t s)
+{
     if (mode == 2) {
         const int64_t n = (nx + 2) * (ny + 2) * nz;
         k_fill_uniform<<<grid_for(n, 256), 256, 0, s>>>(u, v, w, n, a, b, c);
@@ -237,10 +252,9 @@ int launch_fill(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t
     }
     const int64_t runs = (nz + kFillRun - 1) / kFillRun;
     const int64_t total = 3 * nx * ny * runs;
-    k_fill_lcg<<<grid_for(total, 256), 256, 0, s>>>(u, v, w, nx, ny, nz, seed, mode == 1);
-    int rc = check_launch("fill_lcg");
-    if (rc) return rc;
-    return launch_wrap3(u, v, w, 3, nx, ny, nz, s);
+    k_fill_lcg<<<grid_for(total, 256), 256, 0, s>>>(u, v, w, nx, ny, nz, gnx, gny, x_off, y_off, seed,
+                                                    mode == 1);
+    return check_launch("fill_lcg");
 }
 
 }  // namespace pwadv

@@ -1,0 +1,402 @@
+"""x-y domain decomposition with a 1-cell periodic halo exchange.
+
+The reference parallelises only over X slabs of threads sharing one array
+(schedules.py:65-75, 207-232); MONC halo-swaps every prognostic field between
+MPI ranks before advection. Here the global interior is split
+into a px x py grid of blocks, one per GPU (rank = cx*py + cy, x = i is the
+slowest axis; "AxB" means px x py). Each rank holds a padded local block of
+shape (nx_l+2, ny_l+2, nz) in the reference layout; k is never split.
+
+The exchange reproduces `wrap_halos` (grid.py:203-208) exactly, with no
+diagonal messages, in two phases:
+
+  X: my plane 1 -> the x- neighbour's halo plane nx+1, my plane nx -> the x+
+     neighbour's halo plane 0 (all j, including the stale y halos);
+  Y: my column 1 -> the y- neighbour's halo column ny+1, my column ny -> the
+     y+ neighbour's halo column 0, for every i including the X halos just
+     received — which carries the corner values (u(x-lo, y-hi), v(x-hi, y-lo)
+     are the corners the stencil reads, SURVEY.md probe P4).
+
+An undivided axis (p = 1) is a local periodic copy (K2 per axis). Faces are
+packed/unpacked by libpwadv kernels (CUDA) or by tensor slicing (CPU, for the
+gloo tests); messages go through a Transport: NCCL point-to-point via
+torch.distributed (one process per GPU), gloo on CPU, or an in-process
+loopback hub that emulates several ranks on one device for the tests.
+
+`advect_overlapped` runs the exchange on a side stream while K1 computes the
+interior box whose stencil stays inside the block, then computes the
+one-cell rim. Outputs are bitwise identical to a single-domain evaluation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from .layout import GridDims, make_grid
+
+__all__ = ["split_extent", "Decomposition", "TorchFaceOps", "CudaFaceOps", "DistTransport",
+           "LoopbackHub", "HaloExchanger", "exchange_all_loopback"]
+
+
+def split_extent(n: int, parts: int) -> list[tuple[int, int]]:
+    """Balanced contiguous split of n cells into (offset, length), wider first
+    (the rule of partition_domain, schedules.py:65-75)."""
+    if not 1 <= parts <= n:
+        raise ValueError(f"cannot split {n} cells into {parts} parts")
+    q, r = divmod(n, parts)
+    out, off = [], 0
+    for p in range(parts):
+        ln = q + (1 if p < r else 0)
+        out.append((off, ln))
+        off += ln
+    return out
+
+
+@dataclass(frozen=True)
+class Decomposition:
+    global_dims: GridDims
+    px: int
+    py: int
+    rank: int
+
+    def __post_init__(self):
+        if self.px < 1 or self.py < 1:
+            raise ValueError("px, py must be >= 1")
+        if not 0 <= self.rank < self.px * self.py:
+            raise ValueError(f"rank {self.rank} outside a {self.px}x{self.py} decomposition")
+        split_extent(self.global_dims.nx, self.px)
+        split_extent(self.global_dims.ny, self.py)
+
+    @property
+    def size(self) -> int:
+        return self.px * self.py
+
+    @property
+    def coords(self) -> tuple[int, int]:
+        return divmod(self.rank, self.py)
+
+    def rank_of(self, cx: int, cy: int) -> int:
+        return (cx % self.px) * self.py + (cy % self.py)
+
+    def block(self, rank: int | None = None) -> tuple[int, int, int, int]:
+        """(x_off, nx_l, y_off, ny_l) of a rank's interior (0-based offsets)."""
+        r = self.rank if rank is None else rank
+        cx, cy = divmod(r, self.py)
+        xo, nxl = split_extent(self.global_dims.nx, self.px)[cx]
+        yo, nyl = split_extent(self.global_dims.ny, self.py)[cy]
+        return xo, nxl, yo, nyl
+
+    @property
+    def local_dims(self) -> GridDims:
+        _, nxl, _, nyl = self.block()
+        return make_grid(nxl, nyl, self.global_dims.nz)
+
+    @property
+    def neighbours(self) -> dict:
+        cx, cy = self.coords
+        return {"xm": self.rank_of(cx - 1, cy), "xp": self.rank_of(cx + 1, cy),
+                "ym": self.rank_of(cx, cy - 1), "yp": self.rank_of(cx, cy + 1)}
+
+    def for_rank(self, rank: int) -> "Decomposition":
+        return Decomposition(self.global_dims, self.px, self.py, rank)
+
+    # -- data placement -----------------------------------------------------
+    def local_view(self, padded_global):
+        """The rank's padded block cut from a wrapped global padded array: its
+        halos are the neighbours' edge cells / the periodic images."""
+        xo, nxl, yo, nyl = self.block()
+        return padded_global[xo:xo + nxl + 2, yo:yo + nyl + 2, :]
+
+    def fill_local(self, spec, device=None, stream=None):
+        """Device fields of this block, generated from the global stream (K5);
+        halos are filled by the first exchange."""
+        from . import _lib, device as dv
+        dims = self.local_dims
+        out = dv.alloc_fields(dims, device or "cuda", zero=True)
+        if spec.mode == "uniform":
+            return dv.fill(dims, spec, device=device, stream=stream, out=out)
+        code = {"random": 0, "baseline": 1}[spec.mode]
+        xo, _, yo, _ = self.block()
+        g = self.global_dims
+        _lib.check(_lib.lib().pwadv_fill_box_f64(
+            dv._p(out[0]), dv._p(out[1]), dv._p(out[2]), dims.nx, dims.ny, dims.nz, g.nx, g.ny, xo,
+            yo, code, int(spec.seed) & (2**64 - 1), float(spec.a), float(spec.b), float(spec.c),
+            dv._stream_handle(stream, out[0].device)))
+        return out
+
+
+# ---------------------------------------------------------------------------
+# face pack/unpack backends
+
+class TorchFaceOps:
+    """Tensor-slicing pack/unpack (CPU tensors; used by the gloo tests)."""
+
+    @staticmethod
+    def pack(fields, buf, axis: int, index: int, stream=None) -> None:
+        for m, f in enumerate(fields):
+            src = f[index] if axis == 0 else f[:, index]
+            buf[m].copy_(src.reshape(-1))
+
+    @staticmethod
+    def unpack(fields, buf, axis: int, index: int, stream=None) -> None:
+        for m, f in enumerate(fields):
+            dst = f[index] if axis == 0 else f[:, index]
+            dst.copy_(buf[m].view_as(dst))
+
+    @staticmethod
+    def wrap_axis(fields, axis: int, stream=None) -> None:
+        for f in fields:
+            if axis == 0:
+                f[0].copy_(f[-2])
+                f[-1].copy_(f[1])
+            else:
+                f[:, 0].copy_(f[:, -2])
+                f[:, -1].copy_(f[:, 1])
+
+
+class CudaFaceOps:
+    """libpwadv pack/unpack kernels (one launch packs u, v and w)."""
+
+    @staticmethod
+    def _call(name, fields, buf, axis, index, stream):
+        from . import _lib, device as dv
+        d = dv.dims_of(fields[0])
+        fn = getattr(_lib.lib(), name)
+        _lib.check(fn(dv._p(fields[0]), dv._p(fields[1]), dv._p(fields[2]), dv._p(buf), d.nx, d.ny,
+                      d.nz, int(index), dv._stream_handle(stream, fields[0].device)))
+
+    @classmethod
+    def pack(cls, fields, buf, axis, index, stream=None):
+        cls._call("pwadv_pack_xface3_f64" if axis == 0 else "pwadv_pack_yface3_f64",
+                  fields, buf, axis, index, stream)
+
+    @classmethod
+    def unpack(cls, fields, buf, axis, index, stream=None):
+        cls._call("pwadv_unpack_xface3_f64" if axis == 0 else "pwadv_unpack_yface3_f64",
+                  fields, buf, axis, index, stream)
+
+    @staticmethod
+    def wrap_axis(fields, axis, stream=None):
+        from . import _lib, device as dv
+        d = dv.dims_of(fields[0])
+        _lib.check(_lib.lib().pwadv_wrap_axis3_f64(
+            dv._p(fields[0]), dv._p(fields[1]), dv._p(fields[2]), d.nx, d.ny, d.nz, int(axis),
+            dv._stream_handle(stream, fields[0].device)))
+
+
+# ---------------------------------------------------------------------------
+# transports. An op is (kind, tensor, peer, tag): kind "send" or "recv"; tag 0
+# marks a message travelling toward the minus neighbour, 1 toward the plus one.
+
+class DistTransport:
+    """torch.distributed point-to-point (NCCL between GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.backend = dist.get_backend(group)
+
+    def run(self, ops) -> None:
+        dist = self.dist
+        if not ops:
+            return
+        if self.backend == "nccl":
+            # one NCCL group; sends/recvs between a pair match in posting order
+            p2p = [dist.P2POp(dist.isend if k == "send" else dist.irecv, t, peer, self.group)
+                   for k, t, peer, _ in ops]
+            for req in dist.batch_isend_irecv(p2p):
+                req.wait()
+        else:
+            reqs = [(dist.isend if k == "send" else dist.irecv)(t, peer, group=self.group, tag=tag)
+                    for k, t, peer, tag in ops]
+            for r in reqs:
+                r.wait()
+
+
+class LoopbackHub:
+    """Emulates the ranks of a decomposition inside one process: every posted
+    send is matched to the recv with the same (src, dst, tag), in order."""
+
+    def run_all(self, ops_by_rank: dict) -> None:
+        queues: dict = {}
+        for r, ops in ops_by_rank.items():
+            for k, t, peer, tag in ops:
+                if k == "send":
+                    queues.setdefault((r, peer, tag), []).append(t)
+        for r, ops in ops_by_rank.items():
+            for k, t, peer, tag in ops:
+                if k == "recv":
+                    t.copy_(queues[(peer, r, tag)].pop(0))
+        left = sum(len(q) for q in queues.values())
+        if left:
+            raise RuntimeError(f"{left} unmatched loopback sends")
+
+
+class ThreadHubTransport:
+    """Emulates NCCL point-to-point for ranks run as host threads of one
+    process (several ranks on one GPU, for tests). Each rank calls `run` from
+    its own thread inside its stream context: sends are published with a CUDA
+    event, the ranks meet at a host barrier, each receiver's stream waits on
+    the sender's event and copies, and a second barrier plus events keep send
+    buffers alive until every receiver has copied. No kernel ever waits on
+    another rank's kernel (only streams wait on recorded events)."""
+
+    def __init__(self, nranks: int):
+        import threading
+        self.n = nranks
+        self.barrier = threading.Barrier(nranks)
+        self.lock = threading.Lock()
+        self.queues: dict = {}
+        self.done: dict = {}
+
+    def bind(self, rank: int) -> "_BoundHub":
+        return _BoundHub(self, rank)
+
+
+class _BoundHub:
+    def __init__(self, hub: ThreadHubTransport, rank: int):
+        self.hub, self.rank = hub, rank
+
+    def run(self, ops) -> None:
+        hub, me = self.hub, self.rank
+        cur = torch.cuda.current_stream()
+        ready = torch.cuda.Event()
+        ready.record(cur)
+        with hub.lock:
+            for k, t, peer, tag in ops:
+                if k == "send":
+                    hub.queues.setdefault((me, peer, tag), []).append((t, ready))
+        hub.barrier.wait()
+        for k, t, peer, tag in ops:
+            if k == "recv":
+                with hub.lock:
+                    src, ev = hub.queues[(peer, me, tag)].pop(0)
+                cur.wait_event(ev)
+                t.copy_(src)
+        copied = torch.cuda.Event()
+        copied.record(cur)
+        with hub.lock:
+            hub.done[me] = copied
+        hub.barrier.wait()
+        for ev in list(hub.done.values()):
+            cur.wait_event(ev)
+        hub.barrier.wait()
+
+
+# ---------------------------------------------------------------------------
+
+class HaloExchanger:
+    """Two-phase periodic halo exchange of (u, v, w) for one rank."""
+
+    def __init__(self, dec: Decomposition, device=None, transport=None, faceops=None):
+        self.dec = dec
+        d = dec.local_dims
+        self.dims = d
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.device = dev
+        self.faceops = faceops or (CudaFaceOps if dev.type == "cuda" else TorchFaceOps)
+        self.transport = transport  # default (torch.distributed) created on first use
+        xf, yf = (d.ny + 2) * d.nz, (d.nx + 2) * d.nz
+
+        def buf(n):
+            return torch.empty((3, n), dtype=torch.float64, device=dev)
+        self.xbuf = {k: buf(xf) for k in ("send_m", "send_p", "recv_m", "recv_p")}
+        self.ybuf = {k: buf(yf) for k in ("send_m", "send_p", "recv_m", "recv_p")}
+        self._side = torch.cuda.Stream(device=dev) if dev.type == "cuda" else None
+
+    # phase pieces (shared by the real transports and the loopback emulation)
+    def _axis(self, axis):
+        p = self.dec.px if axis == 0 else self.dec.py
+        n = self.dims.nx if axis == 0 else self.dims.ny
+        nb = self.dec.neighbours
+        m, pl = (nb["xm"], nb["xp"]) if axis == 0 else (nb["ym"], nb["yp"])
+        return p, n, m, pl, (self.xbuf if axis == 0 else self.ybuf)
+
+    def pre(self, fields, axis, stream=None) -> list:
+        p, n, m, pl, b = self._axis(axis)
+        if p == 1:
+            self.faceops.wrap_axis(fields, axis, stream)
+            return []
+        self.faceops.pack(fields, b["send_m"], axis, 1, stream)
+        self.faceops.pack(fields, b["send_p"], axis, n, stream)
+        # order matters when both neighbours are one rank (p == 2): the peer
+        # receives my first message into its plus-side halo
+        return [("send", b["send_m"], m, 0), ("send", b["send_p"], pl, 1),
+                ("recv", b["recv_p"], pl, 0), ("recv", b["recv_m"], m, 1)]
+
+    def post(self, fields, axis, stream=None) -> None:
+        p, n, _, _, b = self._axis(axis)
+        if p == 1:
+            return
+        self.faceops.unpack(fields, b["recv_p"], axis, n + 1, stream)
+        self.faceops.unpack(fields, b["recv_m"], axis, 0, stream)
+
+    def exchange(self, fields, stream=None) -> None:
+        """Refresh the halos of `fields` (X phase, then Y phase)."""
+        for axis in (0, 1):
+            ops = self.pre(fields, axis, stream)
+            if ops:
+                if self.transport is None:
+                    self.transport = DistTransport()
+                if self.device.type == "cuda":
+                    s = stream or torch.cuda.current_stream(self.device)
+                    with torch.cuda.stream(s):
+                        self.transport.run(ops)
+                else:
+                    self.transport.run(ops)
+            self.post(fields, axis, stream)
+
+    # -- compute with overlap ----------------------------------------------
+    def boxes(self):
+        """(interior box, rim boxes) in local 1-based interior coordinates."""
+        nx, ny = self.dims.nx, self.dims.ny
+        if nx < 3 or ny < 3:
+            return None, [(1, nx + 1, 1, ny + 1)]
+        inner = (2, nx, 2, ny)
+        rims = [(1, 2, 1, ny + 1), (nx, nx + 1, 1, ny + 1), (2, nx, 1, 2), (2, nx, ny, ny + 1)]
+        return inner, rims
+
+    def run_overlapped(self, launch, fields, stream=None) -> None:
+        """Exchange halos on a side stream while `launch(box, stream)` computes
+        the interior, then compute the rim once the halos have landed."""
+        from . import device as dv
+        main = stream or torch.cuda.current_stream(self.device)
+        side = self._side
+        inner, rims = self.boxes()
+        side.wait_stream(main)
+        self.exchange(fields, stream=side)
+        if inner is not None:
+            launch(inner, main)
+        main.wait_stream(side)
+        simple = dv.make_opts("simple")
+        for b in rims:
+            launch(b, main, simple)
+
+    def advect_overlapped(self, fields, coeffs, out, opts=None, stream=None) -> None:
+        from . import device as dv
+
+        def launch(box, s, o=None):
+            dv.advect(*fields, coeffs, out, box=box, opts=o or opts, stream=s)
+        self.run_overlapped(launch, fields, stream)
+
+    def step_overlapped(self, fields, coeffs, dt, out, opts=None, stream=None) -> None:
+        from . import device as dv
+
+        def launch(box, s, o=None):
+            dv.step(*fields, coeffs, dt, out, box=box, opts=o or opts, stream=s)
+        self.run_overlapped(launch, fields, stream)
+
+
+def exchange_all_loopback(exchangers: list, fields_by_rank: list, stream=None) -> None:
+    """Run one halo exchange for all emulated ranks of a decomposition in one
+    process (the same pack / message / unpack code as the real transports)."""
+    hub = LoopbackHub()
+    for axis in (0, 1):
+        ops = {ex.dec.rank: ex.pre(f, axis, stream) for ex, f in zip(exchangers, fields_by_rank)}
+        hub.run_all(ops)
+        for ex, f in zip(exchangers, fields_by_rank):
+            ex.post(f, axis, stream)

@@ -3,15 +3,17 @@
 The reference has no time integration; MONC integrates the
 source terms into the flow fields after advection. One step is
 
-    halo exchange / periodic wrap of (u, v, w)
+    refresh the halos of (u, v, w)        [K2 wrap, or the x-y halo exchange]
     (u', v', w') = (u, v, w) + dt * PW(u, v, w)         [K4, fused, ping-pong]
 
 so each step streams 48 B per point (3 fields in, 3 fields out) instead of
-the 120 B of advect-then-update. The composed oracle is
-run_reference + numpy `f + dt*s` + wrap_halos (tests/golden/make_golden.py).
+the 120 B of advect-then-update. With a decomposition the exchange runs on a
+side stream while K4 updates the interior (decomp.HaloExchanger). The
+composed oracle is run_reference + numpy `f + dt*s` + wrap_halos
+(tests/golden/make_golden.py).
 
-Steps can be captured once into a CUDA graph and replayed (`capture`), which
-removes per-step launch overhead for small per-GPU domains.
+Single-GPU steps can be captured once into a CUDA graph and replayed
+(`capture`), which removes per-step launch overhead for small domains.
 """
 
 from __future__ import annotations
@@ -22,14 +24,9 @@ from . import device
 
 
 class Stepper:
-    """Owns two field triples (ping-pong) on one device.
+    """Owns two field triples (ping-pong) on one device."""
 
-    `exchange(fields, stream)` refreshes the halos of a field triple; by
-    default the single-domain periodic wrap (K2). The multi-GPU decomposition
-    passes `decomp.HaloExchanger.exchange`.
-    """
-
-    def __init__(self, fields, coeffs, dt: float, *, opts=None, exchange=None):
+    def __init__(self, fields, coeffs, dt: float, *, opts=None, exchanger=None):
         u = fields[0]
         self.dims = device.dims_of(u)
         self.coeffs = device._as_device_coeffs(coeffs, u.device)
@@ -37,37 +34,44 @@ class Stepper:
         self.opts = opts
         self.a = tuple(fields)
         self.b = device.alloc_fields(self.dims, u.device)
-        self._exchange = exchange
+        self.exchanger = exchanger
         self.graph = None
         self.graph_steps = 0
         self.steps_done = 0
+        self._halos_fresh = False
 
-    def _halo(self, fields, stream=None):
-        if self._exchange is not None:
-            self._exchange(fields, stream)
+    def _refresh(self, fields, stream=None):
+        if self.exchanger is not None:
+            self.exchanger.exchange(fields, stream)
         else:
             device.wrap_halos(*fields, stream=stream)
 
     def _one(self, stream=None):
-        device.step(*self.a, self.coeffs, self.dt, self.b, opts=self.opts, stream=stream)
-        self._halo(self.b, stream)
+        if self.exchanger is not None:
+            self.exchanger.step_overlapped(self.a, self.coeffs, self.dt, self.b, self.opts, stream)
+        else:
+            device.wrap_halos(*self.a, stream=stream)
+            device.step(*self.a, self.coeffs, self.dt, self.b, opts=self.opts, stream=stream)
         self.a, self.b = self.b, self.a
+        self._halos_fresh = False
 
     def step(self, n: int = 1) -> None:
         """Advance n steps (replaying the captured graph when it divides n)."""
         if self.graph is not None and n % self.graph_steps == 0:
             for _ in range(n // self.graph_steps):
                 self.graph.replay()
-            self.steps_done += n
-            return
-        for _ in range(n):
-            self._one()
+        else:
+            for _ in range(n):
+                self._one()
         self.steps_done += n
+        self._halos_fresh = False
 
     def capture(self, steps: int = 2) -> None:
         """Capture `steps` (even, so the ping-pong returns to the same buffers)."""
         if steps < 2 or steps % 2:
             raise ValueError("capture an even number of steps")
+        if self.exchanger is not None:
+            raise ValueError("graph capture is for the single-GPU stepper")
         self._one()  # warm-up outside capture (sets kernel attributes)
         self._one()
         torch.cuda.synchronize()
@@ -85,4 +89,8 @@ class Stepper:
 
     @property
     def fields(self):
+        """Current fields with their halos refreshed (as wrap_halos leaves them)."""
+        if not self._halos_fresh:
+            self._refresh(self.a)
+            self._halos_fresh = True
         return self.a

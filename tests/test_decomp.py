@@ -1,0 +1,136 @@
+"""Host-side tests of the x-y decomposition and halo exchange.
+
+CPU only: the exchange runs on CPU tensors (TorchFaceOps) through the same
+pre/post + transport code as on GPUs — an in-process loopback hub for many
+decompositions, and real multi-process torch.distributed (gloo, world sizes
+2 and 4, rendezvous on 127.0.0.1). After the exchange every block must equal
+its view of the globally wrapped field (reference wrap_halos semantics,
+grid.py:203-208), and the oracle evaluated block by block must reassemble
+the single-domain result bit for bit (the reference's engine-count
+independence, test_schedules.py:72-77, extended to x-y blocks).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2010_01545_b200 as pw
+from paper_2010_01545_b200.decomp import (Decomposition, DistTransport, HaloExchanger,
+                                          TorchFaceOps, exchange_all_loopback, split_extent)
+from oracle import oracle
+
+
+def test_split_extent_and_blocks_cover():
+    assert split_extent(10, 3) == [(0, 4), (4, 3), (7, 3)]
+    with pytest.raises(ValueError):
+        split_extent(3, 4)
+    g = pw.make_grid(13, 11, 4)
+    for px, py in ((1, 1), (1, 2), (2, 2), (2, 4), (3, 3), (13, 1)):
+        seen = np.zeros((13, 11), dtype=int)
+        for r in range(px * py):
+            xo, nx, yo, ny = Decomposition(g, px, py, r).block()
+            seen[xo:xo + nx, yo:yo + ny] += 1
+        assert np.all(seen == 1)
+
+
+def test_neighbours_are_periodic():
+    d = Decomposition(pw.make_grid(8, 8, 2), 2, 4, 0)
+    assert d.coords == (0, 0)
+    assert d.neighbours == {"xm": 4, "xp": 4, "ym": 3, "yp": 1}
+    d5 = d.for_rank(5)
+    assert d5.coords == (1, 1) and d5.neighbours == {"xm": 1, "xp": 1, "ym": 4, "yp": 6}
+    with pytest.raises(ValueError):
+        Decomposition(pw.make_grid(8, 8, 2), 2, 4, 8)
+
+
+def _global_case(nx, ny, nz, seed=5):
+    u, v, w = oracle.fill_random(nx, ny, nz, seed, baseline=True)
+    co = oracle.baseline_coefficients(seed, nz)
+    return (u, v, w), co
+
+
+def _stale_blocks(dec, glob):
+    """Each rank's block with its halos poisoned (the exchange must fill them)."""
+    blocks = []
+    for r in range(dec.size):
+        d = dec.for_rank(r)
+        fs = [torch.from_numpy(np.ascontiguousarray(d.local_view(g))).clone() for g in glob]
+        for f in fs:
+            f[0] = f[-1] = f[:, 0] = f[:, -1] = np.nan
+        blocks.append(fs)
+    return blocks
+
+
+@pytest.mark.parametrize("px,py", [(1, 1), (1, 2), (2, 1), (2, 2), (2, 4), (3, 3), (4, 2)])
+def test_loopback_exchange_and_blockwise_oracle(px, py):
+    nx, ny, nz = 17, 13, 6
+    glob, co = _global_case(nx, ny, nz)
+    dec = Decomposition(pw.make_grid(nx, ny, nz), px, py, 0)
+    blocks = _stale_blocks(dec, glob)
+    ex = [HaloExchanger(dec.for_rank(r), device="cpu", faceops=TorchFaceOps) for r in range(dec.size)]
+    exchange_all_loopback(ex, blocks)
+    want = oracle.advect(*glob, co["tcx"], co["tcy"], co["tzc1"], co["tzc2"])
+    for r, fs in enumerate(blocks):
+        d = dec.for_rank(r)
+        for f, g in zip(fs, glob):
+            assert np.array_equal(f.numpy(), d.local_view(g)), (r, "halo")
+        got = oracle.advect(*(f.numpy() for f in fs), co["tcx"], co["tcy"], co["tzc1"], co["tzc2"])
+        xo, bx, yo, by = d.block()
+        for gb, wn in zip(got, want):
+            assert gb[1:-1, 1:-1].tobytes() == wn[1 + xo:1 + xo + bx, 1 + yo:1 + yo + by].tobytes()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, px, py, q):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        nx, ny, nz = 12, 10, 5
+        glob, co = _global_case(nx, ny, nz, seed=9)
+        dec = Decomposition(pw.make_grid(nx, ny, nz), px, py, rank)
+        fs = _stale_blocks(dec, glob)[rank]
+        ex = HaloExchanger(dec, device="cpu", transport=DistTransport(), faceops=TorchFaceOps)
+        ex.exchange(fs)
+        ok = all(np.array_equal(f.numpy(), dec.local_view(g)) for f, g in zip(fs, glob))
+        got = oracle.advect(*(f.numpy() for f in fs), co["tcx"], co["tcy"], co["tzc1"], co["tzc2"])
+        want = oracle.advect(*glob, co["tcx"], co["tcy"], co["tzc1"], co["tzc2"])
+        xo, bx, yo, by = dec.block()
+        ok &= all(gb[1:-1, 1:-1].tobytes() == wn[1 + xo:1 + xo + bx, 1 + yo:1 + yo + by].tobytes()
+                  for gb, wn in zip(got, want))
+        # a second exchange on updated data (buffers are reused)
+        for f in fs:
+            f.mul_(2.0)
+        ex.exchange(fs)
+        ok &= all(np.array_equal(f.numpy(), 2.0 * dec.local_view(g)) for f, g in zip(fs, glob))
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, bool(ok), ""))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, False, repr(e)))
+
+
+@pytest.mark.parametrize("px,py", [(1, 2), (2, 1), (2, 2)])
+def test_gloo_multiprocess_exchange(px, py):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    world = px * py
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, px, py, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r for r, _, _ in results) == list(range(world))
+    for r, ok, err in results:
+        assert ok, (r, err)
