@@ -300,9 +300,10 @@ def run_ours(args):
     peak, peak_src = measured_peak()
     achieved = BYTES_PER_POINT * pts_rank / (kern_ms / 1e3) / 1e9
     key = f"{args.config}:{args.variant}:{nx}x{ny}x{nz}"
-    traffic = ncu_traffic(key)
+    tr = ncu_traffic(key) or {}
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "frac": round(achieved / peak, 4), "traffic": tr.get("bytes"),
+                "traffic_source": tr.get("source"),
                 "peak_source": peak_src, "kernel_ms": round(kern_ms, 5),
                 "algorithmic_bytes_per_launch": BYTES_PER_POINT * pts_rank,
                 "bytes_per_point": BYTES_PER_POINT,
