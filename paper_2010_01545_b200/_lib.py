@@ -12,7 +12,10 @@ import threading
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libpwadv.so"
+import os as _os
+
+# PWADV_LIB overrides the library (A/B builds of the same ABI for profiling)
+LIB_PATH = Path(_os.environ["PWADV_LIB"]) if _os.environ.get("PWADV_LIB") else _PKG / "libpwadv.so"
 
 _lock = threading.Lock()
 _lib = None

@@ -141,9 +141,15 @@ __global__ void __launch_bounds__(256) k_advect_simple(BoxArgs a)
 
 // value at k0-1 of the thread's pair: the previous lane's k1, or (across a
 // warp boundary inside a column, FIX only) straight from the shared plane.
+// When columns straddle warps (FIX, e.g. nz = 128) the neighbour is read from
+// the staged plane instead (measured faster there than shuffles + fix-ups).
+#ifndef PWADV_NBR_SMEM
+#define PWADV_NBR_SMEM 0
+#endif
 template <bool FIX>
 __device__ __forceinline__ double nbr_m(double2 p, const double *colp, int k0, bool fix)
 {
+    if constexpr (PWADV_NBR_SMEM || FIX) return colp[k0 > 0 ? k0 - 1 : 0];
     double m = __shfl_up_sync(0xffffffffu, p.y, 1);
     if constexpr (FIX) {
         if (fix) m = colp[k0 - 1];
@@ -153,8 +159,9 @@ __device__ __forceinline__ double nbr_m(double2 p, const double *colp, int k0, b
 
 // value at k0+2: the next lane's k0, or from the shared plane.
 template <bool FIX>
-__device__ __forceinline__ double nbr_q(double2 p, const double *colp, int k0, bool fix)
+__device__ __forceinline__ double nbr_q(double2 p, const double *colp, int k0, bool fix, int nz)
 {
+    if constexpr (PWADV_NBR_SMEM || FIX) return colp[k0 + 2 < nz ? k0 + 2 : nz - 1];
     double q = __shfl_down_sync(0xffffffffu, p.x, 1);
     if constexpr (FIX) {
         if (fix) q = colp[k0 + 2];
@@ -365,10 +372,10 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT)) k_advect_xmarch(BoxAr
             const double2 umc = P(C, 0, -1), v1c = P(C, 1, 1), w1c = P(C, 2, 1), wmc = P(C, 2, -1);
             const double w1cM = nbr_m<FIX>(w1c, colp(C, 2, 1), k0, fixM);
             U0M[r] = nbr_m<FIX>(U0[r], colp(C, 0, 0), k0, fixM);
-            const double u0cQ = nbr_q<FIX>(U0[r], colp(C, 0, 0), k0, fixQ);
+            const double u0cQ = nbr_q<FIX>(U0[r], colp(C, 0, 0), k0, fixQ, nz);
             const double v0cM = nbr_m<FIX>(V0[r], colp(C, 1, 0), k0, fixM);
-            const double v0cQ = nbr_q<FIX>(V0[r], colp(C, 1, 0), k0, fixQ);
-            const double w0cQ = nbr_q<FIX>(W0[r], colp(C, 2, 0), k0, fixQ);
+            const double v0cQ = nbr_q<FIX>(V0[r], colp(C, 1, 0), k0, fixQ, nz);
+            const double w0cQ = nbr_q<FIX>(W0[r], colp(C, 2, 0), k0, fixQ, nz);
             const double vmcM = nbr_m<FIX>(VM[r], colp(C, 1, -1), k0, fixM);
             release(cseq - 1, pst);  // plane i fully consumed by this warp
 
