@@ -65,7 +65,7 @@ def main():
         name = kw.pop("variant")
         dbg = kw.pop("debug", 0)
         opts = device.make_opts(name, **kw)
-        opts.flags |= dbg << 8
+        opts.flags |= (dbg << 8)
         try:
             plan = device.describe_plan(dims, None, opts)
             ms = time_it(lambda: device.advect(*fields, co, out, opts=opts), args.reps)
