@@ -235,11 +235,15 @@ def run_ours(args):
         from paper_2010_01545_b200 import decomp
         exch = decomp.HaloExchanger(dec, dev)
         if stepping:
-            from paper_2010_01545_b200.stepper import Stepper
-            st = Stepper(fields, co, 0.1, opts=opts, exchanger=exch)
+            # K4 with the exchange fused in: boundary values stored into the
+            # neighbours' halos over NVLink (CUDA IPC), one NCCL barrier per step
+            st = decomp.PushStepper(dec, fields, co, 0.1, decomp.IpcPeerRegistry(dec),
+                                    decomp.NcclBarrier(dev), opts=opts,
+                                    initial_exchange=lambda f: exch.exchange(f, stream=stream))
+            st.step(1, stream=stream)
 
             def one_step():
-                st._one(stream)
+                st.step(1, stream=stream)
         else:
             def one_step():
                 exch.advect_overlapped(fields, co, out, opts=opts, stream=stream)

@@ -133,6 +133,39 @@ int pwadv_step_box_f64(const double *u, const double *v, const double *w,
                        int64_t x_begin, int64_t x_end, int64_t y_begin, int64_t y_end,
                        const pwadv_opts *opts, void *stream);
 
+/*
+ * K4 with the halo exchange fused in (multi-GPU time stepping, SURVEY.md §8e
+ * and §8f1): computes the whole local interior like pwadv_step_box_f64 AND
+ * stores every boundary value of u_new/v_new/w_new into the halo cells of the
+ * neighbouring blocks' NEW buffers that mirror it (x/y faces and corners), so
+ * after one barrier across ranks every block's halos equal the periodic wrap of
+ * the global fields — no separate exchange. Peer buffers are device memory
+ * this GPU can store to: the same device, or another GPU's allocation opened
+ * with pwadv_ipc_open (CUDA IPC, NVLink P2P). A neighbour that is this block
+ * itself (an undivided axis) is given as its own buffers.
+ */
+enum {
+    PWADV_NB_XM = 0, PWADV_NB_XP = 1, PWADV_NB_YM = 2, PWADV_NB_YP = 3,
+    PWADV_NB_XMYM = 4, PWADV_NB_XMYP = 5, PWADV_NB_XPYM = 6, PWADV_NB_XPYP = 7
+};
+typedef struct pwadv_peers {
+    double *u[8], *v[8], *w[8];  /* neighbour d's new u, v, w (padded layout) */
+    int64_t nx[8], ny[8];        /* neighbour d's local interior extents */
+} pwadv_peers;
+int pwadv_step_push_f64(const double *u, const double *v, const double *w,
+                        double *u_new, double *v_new, double *w_new,
+                        int64_t nx, int64_t ny, int64_t nz,
+                        double tcx, double tcy,
+                        const double *tzc1, const double *tzc2, double dt,
+                        const pwadv_peers *peers, const pwadv_opts *opts, void *stream);
+
+/* CUDA IPC helpers for the peer buffers of pwadv_step_push_f64 (one process
+ * per GPU): export a device allocation (handle: 64 opaque bytes, plus the
+ * pointer's byte offset inside its allocation), open a peer's export, close. */
+int pwadv_ipc_export(const void *dev_ptr, unsigned char handle[64], uint64_t *offset);
+int pwadv_ipc_open(const unsigned char handle[64], uint64_t offset, void **dev_ptr);
+int pwadv_ipc_close(void *dev_ptr, uint64_t offset);
+
 /* K2 — periodic halo wrap in place (grid.py:203-208: X then Y semantics). */
 int pwadv_wrap_halos_f64(double *f, int64_t nx, int64_t ny, int64_t nz, void *stream);
 /* K2 on three fields in one launch. */

@@ -56,6 +56,16 @@ class PlanInfo(ctypes.Structure):
                 ("chunks", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
+class Peers(ctypes.Structure):
+    """pwadv_peers (include/pwadv.h): neighbour d's new u, v, w and extents."""
+
+    _fields_ = [("u", ctypes.c_void_p * 8), ("v", ctypes.c_void_p * 8), ("w", ctypes.c_void_p * 8),
+                ("nx", ctypes.c_int64 * 8), ("ny", ctypes.c_int64 * 8)]
+
+
+NB_XM, NB_XP, NB_YM, NB_YP, NB_XMYM, NB_XMYP, NB_XPYM, NB_XPYP = range(8)
+
+
 # name -> (restype, argtypes); every symbol include/pwadv.h declares
 SIGNATURES = {
     "pwadv_abi_version": (ctypes.c_int, []),
@@ -68,6 +78,10 @@ SIGNATURES = {
     "pwadv_step_box_f64": (ctypes.c_int, [_P] * 6 + [_I64] * 3 + [_D, _D, _P, _P, _D]
                            + [_I64] * 4 + [_P, _P]),
     "pwadv_describe_plan": (ctypes.c_int, [_I64] * 7 + [_P, ctypes.c_int, _P]),
+    "pwadv_step_push_f64": (ctypes.c_int, [_P] * 6 + [_I64] * 3 + [_D, _D, _P, _P, _D, _P, _P, _P]),
+    "pwadv_ipc_export": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_uint64)]),
+    "pwadv_ipc_open": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.POINTER(_P)]),
+    "pwadv_ipc_close": (ctypes.c_int, [_P, ctypes.c_uint64]),
     "pwadv_wrap_halos_f64": (ctypes.c_int, [_P, _I64, _I64, _I64, _P]),
     "pwadv_wrap_halos3_f64": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, _P]),
     "pwadv_wrap_axis3_f64": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, ctypes.c_int32, _P]),

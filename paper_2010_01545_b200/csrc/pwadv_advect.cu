@@ -46,7 +46,50 @@ struct BoxArgs {
     double tcx, tcy, dt;
     int64_t x0, x1, y0, y1;  // interior box, 1-based, half-open
     unsigned long long *trace;  // profiling only: per-plane issue/arrival timestamps (CTA 0)
+    int push;                   // fused step only: also store boundary values into peers' halos
+    pwadv_peers peers;          // (include/pwadv.h) the neighbours' new buffers and extents
 };
+
+// Fused halo push (K4 + exchange in one kernel): an interior boundary value of
+// this block is also stored into every neighbour halo cell that mirrors it —
+// x/y faces and the four corners — in the neighbour's NEW buffers (peer
+// memory: the same GPU, or another GPU's memory mapped over NVLink by CUDA
+// IPC). After all ranks' kernels finish (one barrier per step) every block's
+// halos equal the periodic wrap of the global field, exactly as the two-phase
+// exchange and wrap_halos (grid.py:203-208) leave them.
+template <int N>
+__device__ __forceinline__ void push_to(const pwadv_peers &p, int d, int64_t pi, int64_t pj, int64_t nz,
+                                        int64_t k, const double *a, const double *b, const double *c)
+{
+    const int64_t off = (pi * (p.ny[d] + 2) + pj) * nz + k;
+    if constexpr (N == 2) {
+        store2(p.u[d] + off, a[0], a[1]);
+        store2(p.v[d] + off, b[0], b[1]);
+        store2(p.w[d] + off, c[0], c[1]);
+    } else {
+        p.u[d][off] = a[0];
+        p.v[d][off] = b[0];
+        p.w[d][off] = c[0];
+    }
+}
+
+template <int N>
+__device__ __forceinline__ void push_boundary(const BoxArgs &A, int64_t i, int64_t j, int64_t k,
+                                              const double *a, const double *b, const double *c)
+{
+    const bool xm = i == 1, xp = i == A.nx, ym = j == 1, yp = j == A.ny;
+    if (!(xm || xp || ym || yp)) return;
+    const pwadv_peers &p = A.peers;
+    const int64_t nz = A.nz;
+    if (xm) push_to<N>(p, PWADV_NB_XM, p.nx[PWADV_NB_XM] + 1, j, nz, k, a, b, c);
+    if (xp) push_to<N>(p, PWADV_NB_XP, 0, j, nz, k, a, b, c);
+    if (ym) push_to<N>(p, PWADV_NB_YM, i, p.ny[PWADV_NB_YM] + 1, nz, k, a, b, c);
+    if (yp) push_to<N>(p, PWADV_NB_YP, i, 0, nz, k, a, b, c);
+    if (xm && ym) push_to<N>(p, PWADV_NB_XMYM, p.nx[PWADV_NB_XMYM] + 1, p.ny[PWADV_NB_XMYM] + 1, nz, k, a, b, c);
+    if (xm && yp) push_to<N>(p, PWADV_NB_XMYP, p.nx[PWADV_NB_XMYP] + 1, 0, nz, k, a, b, c);
+    if (xp && ym) push_to<N>(p, PWADV_NB_XPYM, 0, p.ny[PWADV_NB_XPYM] + 1, nz, k, a, b, c);
+    if (xp && yp) push_to<N>(p, PWADV_NB_XPYP, 0, 0, nz, k, a, b, c);
+}
 
 struct TileCfg {
     int tj;           // columns per strip
@@ -133,6 +176,9 @@ __global__ void __launch_bounds__(256) k_advect_simple(BoxArgs a)
         a.o0[o] = r0;
         a.o1[o] = r1;
         a.o2[o] = r2;
+        if constexpr (STEP) {
+            if (a.push) push_boundary<1>(a, i, j, k, &r0, &r1, &r2);
+        }
     }
 }
 
@@ -357,6 +403,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT)) k_advect_xmarch(BoxAr
         double *o2 = a.o2 + (ib * ny2 + (j0 + c)) * (int64_t)nz + k0;
         const int64_t ostep = ny2 * nz;
 
+        int64_t ci = ib;  // the output plane of the current step
         auto body = [&](auto R) {
             constexpr int r = decltype(R)::value;
             constexpr int rm = (r + 2) % 3, rp = (r + 1) % 3;
@@ -431,6 +478,13 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT)) k_advect_xmarch(BoxAr
                 store2(o1, sv_a, sv_b);
                 store2(o2, sw_a, sw_b);
             }
+            if constexpr (STEP) {
+                if (a.push && active) {
+                    const double pa[2] = {su_a, su_b}, pb[2] = {sv_a, sv_b}, pc[2] = {sw_a, sw_b};
+                    push_boundary<2>(a, ci, j0 + c, k0, pa, pb, pc);
+                }
+            }
+            ++ci;
             o0 += ostep;
             o1 += ostep;
             o2 += ostep;
@@ -489,6 +543,9 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
     a.y0 = L.y0;
     a.y1 = L.y1;
     a.trace = reinterpret_cast<unsigned long long *>(L.trace);
+    a.push = L.peers != nullptr ? 1 : 0;
+    if (L.peers) a.peers = *L.peers;
+    else a.peers = pwadv_peers{};
     const bool fma = (L.flags & PWADV_FLAG_FMA) != 0;
     const int64_t nbx = L.x1 - L.x0, nby = L.y1 - L.y0;
     if (nbx <= 0 || nby <= 0) return PWADV_OK;

@@ -76,7 +76,8 @@ static int check_ptrs(std::initializer_list<const void *> ps)
 static int run_box(const double *u, const double *v, const double *w, double *o0, double *o1,
                    double *o2, int64_t nx, int64_t ny, int64_t nz, double tcx, double tcy,
                    const double *tzc1, const double *tzc2, double dt, bool step, int64_t x0,
-                   int64_t x1, int64_t y0, int64_t y1, const pwadv_opts *opts, void *stream)
+                   int64_t x1, int64_t y0, int64_t y1, const pwadv_opts *opts, void *stream,
+                   const pwadv_peers *peers = nullptr)
 {
     int rc = check_dims(nx, ny, nz);
     if (rc) return rc;
@@ -113,6 +114,7 @@ static int run_box(const double *u, const double *v, const double *w, double *o0
     L.max_threads = opts ? opts->max_threads : 0;
     L.chunks = opts ? opts->chunks : 0;
     L.trace = opts ? opts->trace : nullptr;
+    L.peers = peers;
     if (L.tile_j < 0 || L.stages < 0 || L.grid < 0 || L.max_threads < 0 || L.chunks < 0)
         return set_error(PWADV_E_ARG, "negative tuning value");
     return launch_box(L, (cudaStream_t)stream);
@@ -172,6 +174,87 @@ int pwadv_step_box_f64(const double *u, const double *v, const double *w, double
         return set_error(PWADV_E_ARG, "fused step needs distinct (ping-pong) output buffers");
     return run_box(u, v, w, u_new, v_new, w_new, nx, ny, nz, tcx, tcy, tzc1, tzc2, dt, true,
                    x_begin, x_end, y_begin, y_end, opts, stream);
+}
+
+int pwadv_step_push_f64(const double *u, const double *v, const double *w, double *u_new,
+                        double *v_new, double *w_new, int64_t nx, int64_t ny, int64_t nz,
+                        double tcx, double tcy, const double *tzc1, const double *tzc2, double dt,
+                        const pwadv_peers *peers, const pwadv_opts *opts, void *stream)
+{
+    if (!peers) return set_error(PWADV_E_NULL, "null peers");
+    for (int d = 0; d < 8; ++d) {
+        if (!peers->u[d] || !peers->v[d] || !peers->w[d])
+            return set_error(PWADV_E_NULL, "peer %d buffers missing", d);
+        if (((uintptr_t)peers->u[d] | (uintptr_t)peers->v[d] | (uintptr_t)peers->w[d]) & 7)
+            return set_error(PWADV_E_ALIGN, "peer %d buffers misaligned", d);
+        if (peers->nx[d] < 1 || peers->ny[d] < 1)
+            return set_error(PWADV_E_DIMS, "peer %d extents invalid", d);
+    }
+    // x neighbours share my y extent, y neighbours my x extent
+    if (peers->ny[PWADV_NB_XM] != ny || peers->ny[PWADV_NB_XP] != ny ||
+        peers->nx[PWADV_NB_YM] != nx || peers->nx[PWADV_NB_YP] != nx)
+        return set_error(PWADV_E_RANGE, "peer extents inconsistent with an x-y decomposition");
+    if (u == u_new || v == v_new || w == w_new)
+        return set_error(PWADV_E_ARG, "fused step needs distinct (ping-pong) output buffers");
+    return run_box(u, v, w, u_new, v_new, w_new, nx, ny, nz, tcx, tcy, tzc1, tzc2, dt, true, 1,
+                   nx + 1, 1, ny + 1, opts, stream, peers);
+}
+
+// Base address of the allocation containing `ptr`, through the driver's
+// cuMemGetAddressRange (fetched with cudaGetDriverEntryPoint: no libcuda link).
+static int allocation_base(const void *ptr, uintptr_t *base)
+{
+    typedef int (*range_fn)(unsigned long long *, size_t *, unsigned long long);
+    static range_fn fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q);
+        if (e != cudaSuccess || !f) return set_cuda_error("cudaGetDriverEntryPoint", e);
+        fn = (range_fn)f;
+    }
+    unsigned long long b = 0;
+    size_t sz = 0;
+    if (fn(&b, &sz, (unsigned long long)(uintptr_t)ptr) != 0)
+        return set_error(PWADV_E_ARG, "pointer %p is not device memory", ptr);
+    *base = (uintptr_t)b;
+    return PWADV_OK;
+}
+
+int pwadv_ipc_export(const void *dev_ptr, unsigned char handle[64], uint64_t *offset)
+{
+    if (!dev_ptr || !handle || !offset) return set_error(PWADV_E_NULL, "null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) <= 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(dev_ptr));
+    if (e != cudaSuccess) return set_cuda_error("cudaIpcGetMemHandle", e);
+    uintptr_t base = 0;
+    int rc = allocation_base(dev_ptr, &base);
+    if (rc) return rc;
+    memset(handle, 0, 64);
+    memcpy(handle, &h, sizeof(h));
+    *offset = (uint64_t)((uintptr_t)dev_ptr - base);  // the handle names the whole allocation
+    return PWADV_OK;
+}
+
+int pwadv_ipc_open(const unsigned char handle[64], uint64_t offset, void **dev_ptr)
+{
+    if (!handle || !dev_ptr) return set_error(PWADV_E_NULL, "null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void *base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return set_cuda_error("cudaIpcOpenMemHandle", e);
+    *dev_ptr = (void *)((char *)base + offset);
+    return PWADV_OK;
+}
+
+int pwadv_ipc_close(void *dev_ptr, uint64_t offset)
+{
+    if (!dev_ptr) return set_error(PWADV_E_NULL, "null argument");
+    cudaError_t e = cudaIpcCloseMemHandle((void *)((char *)dev_ptr - offset));
+    if (e != cudaSuccess) return set_cuda_error("cudaIpcCloseMemHandle", e);
+    return PWADV_OK;
 }
 
 int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz, int64_t x0, int64_t x1, int64_t y0,

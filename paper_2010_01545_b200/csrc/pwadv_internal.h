@@ -27,6 +27,7 @@ struct BoxLaunch {
     uint32_t flags;
     int tile_j, stages, grid, max_threads, chunks;
     void *trace;
+    const pwadv_peers *peers;  // fused step: push boundary values into these halos
 };
 
 struct XmarchPlan {

@@ -400,3 +400,184 @@ def exchange_all_loopback(exchangers: list, fields_by_rank: list, stream=None) -
         hub.run_all(ops)
         for ex, f in zip(exchangers, fields_by_rank):
             ex.post(f, axis, stream)
+
+
+# ---------------------------------------------------------------------------
+# Fused stepping: K4 pushes boundary values straight into the neighbours'
+# halos (pwadv_step_push_f64) — the exchange is part of the compute kernel,
+# stores over NVLink to peer memory; one barrier per step.
+
+_DIRS = ((-1, 0), (1, 0), (0, -1), (0, 1), (-1, -1), (-1, 1), (1, -1), (1, 1))  # PWADV_NB_* order
+
+
+def neighbour_ranks(dec: Decomposition) -> list[int]:
+    cx, cy = dec.coords
+    return [dec.rank_of(cx + dx, cy + dy) for dx, dy in _DIRS]
+
+
+class LocalPeerRegistry:
+    """Peer buffers of ranks living in this process (emulation on one GPU):
+    rank -> ((u, v, w) of set 0, (u, v, w) of set 1) as device pointers."""
+
+    def __init__(self):
+        self.sets: dict = {}
+
+    def publish(self, rank: int, sets) -> None:
+        self.sets[rank] = tuple(tuple(t.data_ptr() for t in s) for s in sets)
+
+    def pointers(self, rank: int, set_index: int):
+        return self.sets[rank][set_index]
+
+
+class IpcPeerRegistry:
+    """Peer buffers across processes (one per GPU): each rank exports CUDA IPC
+    handles of its two buffer sets, all ranks exchange them with
+    torch.distributed, and each rank maps its neighbours' buffers (NVLink P2P)."""
+
+    def __init__(self, dec: Decomposition, group=None):
+        self.dec, self.group = dec, group
+        self.sets: dict = {}
+        self._opened: list = []
+
+    def publish(self, rank: int, sets) -> None:
+        import torch.distributed as dist
+        from . import _lib
+        L = _lib.lib()
+        mine = []
+        for s in sets:
+            entry = []
+            for t in s:
+                h = (ctypes.c_ubyte * 64)()
+                off = ctypes.c_uint64()
+                _lib.check(L.pwadv_ipc_export(ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off)))
+                entry.append((bytes(h), int(off.value)))
+            mine.append(entry)
+        everyone = [None] * self.dec.size
+        dist.all_gather_object(everyone, mine, group=self.group)
+        self.sets[rank] = tuple(tuple(t.data_ptr() for t in s) for s in sets)
+        for r in set(neighbour_ranks(self.dec)) - {rank}:
+            ptrs = []
+            for entry in everyone[r]:
+                row = []
+                for hb, off in entry:
+                    p = ctypes.c_void_p()
+                    _lib.check(L.pwadv_ipc_open((ctypes.c_ubyte * 64)(*hb), off, ctypes.byref(p)))
+                    self._opened.append((p.value, off))
+                    row.append(p.value)
+                ptrs.append(tuple(row))
+            self.sets[r] = tuple(ptrs)
+
+    def pointers(self, rank: int, set_index: int):
+        return self.sets[rank][set_index]
+
+    def close(self) -> None:
+        from . import _lib
+        for p, off in self._opened:
+            _lib.lib().pwadv_ipc_close(ctypes.c_void_p(p), off)
+        self._opened = []
+
+
+class NcclBarrier:
+    """Stream-ordered barrier across ranks: a one-element all-reduce on the
+    compute stream completes only after every rank's preceding kernels."""
+
+    def __init__(self, device, group=None):
+        self.flag = torch.zeros(1, device=device)
+        self.group = group
+
+    def __call__(self, stream=None) -> None:
+        import torch.distributed as dist
+        s = stream or torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            dist.all_reduce(self.flag, group=self.group)
+
+
+class ThreadStreamBarrier:
+    """Barrier for ranks emulated as host threads on one GPU: every rank's
+    stream waits on every other rank's event (kernels never wait on kernels)."""
+
+    def __init__(self, nranks: int):
+        import threading
+        self.b = threading.Barrier(nranks)
+        self.lock = threading.Lock()
+        self.events: dict = {}
+
+    def bind(self, rank: int):
+        def barrier(stream=None):
+            s = stream or torch.cuda.current_stream()
+            ev = torch.cuda.Event()
+            ev.record(s)
+            with self.lock:
+                self.events[rank] = ev
+            self.b.wait()
+            for e in list(self.events.values()):
+                s.wait_event(e)
+            self.b.wait()
+        return barrier
+
+
+class PushStepper:
+    """Forward-Euler steps of one block with the halo exchange fused into K4.
+
+    Two buffer sets (ping-pong); step n reads set n%2 (halos valid) and writes
+    set (n+1)%2 — its interior and, through peer stores, the halos of every
+    block that mirrors its boundary — then all ranks meet at `barrier`.
+    `initial_exchange(fields)` fills the halos of the starting fields once.
+    """
+
+    def __init__(self, dec: Decomposition, fields, coeffs, dt: float, registry, barrier, *,
+                 opts=None, initial_exchange=None):
+        from . import device as dv
+        self.dec = dec
+        self.dims = dec.local_dims
+        u = fields[0]
+        self.coeffs = dv._as_device_coeffs(coeffs, u.device)
+        self.dt = float(dt)
+        self.opts = opts
+        self.sets = (tuple(fields), dv.alloc_fields(self.dims, u.device))
+        self.cur = 0
+        self.registry = registry
+        self.barrier = barrier
+        registry.publish(dec.rank, self.sets)
+        self._initial = initial_exchange
+        self._peers = None
+        self.steps_done = 0
+
+    def _build_peers(self):
+        from . import _lib
+        P = []
+        nbr = neighbour_ranks(self.dec)
+        for set_index in (0, 1):
+            p = _lib.Peers()
+            for d, r in enumerate(nbr):
+                u, v, w = self.registry.pointers(r, set_index)
+                p.u[d], p.v[d], p.w[d] = u, v, w
+                _, nxl, _, nyl = self.dec.block(r)
+                p.nx[d], p.ny[d] = nxl, nyl
+            P.append(p)
+        return P
+
+    def step(self, n: int = 1, stream=None) -> None:
+        from . import _lib, device as dv
+        if self._peers is None:  # all ranks have published by the first step
+            if self._initial is not None:
+                self._initial(self.sets[0])
+            self.barrier(stream)
+            self._peers = self._build_peers()
+        L = _lib.lib()
+        dc = self.coeffs
+        d = self.dims
+        for _ in range(n):
+            src, dst = self.sets[self.cur], self.sets[1 - self.cur]
+            h = dv._stream_handle(stream, src[0].device)
+            _lib.check(L.pwadv_step_push_f64(
+                dv._p(src[0]), dv._p(src[1]), dv._p(src[2]), dv._p(dst[0]), dv._p(dst[1]),
+                dv._p(dst[2]), d.nx, d.ny, d.nz, dc.tcx, dc.tcy, dv._p(dc.tz[0]), dv._p(dc.tz[1]),
+                self.dt, ctypes.byref(self._peers[1 - self.cur]), _lib.opts_ptr(self.opts), h))
+            self.barrier(stream)
+            self.cur = 1 - self.cur
+            self.steps_done += 1
+
+    @property
+    def fields(self):
+        return self.sets[self.cur]

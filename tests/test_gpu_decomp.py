@@ -98,3 +98,35 @@ def test_emulated_decomposed_time_stepping(px, py):
     for dec, final in run_ranks(px * py, rank):
         for f, w in zip(final, want):
             assert torch.equal(f.view(torch.int64), dec.local_view(w).contiguous().view(torch.int64)), dec.rank
+
+
+@pytest.mark.parametrize("px,py,shape", [(2, 4, (48, 40, 16)), (1, 2, (30, 26, 64)), (2, 2, (25, 23, 6)),
+                                         (1, 1, (20, 18, 64)), (3, 2, (36, 30, 128))])
+def test_emulated_fused_push_stepping(px, py, shape):
+    """K4 with the exchange fused in (peer stores + one barrier per step) ==
+    single-domain stepping, bitwise, halos included."""
+    from paper_2010_01545_b200.decomp import LocalPeerRegistry, PushStepper, ThreadStreamBarrier
+    gd = pw.make_grid(*shape)
+    spec = pw.GeneratorSpec.baseline(11)
+    co = pw.baseline_coefficients(11, gd.nz)
+    single = Stepper(device.fill(gd, spec), co, 0.1)
+    single.step(4)
+    want = single.fields
+    torch.cuda.synchronize()
+    n = px * py
+    hub = ThreadHubTransport(n)
+    reg = LocalPeerRegistry()
+    bar = ThreadStreamBarrier(n)
+
+    def rank(r):
+        dec = Decomposition(gd, px, py, r)
+        fs = dec.fill_local(spec)
+        ex = HaloExchanger(dec, device="cuda", transport=hub.bind(r))
+        st = PushStepper(dec, fs, co, 0.1, reg, bar.bind(r), initial_exchange=ex.exchange)
+        st.step(4)
+        torch.cuda.current_stream().synchronize()
+        return dec, st.fields
+
+    for dec, final in run_ranks(n, rank):
+        for f, w in zip(final, want):
+            assert torch.equal(f.view(torch.int64), dec.local_view(w).contiguous().view(torch.int64)), dec.rank
