@@ -1,4 +1,6 @@
-"""python -m paper_2010_01545_b200  -> build libpwadv.so in-tree."""
-from .build import build
+"""python -m paper_2010_01545_b200 {bench,build} ..."""
+import sys
 
-print(build(force=True))
+from .cli import main
+
+sys.exit(main())

@@ -4,7 +4,12 @@
 // raise the same exceptions (GridError/ValueError before any compute,
 // grid.py:52-58, kernel.py:178-179, schedules.py:65-68); here they come back
 // as negative codes with a message in pwadv_last_error().
+#include <algorithm>
+#include <condition_variable>
 #include <cstdarg>
+#include <deque>
+#include <functional>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -396,6 +401,74 @@ int pwadv_unpack_xface3_f64(double *u, double *v, double *w, const double *buf, 
 // ---------------------------------------------------------------------------
 // host-buffer context: pipelined H2D / K1 / D2H over X-slab chunks
 
+namespace pwadv {
+
+// Small persistent host thread pool: one memcpy split across the workers
+// (pageable <-> pinned staging for host buffers that are not page-locked).
+class CopyPool {
+  public:
+    explicit CopyPool(int n) : stop_(false), pending_(0)
+    {
+        for (int i = 0; i < n; ++i) workers_.emplace_back([this] { run(); });
+    }
+    ~CopyPool()
+    {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto &t : workers_) t.join();
+    }
+    void memcpy_parallel(void *dst, const void *src, size_t bytes)
+    {
+        const size_t parts = std::min(workers_.size() + 1, std::max<size_t>(1, bytes >> 21));
+        const size_t step = (bytes / parts + 63) & ~size_t(63);
+        std::vector<std::pair<size_t, size_t>> spans;
+        for (size_t off = 0; off < bytes; off += step) spans.push_back({off, std::min(step, bytes - off)});
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (size_t k = 1; k < spans.size(); ++k) {
+                const auto sp = spans[k];
+                tasks_.push_back([=] { memcpy((char *)dst + sp.first, (const char *)src + sp.first, sp.second); });
+                ++pending_;
+            }
+        }
+        cv_.notify_all();
+        memcpy(dst, src, spans.empty() ? 0 : spans[0].second);  // the caller copies the first span
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [this] { return pending_ == 0; });
+    }
+
+  private:
+    void run()
+    {
+        for (;;) {
+            std::function<void()> job;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [this] { return stop_ || !tasks_.empty(); });
+                if (stop_ && tasks_.empty()) return;
+                job = std::move(tasks_.front());
+                tasks_.pop_front();
+            }
+            job();
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (--pending_ == 0) done_.notify_all();
+            }
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::deque<std::function<void()>> tasks_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_;
+    bool stop_;
+    int pending_;
+};
+
+}  // namespace pwadv
+
 struct pwadv_ctx {
     int device;
     int64_t nx, ny, nz;
@@ -405,6 +478,11 @@ struct pwadv_ctx {
     cudaStream_t s_h2d, s_cmp, s_d2h;
     std::vector<cudaEvent_t> ev_in, ev_cmp;
     uint64_t last_h2d, last_d2h;
+    // pageable-host staging (created on first use)
+    pwadv::CopyPool *pool;
+    double *pin_in[2], *pin_out[2];
+    int64_t pin_planes;  // planes per field a staging buffer holds
+    cudaEvent_t ev_h2d[2], ev_d2h[2];
 };
 
 
@@ -447,6 +525,13 @@ int pwadv_ctx_destroy(pwadv_ctx *c)
         if (c->d_out[m]) cudaFree(c->d_out[m]);
     }
     if (c->d_tz) cudaFree(c->d_tz);
+    for (int b = 0; b < 2; ++b) {
+        if (c->pin_in[b]) cudaFreeHost(c->pin_in[b]);
+        if (c->pin_out[b]) cudaFreeHost(c->pin_out[b]);
+        if (c->ev_h2d[b]) cudaEventDestroy(c->ev_h2d[b]);
+        if (c->ev_d2h[b]) cudaEventDestroy(c->ev_d2h[b]);
+    }
+    delete c->pool;
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_cmp) cudaStreamDestroy(c->s_cmp);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
@@ -462,6 +547,103 @@ int pwadv_ctx_last_bytes(const pwadv_ctx *c, uint64_t *h2d, uint64_t *d2h)
     *h2d = c->last_h2d;
     *d2h = c->last_d2h;
     return PWADV_OK;
+}
+
+static bool is_pinned(const void *p)
+{
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeHost;
+}
+
+// Host buffers that are not page-locked: stream them through double-buffered
+// pinned staging. Per chunk the host threads copy the inputs into staging
+// while the previous chunk's H2D, K1 and D2H run, then copy the previous
+// chunk's outputs out of staging.
+static int advect_host_staged(pwadv_ctx *c, const double *const hin[3], double *const hout[3],
+                              double tcx, double tcy, const pwadv_opts *o, uint64_t *h2d,
+                              uint64_t *d2h)
+{
+    const int64_t nx = c->nx, ny = c->ny, nz = c->nz;
+    const size_t plane = (size_t)(ny + 2) * nz;
+    const size_t pb = plane * sizeof(double);
+    cudaError_t e;
+    if (!c->pool) {
+        const int64_t target = (int64_t)(24u << 20) / (int64_t)(3 * pb);  // ~24 MB per buffer
+        c->pin_planes = std::max<int64_t>(3, std::min<int64_t>(target, nx + 2));
+        for (int b = 0; b < 2; ++b) {
+            e = cudaHostAlloc(&c->pin_in[b], 3 * c->pin_planes * pb, cudaHostAllocDefault);
+            if (e == cudaSuccess) e = cudaHostAlloc(&c->pin_out[b], 3 * c->pin_planes * pb, cudaHostAllocDefault);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_h2d[b], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_d2h[b], cudaEventDisableTiming);
+            if (e != cudaSuccess) return set_cuda_error("staging buffers", e);
+        }
+        const unsigned hc = std::thread::hardware_concurrency();
+        c->pool = new pwadv::CopyPool((int)std::min(15u, hc > 1 ? hc - 1 : 1u));
+    }
+    const int64_t P = c->pin_planes;
+    // output chunk of at most P-2 planes so its input range (+1 plane each side) fits
+    const int64_t per = std::max<int64_t>(1, P - 2);
+    const int chunks = (int)((nx + per - 1) / per);
+    while ((int)c->ev_cmp.size() < chunks) {
+        cudaEvent_t a;
+        cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+        c->ev_cmp.push_back(a);
+    }
+    int64_t copied = 0;
+    int64_t prev_o0 = 0, prev_o1 = 0;
+    auto drain = [&](int ch, int64_t o0, int64_t o1) -> int {
+        const int b = ch & 1;
+        cudaError_t err = cudaEventSynchronize(c->ev_d2h[b]);
+        if (err != cudaSuccess) return set_cuda_error("D2H wait", err);
+        for (int m = 0; m < 3; ++m)
+            c->pool->memcpy_parallel(hout[m] + o0 * plane, c->pin_out[b] + m * P * plane, (o1 - o0) * pb);
+        return PWADV_OK;
+    };
+    for (int ch = 0; ch < chunks; ++ch) {
+        const int b = ch & 1;
+        const int64_t x0 = 1 + (int64_t)ch * per;
+        const int64_t x1 = std::min<int64_t>(nx + 1, x0 + per);
+        const int64_t need = (ch == chunks - 1) ? nx + 2 : x1 + 1;
+        if (ch >= 2) {
+            e = cudaEventSynchronize(c->ev_h2d[b]);  // staging b no longer read by its H2D
+            if (e != cudaSuccess) return set_cuda_error("H2D wait", e);
+        }
+        const int64_t n_in = need - copied;
+        for (int m = 0; m < 3; ++m)
+            c->pool->memcpy_parallel(c->pin_in[b] + m * P * plane, hin[m] + copied * plane, n_in * pb);
+        for (int m = 0; m < 3; ++m) {
+            e = cudaMemcpyAsync(c->d_in[m] + copied * plane, c->pin_in[b] + m * P * plane, n_in * pb,
+                                cudaMemcpyHostToDevice, c->s_h2d);
+            if (e != cudaSuccess) return set_cuda_error("H2D", e);
+        }
+        *h2d += 3 * (uint64_t)n_in * pb;
+        copied = need;
+        cudaEventRecord(c->ev_h2d[b], c->s_h2d);
+        cudaStreamWaitEvent(c->s_cmp, c->ev_h2d[b], 0);
+        int rc = pwadv_advect_box_f64(c->d_in[0], c->d_in[1], c->d_in[2], c->d_out[0], c->d_out[1],
+                                      c->d_out[2], nx, ny, nz, tcx, tcy, c->d_tz, c->d_tz + nz, x0, x1,
+                                      1, ny + 1, o, c->s_cmp);
+        if (rc) return rc;
+        cudaEventRecord(c->ev_cmp[ch], c->s_cmp);
+        cudaStreamWaitEvent(c->s_d2h, c->ev_cmp[ch], 0);
+        const int64_t o0 = (ch == 0) ? 0 : x0;
+        const int64_t o1 = (ch == chunks - 1) ? nx + 2 : x1;
+        for (int m = 0; m < 3; ++m) {
+            e = cudaMemcpyAsync(c->pin_out[b] + m * P * plane, c->d_out[m] + o0 * plane, (o1 - o0) * pb,
+                                cudaMemcpyDeviceToHost, c->s_d2h);
+            if (e != cudaSuccess) return set_cuda_error("D2H", e);
+        }
+        *d2h += 3 * (uint64_t)(o1 - o0) * pb;
+        cudaEventRecord(c->ev_d2h[b], c->s_d2h);
+        if (ch >= 1 && (rc = drain(ch - 1, prev_o0, prev_o1))) return rc;
+        prev_o0 = o0;
+        prev_o1 = o1;
+    }
+    return drain(chunks - 1, prev_o0, prev_o1);
 }
 
 int pwadv_ctx_advect_host(pwadv_ctx *c, const double *u, const double *v, const double *w,
@@ -496,6 +678,16 @@ int pwadv_ctx_advect_host(pwadv_ctx *c, const double *u, const double *v, const 
     if (e != cudaSuccess) return set_cuda_error("coefficient upload", e);
     h2d += 2 * nz * sizeof(double);
     pwadv_opts o = opts ? *opts : pwadv_opts{0u, 0, 0, 0, 0, 0, nullptr};
+    bool all_pinned = true;
+    for (int m = 0; m < 3; ++m) all_pinned = all_pinned && is_pinned(hin[m]) && is_pinned(hout[m]);
+    if (!all_pinned) {
+        uint64_t sh2d = 0, sd2h = 0;
+        int rc = advect_host_staged(c, hin, hout, tcx, tcy, &o, &sh2d, &sd2h);
+        if (rc) return rc;
+        c->last_h2d = h2d + sh2d;
+        c->last_d2h = sd2h;
+        return PWADV_OK;
+    }
     int64_t copied = 0;  // input planes [0, copied) are on the device
     int64_t base = nx / chunks, rem = nx % chunks, x = 1;
     for (int ch = 0; ch < chunks; ++ch) {

@@ -8,6 +8,8 @@ Ports of the reference's hot-path known-answer tests
 test_schedules.py) run through the GPU here.
 """
 
+import json
+
 import numpy as np
 import pytest
 import torch
@@ -365,3 +367,16 @@ def test_time_stepping_graph_replay_matches_oracle():
     oracle.step(u, v, w, co.tcx, co.tcy, co.tzc1, co.tzc2, 0.1, steps, engines=oracle.host_threads())
     assert_bitwise([f.cpu().numpy() for f in st.fields], (u, v, w), "stepping")
     assert np.all(st.fields[2][1:-1, 1:-1, 0].cpu().numpy() == 0.0)  # w at k=0 stays 0
+
+
+def test_cli_bench_rows_and_checksums(tmp_path, capsys):
+    from paper_2010_01545_b200 import cli
+    out = tmp_path / "rows.json"
+    rc = cli.main(["bench", "--grid", "24x20x16", "--schedule", "xmarch", "--schedule", "simple",
+                   "--schedule", "x_reordered", "--engines", "3", "--reps", "2", "--out", str(out),
+                   "--format", "json"])
+    assert rc == 0
+    rows = json.loads(out.read_text())
+    assert [r["schedule"] for r in rows] == ["xmarch", "simple", "x_reordered"]
+    assert len({(r["checksum_su"], r["checksum_sv"], r["checksum_sw"]) for r in rows}) == 1
+    assert all(r["wall_min_s"] > 0 for r in rows)

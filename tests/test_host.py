@@ -217,3 +217,15 @@ def test_plan_traffic_accounting():
     assert tr.external_writes == interior_in
     simple = plan_traffic(dims, (1, 513, 1, 513), {"kernel": "simple"})
     assert simple.external_reads == 27 * 512 * 512 * 63
+
+
+def test_cli_parser_and_schedule_names():
+    from paper_2010_01545_b200 import cli
+    p = cli.build_parser()
+    a = p.parse_args(["bench", "--grid", "8x6x4", "--schedule", "x-reordered", "--schedule", "simple_fma"])
+    assert a.grid.cells == 192 and a.schedule == ["x_reordered", "simple_fma"]
+    with pytest.raises(SystemExit):
+        p.parse_args(["bench", "--grid", "8x6"])
+    with pytest.raises(SystemExit):
+        p.parse_args(["bench", "--grid", "8x6x4", "--schedule", "nonsense"])
+    assert cli.BENCH_COLUMNS[:3] == ("schedule", "engines", "y_batch")
