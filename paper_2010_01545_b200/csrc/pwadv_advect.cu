@@ -17,9 +17,9 @@
 //    the same pass, so each input byte crosses HBM about once and each output
 //    byte once (48 B per point). fp64 CUDA cores only: this is
 //    not a contraction, no tensor cores.
-//    Work distribution: the (strip, plane) space is split evenly over a
-//    persistent grid of one CTA per SM; a CTA crossing a strip boundary just
-//    continues its plane sequence (the ring never drains).
+//    Work distribution: (X chunk, strip) units dealt round-robin to a
+//    persistent grid of one CTA per SM (see Unit below); a CTA moving to its
+//    next unit just continues its plane sequence (the ring never drains).
 //
 //  * k_advect_simple — one thread per output point, direct global loads. Used
 //    for shapes the X-march does not cover (odd nz, misaligned pointers, very
