@@ -7,8 +7,12 @@ A "step" is one PW-advection evaluation (su, sv, sw from u, v, w) over the
 whole grid (configs c0-c3), or one forward-Euler step (config c4: exchange +
 fused advect/update). N=1 runs BASELINE.json configs[1] (512x512x64) by
 default. N>1 (torchrun, one rank per GPU, NCCL) runs a px x py x-y
-decomposition with a 1-cell halo exchange before each evaluation, weak
-scaling (the per-GPU block is the config's grid). Device time from CUDA events
+decomposition (1x2, 2x2, 2x4) with a 1-cell halo exchange before each
+evaluation overlapped with the interior compute; weak scaling by default (each
+GPU holds the config's grid), strong for c2 (BASELINE's strong-scaling config:
+1024x1024x64 split over the GPUs, `--scaling` overrides). c4 steps a
+2048x1024x128 block per GPU — BASELINE's 4096x4096x128 at 2x4 — with the
+exchange fused into the step kernel (peer stores over NVLink). Device time from CUDA events
 on the launching stream, barrier + synchronize around the timed region, max
 over ranks. Inputs (0.8-13 GB per evaluation) are larger than the 126 MB L2,
 so no L2 flush is needed between steps.
@@ -202,22 +206,30 @@ def run_ours(args):
     nx, ny, nz, desc = CONFIGS[args.config]
     px, py = decomposition(ws)
     stepping = args.config == "c4"
-    if args.config == "c4" and ws == 1 and not args.full_c4:
-        # the 2x4 config's per-GPU block (4096/2 x 4096/4 x 128)
+    if args.config == "c4" and not (ws == 1 and args.full_c4):
+        # the 2x4 config's per-GPU block (4096/2 x 4096/4 x 128): weak scaling
+        # from 1 GPU reaches BASELINE's 4096x4096x128 exactly at 8 GPUs (2x4)
         nx, ny = 2048, 1024
-        desc = "BASELINE configs[4] per-GPU block 2048x1024x128 (of 4096x4096x128 at 2x4), forward-Euler step"
-    dims = pw.make_grid(nx, ny, nz)  # per-GPU block (weak scaling)
+        desc = "BASELINE configs[4]: forward-Euler step, 2048x1024x128 per GPU (4096x4096x128 at 2x4)"
+    scaling = args.scaling or ("strong" if args.config == "c2" else "weak")
+    if scaling == "strong":
+        gx, gy = nx, ny               # the config grid is the global grid
+    else:
+        gx, gy = px * nx, py * ny     # the config grid is each GPU's block
     opts = device.make_opts(args.variant)
     stream = torch.cuda.current_stream(dev)
 
     # inputs generated on the device (K5, reference LCG stream + BASELINE map)
-    gx, gy = px * nx, py * ny
     if ws == 1:
+        dims = pw.make_grid(gx, gy, nz)
         fields = device.fill(dims, pw.GeneratorSpec.baseline(SEED), device=dev)
     else:
         from paper_2010_01545_b200 import decomp
         dec = decomp.Decomposition(pw.make_grid(gx, gy, nz), px, py, rank)
+        dims = dec.local_dims
         fields = dec.fill_local(pw.GeneratorSpec.baseline(SEED), device=dev)
+    nx, ny = dims.nx, dims.ny
+    global_points = gx * gy * nz
     co = device.DeviceCoefficients.from_host(pw.baseline_coefficients(SEED, nz), dev)
     out = device.alloc_fields(dims, dev)
 
@@ -282,7 +294,7 @@ def run_ours(args):
         ms = float(t.item())
     ms_step = ms / args.steps
     pts_rank = dims.cells
-    value = pts_rank * ws * args.steps / (ms / 1e3) / 1e9
+    value = global_points * args.steps / (ms / 1e3) / 1e9
 
     # dominant-kernel roofline: per-launch duration of K1/K4 alone (N=1: the
     # step is exactly one launch; N>1: time the interior kernel separately)
@@ -361,7 +373,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: reference Knuth-MMIX LCG stream (seed 42) mapped to [-10,10], "
                     "w=0 at k=0 and k=nz-1, tzc in [1e-3,5e-3), tcx=tcy=0.005 (BASELINE.json)",
             "config": {"workload": desc, "nx": nx, "ny": ny, "nz": nz,
@@ -431,6 +443,9 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--full-c4", action="store_true", help="c4 on one GPU at the full 4096x4096x128")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default=None,
+                    help="N>1: weak = the config grid per GPU (default), strong = the config grid "
+                         "split over the GPUs (default for c2, BASELINE's strong-scaling config)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
