@@ -55,9 +55,8 @@ enum {
 #define PWADV_FLAG_FMA 1u           /* contract into DFMA (not bit-exact; <=1e-12 normwise) */
 #define PWADV_FLAG_SIMPLE 2u        /* force the one-thread-per-point kernel */
 /* ablation switches for profiling only (results are NOT the PW sources):
- * skip the arithmetic / skip waiting for staged planes */
+ * skip the PW arithmetic / skip the output stores of the X-march kernel */
 #define PWADV_FLAG_DEBUG_NO_COMPUTE 0x100u
-#define PWADV_FLAG_DEBUG_NO_WAIT 0x200u
 #define PWADV_FLAG_DEBUG_NO_STORE 0x400u
 
 /* Optional tuning / variant selection; pass NULL for defaults. */
@@ -225,6 +224,17 @@ int pwadv_ctx_advect_host(pwadv_ctx *ctx,
                           double *su, double *sv, double *sw,
                           double tcx, double tcy, const double *tzc1, const double *tzc2,
                           int32_t chunks, const pwadv_opts *opts);
+/* Asynchronous form for streams of grids (page-locked host buffers only):
+ * enqueues one evaluation exactly like pwadv_ctx_advect_host and returns;
+ * consecutive submissions alternate between two device buffer sets so the H2D
+ * of one overlaps the K1/D2H of the previous. Host buffers must stay valid
+ * until pwadv_ctx_sync returns (it waits for every submission). */
+int pwadv_ctx_submit_host(pwadv_ctx *ctx,
+                          const double *u, const double *v, const double *w,
+                          double *su, double *sv, double *sw,
+                          double tcx, double tcy, const double *tzc1, const double *tzc2,
+                          int32_t chunks, const pwadv_opts *opts);
+int pwadv_ctx_sync(pwadv_ctx *ctx);
 /* Bytes moved host->device and device->host by the last ctx_advect_host call. */
 int pwadv_ctx_last_bytes(const pwadv_ctx *ctx, uint64_t *h2d, uint64_t *d2h);
 

@@ -96,6 +96,8 @@ SIGNATURES = {
     "pwadv_ctx_create": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, _I64, _I64, _I64]),
     "pwadv_ctx_destroy": (ctypes.c_int, [_P]),
     "pwadv_ctx_advect_host": (ctypes.c_int, [_P] * 7 + [_D, _D, _P, _P, ctypes.c_int32, _P]),
+    "pwadv_ctx_submit_host": (ctypes.c_int, [_P] * 7 + [_D, _D, _P, _P, ctypes.c_int32, _P]),
+    "pwadv_ctx_sync": (ctypes.c_int, [_P]),
     "pwadv_ctx_last_bytes": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint64),
                                             ctypes.POINTER(ctypes.c_uint64)]),
 }

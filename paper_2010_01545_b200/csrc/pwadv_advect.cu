@@ -96,8 +96,7 @@ struct TileCfg {
     int kp;           // threads per column (= nz/2)
     int stages;       // ring depth
     int nchunks;      // X chunks per strip; work unit = (chunk, strip)
-    int debug;        // ablation bits (PWADV_FLAG_DEBUG_*): 1 = no compute, 2 = no data waits,
-                      // 4 = no stores
+    int debug;        // ablation bits (PWADV_FLAG_DEBUG_*): 1 = no PW arithmetic, 4 = no stores
     int64_t nstrips;  // ceil((y1-y0)/tj)
 };
 
@@ -347,7 +346,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT)) k_advect_xmarch(BoxAr
         }
     };
     auto wait_next = [&]() -> const double * {
-        if (!(t.debug & 2)) mbar_wait(&full[cst], cph);
+        mbar_wait(&full[cst], cph);
         if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && cseq < 4096) a.trace[2 * cseq + 1] = gtime();
         return ring + (size_t)cst * 3 * CS;
     };
@@ -508,12 +507,6 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT)) k_advect_xmarch(BoxAr
         }
         release(cseq - 1, pst);  // plane ie was only read as the x+1 plane
     }
-    if (t.debug & 2) {  // ablation: drain the copies still in flight before exit
-        for (int n = 0; n < S && n < total; ++n) {
-            const int q = total - 1 - n;
-            mbar_wait(&full[q % S], (uint32_t)((q / S) & 1));
-        }
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -561,7 +554,7 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         t.kp = plan.kp;
         t.stages = plan.stages;
         t.nchunks = plan.nchunks;
-        t.debug = (int)((L.flags >> 8) & 7u);
+        t.debug = (int)((L.flags >> 8) & 5u);
         t.nstrips = plan.nstrips;
         void (*kern)(BoxArgs, TileCfg) = nullptr;
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary

@@ -483,6 +483,11 @@ struct pwadv_ctx {
     double *pin_in[2], *pin_out[2];
     int64_t pin_planes;  // planes per field a staging buffer holds
     cudaEvent_t ev_h2d[2], ev_d2h[2];
+    // asynchronous submissions alternate between two device buffer sets
+    double *set2_in[3], *set2_out[3], *set2_tz;  // set 1 (lazily allocated)
+    cudaEvent_t ev_in_free[2], ev_out_free[2];   // set s's inputs / outputs no longer in use
+    bool set_used[2];
+    uint64_t submits;
 };
 
 
@@ -532,6 +537,15 @@ int pwadv_ctx_destroy(pwadv_ctx *c)
         if (c->ev_d2h[b]) cudaEventDestroy(c->ev_d2h[b]);
     }
     delete c->pool;
+    for (int m = 0; m < 3; ++m) {
+        if (c->set2_in[m]) cudaFree(c->set2_in[m]);
+        if (c->set2_out[m]) cudaFree(c->set2_out[m]);
+    }
+    if (c->set2_tz) cudaFree(c->set2_tz);
+    for (int b = 0; b < 2; ++b) {
+        if (c->ev_in_free[b]) cudaEventDestroy(c->ev_in_free[b]);
+        if (c->ev_out_free[b]) cudaEventDestroy(c->ev_out_free[b]);
+    }
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_cmp) cudaStreamDestroy(c->s_cmp);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
@@ -646,6 +660,77 @@ static int advect_host_staged(pwadv_ctx *c, const double *const hin[3], double *
     return drain(chunks - 1, prev_o0, prev_o1);
 }
 
+// Page-locked host buffers: H2D, K1 and D2H of X-slab chunks on three streams
+// into buffer set `set`; returns once everything is enqueued. Waits (on the
+// device) until the set's previous use has released its inputs / outputs.
+static int enqueue_pinned(pwadv_ctx *c, int set, const double *const hin[3], double *const hout[3],
+                          double tcx, double tcy, int chunks, const pwadv_opts *o, uint64_t *h2d,
+                          uint64_t *d2h)
+{
+    const int64_t nx = c->nx, ny = c->ny, nz = c->nz;
+    const size_t plane = (size_t)(ny + 2) * nz;
+    const size_t pb = plane * sizeof(double);
+    double *din[3], *dout[3];
+    for (int m = 0; m < 3; ++m) {
+        din[m] = set ? c->set2_in[m] : c->d_in[m];
+        dout[m] = set ? c->set2_out[m] : c->d_out[m];
+    }
+    const double *tz = set ? c->set2_tz : c->d_tz;
+    while ((int)c->ev_in.size() < chunks) {
+        cudaEvent_t a, b;
+        cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
+        c->ev_in.push_back(a);
+        c->ev_cmp.push_back(b);
+    }
+    if (!c->ev_in_free[set]) {
+        cudaEventCreateWithFlags(&c->ev_in_free[set], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&c->ev_out_free[set], cudaEventDisableTiming);
+    }
+    if (c->set_used[set]) {
+        cudaStreamWaitEvent(c->s_h2d, c->ev_in_free[set], 0);   // kernels done reading inputs
+        cudaStreamWaitEvent(c->s_cmp, c->ev_out_free[set], 0);  // D2H done reading outputs
+    }
+    cudaError_t e;
+    int64_t copied = 0;  // input planes [0, copied) are on the device
+    int64_t base = nx / chunks, rem = nx % chunks, x = 1;
+    for (int ch = 0; ch < chunks; ++ch) {
+        const int64_t x0 = x, x1 = x + base + (ch < rem ? 1 : 0);
+        x = x1;
+        const int64_t need = (ch == chunks - 1) ? nx + 2 : x1 + 1;  // planes up to x1 inclusive
+        if (need > copied) {
+            for (int m = 0; m < 3; ++m) {
+                e = cudaMemcpyAsync(din[m] + copied * plane, hin[m] + copied * plane,
+                                    (need - copied) * pb, cudaMemcpyHostToDevice, c->s_h2d);
+                if (e != cudaSuccess) return set_cuda_error("H2D", e);
+            }
+            *h2d += 3 * (uint64_t)(need - copied) * pb;
+            copied = need;
+        }
+        cudaEventRecord(c->ev_in[ch], c->s_h2d);
+        cudaStreamWaitEvent(c->s_cmp, c->ev_in[ch], 0);
+        int rc = pwadv_advect_box_f64(din[0], din[1], din[2], dout[0], dout[1], dout[2], nx, ny, nz,
+                                      tcx, tcy, tz, tz + nz, x0, x1, 1, ny + 1, o, c->s_cmp);
+        if (rc) return rc;
+        cudaEventRecord(c->ev_cmp[ch], c->s_cmp);
+        cudaStreamWaitEvent(c->s_d2h, c->ev_cmp[ch], 0);
+        // output planes of this chunk; the first/last chunk also returns the
+        // all-zero halo planes 0 / nx+1 so host outputs match zeros_sources
+        const int64_t o0 = (ch == 0) ? 0 : x0;
+        const int64_t o1 = (ch == chunks - 1) ? nx + 2 : x1;
+        for (int m = 0; m < 3; ++m) {
+            e = cudaMemcpyAsync(hout[m] + o0 * plane, dout[m] + o0 * plane, (o1 - o0) * pb,
+                                cudaMemcpyDeviceToHost, c->s_d2h);
+            if (e != cudaSuccess) return set_cuda_error("D2H", e);
+        }
+        *d2h += 3 * (uint64_t)(o1 - o0) * pb;
+    }
+    cudaEventRecord(c->ev_in_free[set], c->s_cmp);
+    cudaEventRecord(c->ev_out_free[set], c->s_d2h);
+    c->set_used[set] = true;
+    return PWADV_OK;
+}
+
 int pwadv_ctx_advect_host(pwadv_ctx *c, const double *u, const double *v, const double *w,
                           double *su, double *sv, double *sw, double tcx, double tcy,
                           const double *tzc1, const double *tzc2, int32_t chunks,
@@ -658,19 +743,11 @@ int pwadv_ctx_advect_host(pwadv_ctx *c, const double *u, const double *v, const 
     const int64_t nx = c->nx, ny = c->ny, nz = c->nz;
     if (chunks < 1) chunks = 1;
     if (chunks > nx) chunks = (int32_t)nx;
-    while ((int)c->ev_in.size() < chunks) {
-        cudaEvent_t a, b;
-        cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&b, cudaEventDisableTiming);
-        c->ev_in.push_back(a);
-        c->ev_cmp.push_back(b);
-    }
-    const size_t plane = (size_t)(ny + 2) * nz;  // doubles per i-plane
-    const size_t pb = plane * sizeof(double);
     const double *hin[3] = {u, v, w};
     double *hout[3] = {su, sv, sw};
     uint64_t h2d = 0, d2h = 0;
     cudaError_t e;
+    if (c->set_used[0]) cudaStreamWaitEvent(c->s_h2d, c->ev_in_free[0], 0);
     e = cudaMemcpyAsync(c->d_tz, tzc1, nz * sizeof(double), cudaMemcpyHostToDevice, c->s_h2d);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(c->d_tz + nz, tzc2, nz * sizeof(double), cudaMemcpyHostToDevice,
@@ -681,6 +758,10 @@ int pwadv_ctx_advect_host(pwadv_ctx *c, const double *u, const double *v, const 
     bool all_pinned = true;
     for (int m = 0; m < 3; ++m) all_pinned = all_pinned && is_pinned(hin[m]) && is_pinned(hout[m]);
     if (!all_pinned) {
+        if (c->set_used[0]) {  // an earlier asynchronous submission may still use set 0
+            cudaStreamWaitEvent(c->s_h2d, c->ev_in_free[0], 0);
+            cudaStreamWaitEvent(c->s_cmp, c->ev_out_free[0], 0);
+        }
         uint64_t sh2d = 0, sd2h = 0;
         int rc = advect_host_staged(c, hin, hout, tcx, tcy, &o, &sh2d, &sd2h);
         if (rc) return rc;
@@ -688,44 +769,66 @@ int pwadv_ctx_advect_host(pwadv_ctx *c, const double *u, const double *v, const 
         c->last_d2h = sd2h;
         return PWADV_OK;
     }
-    int64_t copied = 0;  // input planes [0, copied) are on the device
-    int64_t base = nx / chunks, rem = nx % chunks, x = 1;
-    for (int ch = 0; ch < chunks; ++ch) {
-        const int64_t x0 = x, x1 = x + base + (ch < rem ? 1 : 0);
-        x = x1;
-        const int64_t need = (ch == chunks - 1) ? nx + 2 : x1 + 1;  // planes up to x1 inclusive
-        if (need > copied) {
-            for (int m = 0; m < 3; ++m) {
-                e = cudaMemcpyAsync(c->d_in[m] + copied * plane, hin[m] + copied * plane,
-                                    (need - copied) * pb, cudaMemcpyHostToDevice, c->s_h2d);
-                if (e != cudaSuccess) return set_cuda_error("H2D", e);
-            }
-            h2d += 3 * (uint64_t)(need - copied) * pb;
-            copied = need;
-        }
-        cudaEventRecord(c->ev_in[ch], c->s_h2d);
-        cudaStreamWaitEvent(c->s_cmp, c->ev_in[ch], 0);
-        int rc = pwadv_advect_box_f64(c->d_in[0], c->d_in[1], c->d_in[2], c->d_out[0],
-                                      c->d_out[1], c->d_out[2], nx, ny, nz, tcx, tcy, c->d_tz,
-                                      c->d_tz + nz, x0, x1, 1, ny + 1, &o, c->s_cmp);
-        if (rc) return rc;
-        cudaEventRecord(c->ev_cmp[ch], c->s_cmp);
-        cudaStreamWaitEvent(c->s_d2h, c->ev_cmp[ch], 0);
-        // output planes of this chunk; the first/last chunk also returns the
-        // all-zero halo planes 0 / nx+1 so host outputs match zeros_sources
-        const int64_t o0 = (ch == 0) ? 0 : x0;
-        const int64_t o1 = (ch == chunks - 1) ? nx + 2 : x1;
-        for (int m = 0; m < 3; ++m) {
-            e = cudaMemcpyAsync(hout[m] + o0 * plane, c->d_out[m] + o0 * plane, (o1 - o0) * pb,
-                                cudaMemcpyDeviceToHost, c->s_d2h);
-            if (e != cudaSuccess) return set_cuda_error("D2H", e);
-        }
-        d2h += 3 * (uint64_t)(o1 - o0) * pb;
-    }
+    int rc = enqueue_pinned(c, 0, hin, hout, tcx, tcy, chunks, &o, &h2d, &d2h);
+    if (rc) return rc;
     e = cudaStreamSynchronize(c->s_d2h);
     if (e != cudaSuccess) return set_cuda_error("ctx_advect_host sync", e);
     c->last_h2d = h2d;
     c->last_d2h = d2h;
+    return PWADV_OK;
+}
+
+int pwadv_ctx_submit_host(pwadv_ctx *c, const double *u, const double *v, const double *w,
+                          double *su, double *sv, double *sw, double tcx, double tcy,
+                          const double *tzc1, const double *tzc2, int32_t chunks,
+                          const pwadv_opts *opts)
+{
+    if (!c) return set_error(PWADV_E_NULL, "null ctx");
+    if (!u || !v || !w || !su || !sv || !sw || !tzc1 || !tzc2)
+        return set_error(PWADV_E_NULL, "null pointer argument");
+    DeviceGuard g(c->device);
+    const double *hin[3] = {u, v, w};
+    double *hout[3] = {su, sv, sw};
+    for (int m = 0; m < 3; ++m)
+        if (!is_pinned(hin[m]) || !is_pinned(hout[m]))
+            return set_error(PWADV_E_ARG, "asynchronous submission needs page-locked host buffers");
+    const int64_t nx = c->nx, ny = c->ny, nz = c->nz;
+    cudaError_t e = cudaSuccess;
+    if (!c->set2_in[0]) {
+        const size_t n = (size_t)(nx + 2) * (ny + 2) * nz;
+        for (int m = 0; m < 3 && e == cudaSuccess; ++m) e = cudaMalloc(&c->set2_in[m], n * sizeof(double));
+        for (int m = 0; m < 3 && e == cudaSuccess; ++m) e = cudaMalloc(&c->set2_out[m], n * sizeof(double));
+        if (e == cudaSuccess) e = cudaMalloc(&c->set2_tz, 2 * (size_t)nz * sizeof(double));
+        for (int m = 0; m < 3 && e == cudaSuccess; ++m) e = cudaMemset(c->set2_out[m], 0, n * sizeof(double));
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return set_cuda_error("second buffer set", e);
+    }
+    if (chunks < 1) chunks = 1;
+    if (chunks > nx) chunks = (int32_t)nx;
+    const int set = (int)(c->submits & 1);
+    ++c->submits;
+    pwadv_opts o = opts ? *opts : pwadv_opts{0u, 0, 0, 0, 0, 0, nullptr};
+    uint64_t h2d = 0, d2h = 0;
+    double *tz = set ? c->set2_tz : c->d_tz;
+    if (c->set_used[set]) cudaStreamWaitEvent(c->s_h2d, c->ev_in_free[set], 0);
+    e = cudaMemcpyAsync(tz, tzc1, nz * sizeof(double), cudaMemcpyHostToDevice, c->s_h2d);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(tz + nz, tzc2, nz * sizeof(double), cudaMemcpyHostToDevice, c->s_h2d);
+    if (e != cudaSuccess) return set_cuda_error("coefficient upload", e);
+    h2d += 2 * nz * sizeof(double);
+    int rc = enqueue_pinned(c, set, hin, hout, tcx, tcy, chunks, &o, &h2d, &d2h);
+    if (rc) return rc;
+    c->last_h2d = h2d;
+    c->last_d2h = d2h;
+    return PWADV_OK;
+}
+
+int pwadv_ctx_sync(pwadv_ctx *c)
+{
+    if (!c) return set_error(PWADV_E_NULL, "null ctx");
+    DeviceGuard g(c->device);
+    cudaError_t e = cudaStreamSynchronize(c->s_d2h);
+    if (e != cudaSuccess) return set_cuda_error("ctx_sync", e);
     return PWADV_OK;
 }
 

@@ -255,3 +255,24 @@ class HostContext:
         a, b = ctypes.c_uint64(), ctypes.c_uint64()
         _lib.check(_lib.lib().pwadv_ctx_last_bytes(self._h, ctypes.byref(a), ctypes.byref(b)))
         return int(a.value), int(b.value)
+
+    def submit_host(self, u, v, w, su, sv, sw, tcx, tcy, tzc1, tzc2, chunks: int = 16,
+                    opts: _lib.Opts | None = None) -> tuple[int, int]:
+        """Asynchronous advect_host for page-locked buffers (consecutive submissions
+        pipeline H2D / K1 / D2H across grids); call sync() before reading outputs."""
+        d = self.dims
+        tz1 = np.ascontiguousarray(tzc1, dtype=np.float64)
+        tz2 = np.ascontiguousarray(tzc2, dtype=np.float64)
+        if tz1.shape != (d.nz,) or tz2.shape != (d.nz,):
+            raise ValueError(f"coefficient length {tz1.shape} != nz {d.nz}")
+        self._keep = (tz1, tz2)  # the coefficient upload is asynchronous
+        _lib.check(_lib.lib().pwadv_ctx_submit_host(
+            self._h, self._hp(u), self._hp(v), self._hp(w), self._hp(su), self._hp(sv),
+            self._hp(sw), float(tcx), float(tcy), ctypes.c_void_p(tz1.ctypes.data),
+            ctypes.c_void_p(tz2.ctypes.data), int(chunks), _lib.opts_ptr(opts)))
+        a, b = ctypes.c_uint64(), ctypes.c_uint64()
+        _lib.check(_lib.lib().pwadv_ctx_last_bytes(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return int(a.value), int(b.value)
+
+    def sync(self) -> None:
+        _lib.check(_lib.lib().pwadv_ctx_sync(self._h))
