@@ -91,6 +91,16 @@ __device__ __forceinline__ void push_boundary(const BoxArgs &A, int64_t i, int64
     if (xp && yp) push_to<N>(p, PWADV_NB_XPYP, 0, 0, nz, k, a, b, c);
 }
 
+// The boundary path of the fused step, out of line: only the few threads on a
+// block face take it, and keeping it out of the march keeps the march's
+// registers (the kernel parameters are __grid_constant__, so no copy is made).
+__device__ __noinline__ void push_pair(const BoxArgs *A, int64_t i, int64_t j, int64_t k0, double a0,
+                                       double a1, double b0, double b1, double c0, double c1)
+{
+    const double pa[2] = {a0, a1}, pb[2] = {b0, b1}, pc[2] = {c0, c1};
+    push_boundary<2>(*A, i, j, k0, pa, pb, pc);
+}
+
 struct TileCfg {
     int tj;           // columns per strip
     int kp;           // threads per column (= nz/2)
@@ -269,7 +279,8 @@ __device__ __forceinline__ void issue_plane(const RingState *rs, const BoxArgs &
 __host__ __device__ constexpr int ctas_per_sm(int maxt) { return maxt <= 128 ? 3 : (maxt <= 192 ? 2 : 1); }
 
 template <bool FMA, bool STEP, int MAXT, bool FIX>
-__global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT)) k_advect_xmarch(BoxArgs a, TileCfg t)
+__global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
+    k_advect_xmarch(const __grid_constant__ BoxArgs a, const __grid_constant__ TileCfg t)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int S = t.stages, TJ = t.tj, KP = t.kp;
@@ -478,10 +489,9 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT)) k_advect_xmarch(BoxAr
                 store2(o2, sw_a, sw_b);
             }
             if constexpr (STEP) {
-                if (a.push && active) {
-                    const double pa[2] = {su_a, su_b}, pb[2] = {sv_a, sv_b}, pc[2] = {sw_a, sw_b};
-                    push_boundary<2>(a, ci, j0 + c, k0, pa, pb, pc);
-                }
+                if (a.push && active &&
+                    (ci == 1 || ci == a.nx || j0 + c == 1 || j0 + c == a.ny))
+                    push_pair(&a, ci, j0 + c, k0, su_a, su_b, sv_a, sv_b, sw_a, sw_b);
             }
             ++ci;
             o0 += ostep;

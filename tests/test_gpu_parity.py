@@ -403,3 +403,17 @@ def test_async_host_submissions_bitwise():
     ctx.advect_host(*hin, *o, co.tcx, co.tcy, *tz)
     assert all(torch.equal(a.view(torch.int64), b.view(torch.int64)) for a, b in zip(o, want))
     ctx.close()
+
+
+@pytest.mark.parametrize("shape", [(5, 4, 300), (3, 3, 512), (2, 3, 1024), (2, 2, 1030), (4, 3, 3)])
+def test_tall_and_odd_columns_bitwise(shape):
+    # narrow X-march tiles (nz 300, 512), the one-thread-per-point fallback
+    # (nz 1024 > thread budget, odd nz), all against the oracle
+    nx, ny, nz = shape
+    u, v, w = oracle.fill_random(nx, ny, nz, 17, baseline=True)
+    co = oracle.baseline_coefficients(17, nz)
+    args = (co["tcx"], co["tcy"], co["tzc1"], co["tzc2"])
+    got, dims = gpu_advect(u, v, w, *args)
+    assert_bitwise(got, oracle.advect(u, v, w, *args), shape)
+    plan = device.describe_plan(dims)
+    assert plan["kernel"] == ("xmarch" if nz in (300, 512) else "simple")
