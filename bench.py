@@ -320,6 +320,9 @@ def run_ours(args):
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": tr.get("bytes"),
                 "traffic_source": tr.get("source"),
+                "ncu": ({k: tr.get(k) for k in ("duration_us", "dram_read", "dram_write",
+                                                "dram_throughput_pct", "fp64_pipe_pct",
+                                                "issue_active_pct", "registers")} if tr else None),
                 "peak_source": peak_src, "kernel_ms": round(kern_ms, 5),
                 "algorithmic_bytes_per_launch": BYTES_PER_POINT * pts_rank,
                 "bytes_per_point": BYTES_PER_POINT,
