@@ -54,6 +54,7 @@ enum {
 /* flags for pwadv_opts.flags */
 #define PWADV_FLAG_FMA 1u           /* contract into DFMA (not bit-exact; <=1e-12 normwise) */
 #define PWADV_FLAG_SIMPLE 2u        /* force the one-thread-per-point kernel */
+#define PWADV_FLAG_RIM 16u          /* only the one-cell rim of the box (one launch; multi-GPU overlap) */
 /* ablation switches for profiling only (results are NOT the PW sources):
  * skip the PW arithmetic / skip the output stores of the X-march kernel */
 #define PWADV_FLAG_DEBUG_NO_COMPUTE 0x100u

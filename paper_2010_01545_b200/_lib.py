@@ -35,6 +35,7 @@ PWADV_E_ALIGN = -6
 
 FLAG_FMA = 1
 FLAG_SIMPLE = 2
+FLAG_RIM = 16
 
 
 class Opts(ctypes.Structure):

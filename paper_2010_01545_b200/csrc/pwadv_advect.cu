@@ -47,6 +47,7 @@ struct BoxArgs {
     int64_t x0, x1, y0, y1;  // interior box, 1-based, half-open
     unsigned long long *trace;  // profiling only: per-plane issue/arrival timestamps (CTA 0)
     int push;                   // fused step only: also store boundary values into peers' halos
+    int rim;                    // simple kernel: only the one-cell rim of the box (x0/x1-1/y0/y1-1)
     pwadv_peers peers;          // (include/pwadv.h) the neighbours' new buffers and extents
 };
 
@@ -140,14 +141,27 @@ __global__ void __launch_bounds__(256) k_advect_simple(BoxArgs a)
 {
     const int64_t nz = a.nz, ny2 = a.ny + 2;
     const int64_t nbx = a.x1 - a.x0, nby = a.y1 - a.y0;
-    const int64_t total = nbx * nby * nz;
+    // rim mode (nbx, nby >= 3): columns of the planes x0 and x1-1, then of the
+    // rows y0 and y1-1 between them — the part of a block that needs halos
+    const int64_t ncols = a.rim ? 2 * nby + 2 * (nbx - 2) : nbx * nby;
+    const int64_t total = ncols * nz;
     const int64_t sI = ny2 * nz, sJ = nz;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = idx % nz;
         const int64_t col = idx / nz;
-        const int64_t i = a.x0 + col / nby;
-        const int64_t j = a.y0 + col % nby;
+        int64_t i, j;
+        if (!a.rim) {
+            i = a.x0 + col / nby;
+            j = a.y0 + col % nby;
+        } else if (col < 2 * nby) {
+            i = col < nby ? a.x0 : a.x1 - 1;
+            j = a.y0 + (col < nby ? col : col - nby);
+        } else {
+            const int64_t r = col - 2 * nby;
+            i = a.x0 + 1 + (r < nbx - 2 ? r : r - (nbx - 2));
+            j = r < nbx - 2 ? a.y0 : a.y1 - 1;
+        }
         const int64_t o = (i * ny2 + j) * nz + k;
         double r0 = 0.0, r1 = 0.0, r2 = 0.0;
         if (k > 0) {
@@ -547,6 +561,7 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
     a.y1 = L.y1;
     a.trace = reinterpret_cast<unsigned long long *>(L.trace);
     a.push = L.peers != nullptr ? 1 : 0;
+    a.rim = (L.flags & PWADV_FLAG_RIM) && (L.x1 - L.x0) >= 3 && (L.y1 - L.y0) >= 3 ? 1 : 0;
     if (L.peers) a.peers = *L.peers;
     else a.peers = pwadv_peers{};
     const bool fma = (L.flags & PWADV_FLAG_FMA) != 0;
@@ -592,7 +607,7 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute", e);
         kern<<<plan.grid, plan.threads, plan.smem, stream>>>(a, t);
     } else {
-        const int64_t total = nbx * nby * L.nz;
+        const int64_t total = (a.rim ? 2 * nby + 2 * (nbx - 2) : nbx * nby) * L.nz;
         int64_t blocks = (total + 255) / 256;
         const int64_t cap = (int64_t)dev->sms * 8;
         if (blocks > cap) blocks = cap;
@@ -617,7 +632,7 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
 
 bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
 {
-    if (L.flags & PWADV_FLAG_SIMPLE) return false;
+    if (L.flags & (PWADV_FLAG_SIMPLE | PWADV_FLAG_RIM)) return false;
     const int64_t nz = L.nz;
     if (nz % 2 != 0 || nz > 1024) return false;
     // 16-byte alignment for the bulk copies and the paired loads/stores

@@ -360,7 +360,7 @@ class HaloExchanger:
         rims = [(1, 2, 1, ny + 1), (nx, nx + 1, 1, ny + 1), (2, nx, 1, 2), (2, nx, ny, ny + 1)]
         return inner, rims
 
-    def run_overlapped(self, launch, fields, stream=None) -> None:
+    def run_overlapped(self, launch, fields, stream=None, opts=None) -> None:
         """Exchange halos on a side stream while `launch(box, stream)` computes
         the interior, then compute the rim once the halos have landed."""
         from . import device as dv
@@ -372,23 +372,28 @@ class HaloExchanger:
         if inner is not None:
             launch(inner, main)
         main.wait_stream(side)
-        simple = dv.make_opts("simple")
-        for b in rims:
-            launch(b, main, simple)
+        from . import _lib
+        rim = dv.make_opts("simple")  # same arithmetic build (FMA or exact) as the interior
+        rim.flags |= (opts.flags & _lib.FLAG_FMA) if opts is not None else 0
+        if inner is None:
+            launch(rims[0], main, rim)
+        else:  # the four one-cell strips in one launch
+            rim.flags |= _lib.FLAG_RIM
+            launch((1, self.dims.nx + 1, 1, self.dims.ny + 1), main, rim)
 
     def advect_overlapped(self, fields, coeffs, out, opts=None, stream=None) -> None:
         from . import device as dv
 
         def launch(box, s, o=None):
             dv.advect(*fields, coeffs, out, box=box, opts=o or opts, stream=s)
-        self.run_overlapped(launch, fields, stream)
+        self.run_overlapped(launch, fields, stream, opts)
 
     def step_overlapped(self, fields, coeffs, dt, out, opts=None, stream=None) -> None:
         from . import device as dv
 
         def launch(box, s, o=None):
             dv.step(*fields, coeffs, dt, out, box=box, opts=o or opts, stream=s)
-        self.run_overlapped(launch, fields, stream)
+        self.run_overlapped(launch, fields, stream, opts)
 
 
 def exchange_all_loopback(exchangers: list, fields_by_rank: list, stream=None) -> None:

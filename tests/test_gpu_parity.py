@@ -417,3 +417,18 @@ def test_tall_and_odd_columns_bitwise(shape):
     assert_bitwise(got, oracle.advect(u, v, w, *args), shape)
     plan = device.describe_plan(dims)
     assert plan["kernel"] == ("xmarch" if nz in (300, 512) else "simple")
+
+
+@pytest.mark.parametrize("variant", ["xmarch", "xmarch_fma"])
+def test_interior_plus_rim_launch_equals_full(variant):
+    dims, fields, co = baseline_case(23, 19, 64, seed=4)
+    full = device.advect(*fields, co, opts=device.make_opts(variant))
+    parts = device.alloc_fields(dims, "cuda")
+    device.advect(*fields, co, parts, box=(2, dims.nx, 2, dims.ny), opts=device.make_opts(variant))
+    rim = device.make_opts("simple_fma" if variant.endswith("_fma") else "simple")
+    rim.flags |= _lib.FLAG_RIM
+    _lib.reset_launch_count()
+    device.advect(*fields, co, parts, opts=rim)
+    assert _lib.launch_count() == 1
+    for a, b in zip(full, parts):
+        assert torch.equal(a.view(torch.int64), b.view(torch.int64))
