@@ -302,10 +302,17 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     const int CS = (TJ + 2) * nz;  // doubles per field per tile-plane
     double *ring = reinterpret_cast<double *>(smem_raw);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)S * 3 * CS * sizeof(double));
-    RingState *rs = reinterpret_cast<RingState *>(full + S);
+    uint64_t *empty = full + S;  // warp-specialised variant only
+    RingState *rs = reinterpret_cast<RingState *>(full + 2 * S);
+    // MAXT == 512: warp-specialised — warpgroups 0-2 compute, warpgroup 3 is
+    // the producer (one thread issuing refills as soon as a stage's last
+    // consumer warp arrives on its empty barrier; setmaxnreg moves the
+    // producer's registers to the consumers)
+    constexpr bool WS = (MAXT == 512);
+    constexpr int kComputeWarps = WS ? 12 : MAXT / 32;
 
     const int tid = threadIdx.x, lane = tid & 31;
-    const int nwarps = blockDim.x >> 5;
+    const int nwarps = WS ? kComputeWarps : (int)(blockDim.x >> 5);
     const bool in_tile = tid < TJ * KP;
     const int c = in_tile ? tid / KP : TJ - 1;
     const int kp = in_tile ? tid - (tid / KP) * KP : 0;
@@ -340,6 +347,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
         rs->nunits = k;
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kComputeWarps);
             rs->released[s] = 0;
         }
         fence_mbar_init();
@@ -349,6 +357,21 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     __syncthreads();
     const int total = rs->total;
     const int my_units = rs->nunits;
+    if constexpr (WS) {
+        if (tid >= 32 * kComputeWarps) {  // producer warpgroup
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+            if (tid == 32 * kComputeWarps) {
+                for (int q = (total < S ? total : S); q < total; ++q) {
+                    const int st = q % S;
+                    mbar_wait(&empty[st], (uint32_t)(((q / S) - 1) & 1));
+                    fence_proxy_async();
+                    issue_plane(rs, a, q, st, CS, ring, full);
+                }
+            }
+            return;
+        }
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 160;\n" ::: "memory");
+    }
 
     // consumer ring position: sequence number, stage and parity of the
     // plane to wait for next
@@ -358,6 +381,10 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
 
     auto release = [&](int seq, int st) {
         __syncwarp();
+        if constexpr (WS) {
+            if (lane == 0) mbar_arrive(&empty[st]);
+            return;
+        }
         if (lane == 0) {
             __threadfence_block();  // this warp's reads of the stage happen before the refill
             const int done = atomicAdd(&rs->released[st], 1);
@@ -592,6 +619,8 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
             kern = fma ? k_advect_xmarch<true, false, MT, FX>                    \
                        : k_advect_xmarch<false, false, MT, FX>;                  \
     }
+        PWADV_PICK(512, false)
+        PWADV_PICK(512, true)
         PWADV_PICK(384, false)
         PWADV_PICK(384, true)
         PWADV_PICK(256, false)
@@ -643,15 +672,19 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     const int64_t nby = L.y1 - L.y0, nbx = L.x1 - L.x0;
     // thread budget per CTA (register file / CTA): 384 by default, which
     // leaves ~168 registers per thread for the rolled x-window
-    int maxt = L.max_threads > 0 ? L.max_threads : 384;
-    if (maxt != 384 && maxt != 256 && maxt != 192 && maxt != 128) return false;
+    // default: warp-specialised 512 threads (3 compute warpgroups of 160
+    // registers + a producer warpgroup); measured 125 Gpts/s at C1/C3 vs 110
+    // for the 384-thread kernel whose warps issue the refills themselves
+    int maxt = L.max_threads > 0 ? L.max_threads : 512;
+    if (maxt != 512 && maxt != 384 && maxt != 256 && maxt != 192 && maxt != 128) return false;
+    const int tile_threads = maxt == 512 ? 384 : maxt;  // 512: 3 compute + 1 producer warpgroup
     const int per_sm = ctas_per_sm(maxt);
     if (kp > maxt) return false;
-    int tj = L.tile_j > 0 ? L.tile_j : maxt / kp;
-    if (tj > maxt / kp) tj = maxt / kp;
+    int tj = L.tile_j > 0 ? L.tile_j : tile_threads / kp;
+    if (tj > tile_threads / kp) tj = tile_threads / kp;
     if (tj < 1) return false;
     if (tj > nby) tj = (int)nby;
-    const size_t bar_bytes = 16 * sizeof(uint64_t) + sizeof(RingState);
+    const size_t bar_bytes = 2 * 16 * sizeof(uint64_t) + sizeof(RingState);
     // shared memory per CTA: the SM's 228 KB split between resident CTAs
     size_t smem_cap = (size_t)dev.smem_optin - bar_bytes - 1024;
     if (per_sm > 1) smem_cap = (size_t)(228 * 1024) / per_sm - bar_bytes - 1024 - 1024;
@@ -660,7 +693,7 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
         const size_t stage_bytes = (size_t)3 * (tj + 2) * nz * sizeof(double);
         int smax = (int)(smem_cap / stage_bytes);
         if (smax > 16) smax = 16;  // RingState::released
-        stages = L.stages > 0 ? (L.stages < smax ? L.stages : smax) : (smax < 8 ? smax : 8);
+        stages = L.stages > 0 ? (L.stages < smax ? L.stages : smax) : (smax < 5 ? smax : 5);  // 5 measured best (tools/sweep.py)
         if (stages >= 3) break;
         if (tj == 1) return false;
         tj = tj / 2;
@@ -669,8 +702,8 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     p->tj = tj;
     p->kp = kp;
     p->stages = stages;
-    p->threads = round_up(tj * kp, 32);
-    p->smem = (size_t)stages * 3 * (tj + 2) * nz * sizeof(double) + stages * sizeof(uint64_t) +
+    p->threads = maxt == 512 ? 512 : round_up(tj * kp, 32);
+    p->smem = (size_t)stages * 3 * (tj + 2) * nz * sizeof(double) + 2 * stages * sizeof(uint64_t) +
               sizeof(RingState);
     p->nstrips = (nby + tj - 1) / tj;
     // X chunking of the (chunk, strip) work units dealt round-robin to the

@@ -163,7 +163,8 @@ def test_dual_oracle_property_loop(variant):
 
 @pytest.mark.parametrize("tile_j,stages,grid,maxt,chunks", [
     (0, 0, 0, 0, 0), (1, 3, 7, 0, 0), (3, 4, 0, 256, 1), (5, 3, 1, 192, 3), (2, 0, 300, 384, 0),
-    (0, 0, 5, 128, 7), (4, 5, 2, 0, 40), (0, 3, 0, 0, 1000), (0, 0, 0, 192, 0)])
+    (0, 0, 5, 128, 7), (4, 5, 2, 0, 40), (0, 3, 0, 0, 1000), (0, 0, 0, 192, 0), (0, 0, 0, 512, 0),
+    (3, 3, 9, 512, 2)])
 def test_xmarch_tilings_bitwise(tile_j, stages, grid, maxt, chunks):
     # every tiling / ring depth / grid / chunking gives identical bits (units
     # dealt round-robin, CTAs running several units, partial strips, single-CTA
