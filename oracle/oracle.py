@@ -66,6 +66,11 @@ def lib():
         L.oracle_step.argtypes = [_D, _D, _D, _D, _I64, _I64, _I64, ctypes.c_double,
                                   ctypes.c_double, _D, _D, ctypes.c_double, ctypes.c_int]
         L.oracle_step.restype = ctypes.c_int
+        L.oracle_step_open.argtypes = L.oracle_step.argtypes
+        L.oracle_step_open.restype = ctypes.c_int
+        L.oracle_fill_box.argtypes = [_D, _D, _D, _I64, _I64, _I64, ctypes.c_uint64, ctypes.c_int,
+                                      _I64, _I64, _I64, _I64]
+        L.oracle_fill_box.restype = None
         _lib = L
     return _lib
 
@@ -98,6 +103,16 @@ def fill_random(nx: int, ny: int, nz: int, seed: int, baseline: bool = False):
     u, v, w = (np.empty(shape) for _ in range(3))
     lib().oracle_fill_random(_p(u), _p(v), _p(w), nx, ny, nz, seed & (2**64 - 1),
                              1 if baseline else 0)
+    return u, v, w
+
+
+def fill_box(gnx: int, gny: int, nz: int, seed: int, i0: int, j0: int, bnx: int, bny: int,
+             baseline: bool = False):
+    """(u, v, w) boxes of shape (bnx, bny, nz): global padded cells
+    (i0.., j0.., :) of fill_random(gnx, gny, nz, seed), taken periodically."""
+    u, v, w = (np.empty((bnx, bny, nz)) for _ in range(3))
+    lib().oracle_fill_box(_p(u), _p(v), _p(w), gnx, gny, nz, seed & (2**64 - 1),
+                          1 if baseline else 0, i0, j0, bnx, bny)
     return u, v, w
 
 
@@ -205,6 +220,34 @@ def step(u, v, w, tcx, tcy, tzc1, tzc2, dt: float, steps: int, engines: int = 1)
                                float(tcy), _p(tzc1), _p(tzc2), float(dt), int(engines))
         if rc:
             raise ValueError("oracle_step: bad arguments")
+
+
+def step_open(u, v, w, tcx, tcy, tzc1, tzc2, dt: float, steps: int, engines: int = 1):
+    """As step(), but the halo ring is never refreshed: after n steps only the
+    cells at distance >= n from the box edge are valid (light-cone check)."""
+    nx, ny, nz = u.shape[0] - 2, u.shape[1] - 2, u.shape[2]
+    scratch = np.zeros((3,) + u.shape)
+    tzc1 = np.ascontiguousarray(tzc1, dtype=np.float64)
+    tzc2 = np.ascontiguousarray(tzc2, dtype=np.float64)
+    for _ in range(steps):
+        rc = lib().oracle_step_open(_p(u), _p(v), _p(w), _p(scratch), nx, ny, nz, float(tcx),
+                                    float(tcy), _p(tzc1), _p(tzc2), float(dt), int(engines))
+        if rc:
+            raise ValueError("oracle_step_open: bad arguments")
+
+
+def lightcone_tile(gnx: int, gny: int, nz: int, seed: int, coeffs: dict, dt: float, steps: int,
+                   i0: int, j0: int, ti: int, tj: int, engines: int = 1):
+    """Interior rows i0..i0+ti-1, columns j0..j0+tj-1 (1-based, periodic) of
+    (u, v, w) after `steps` forward steps of the BASELINE fill, computed from
+    the (ti+2*steps) x (tj+2*steps) neighbourhood only."""
+    r = steps
+    fs = fill_box(gnx, gny, nz, seed, i0 - r, j0 - r, ti + 2 * r, tj + 2 * r, baseline=True)
+    for _ in range(steps):
+        step_open(*fs, coeffs["tcx"], coeffs["tcy"], coeffs["tzc1"], coeffs["tzc2"], dt, 1, engines)
+        # only the interior is valid now: it is the next step's padded box
+        fs = tuple(np.ascontiguousarray(f[1:-1, 1:-1]) for f in fs)
+    return fs
 
 
 # --------------------------------------------------------------------------

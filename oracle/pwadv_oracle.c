@@ -259,13 +259,53 @@ void oracle_baseline_coefficients(uint64_t seed, int64_t nz, double *tzc1, doubl
 }
 
 /*
+ * A box of the same fill (light-cone checks): box cell
+ * (a, b, k), a in [0, bnx), b in [0, bny), holds global padded cell
+ * (i0 + a, j0 + b, k) of a gnx x gny x nz fill. Global coordinates are taken
+ * periodically at any distance (the wrap of grid.py:203-208), so a box may
+ * straddle the domain edge or be larger than the domain. Each column jumps
+ * the LCG to its own offset, so the cost is that of the box, not the grid.
+ */
+void oracle_fill_box(double *u, double *v, double *w, int64_t gnx, int64_t gny, int64_t nz,
+                     uint64_t seed, int baseline, int64_t i0, int64_t j0,
+                     int64_t bnx, int64_t bny)
+{
+    double *f[3] = {u, v, w};
+    uint64_t cells = (uint64_t)gnx * (uint64_t)gny * (uint64_t)nz;
+    for (int n = 0; n < 3; ++n)
+        for (int64_t a = 0; a < bnx; ++a) {
+            int64_t gi = ((i0 + a - 1) % gnx + gnx) % gnx;      /* 0-based interior row */
+            for (int64_t b = 0; b < bny; ++b) {
+                int64_t gj = ((j0 + b - 1) % gny + gny) % gny;
+                uint64_t first = (uint64_t)n * cells +
+                                 ((uint64_t)gi * (uint64_t)gny + (uint64_t)gj) * (uint64_t)nz;
+                uint64_t ja, jc;
+                lcg_jump(first, &ja, &jc);
+                uint64_t s = ja * seed + jc;
+                double *col = f[n] + ((size_t)a * (size_t)bny + (size_t)b) * (size_t)nz;
+                for (int64_t k = 0; k < nz; ++k) {
+                    s = s * ORACLE_LCG_MULT + ORACLE_LCG_INC;
+                    double d = (double)(s >> 11) * 0x1.0p-53;
+                    if (baseline) {
+                        d = d * 20.0 - 10.0;
+                        if (n == 2 && (k == 0 || k == nz - 1)) d = 0.0;
+                    }
+                    col[k] = d;
+                }
+            }
+        }
+}
+
+/*
  * Composed time-step oracle (the reference has no time
  * integration): f <- f + dt*s on every interior cell (mul then
  * add), then wrap_halos. `scratch` holds 3 padded fields for su/sv/sw.
+ * With wrap == 0 the halo ring is left as it is (an open box whose valid
+ * region shrinks by one cell per side per step: the light-cone check).
  */
-int oracle_step(double *u, double *v, double *w, double *scratch,
-                int64_t nx, int64_t ny, int64_t nz, double tcx, double tcy,
-                const double *tzc1, const double *tzc2, double dt, int engines)
+static int step_impl(double *u, double *v, double *w, double *scratch,
+                     int64_t nx, int64_t ny, int64_t nz, double tcx, double tcy,
+                     const double *tzc1, const double *tzc2, double dt, int engines, int wrap)
 {
     size_t n = (size_t)(nx + 2) * (size_t)(ny + 2) * (size_t)nz;
     double *su = scratch, *sv = scratch + n, *sw = scratch + 2 * n;
@@ -280,7 +320,21 @@ int oracle_step(double *u, double *v, double *w, double *scratch,
                 for (int64_t k = 0; k < nz; ++k) {
                     f[m][IX(i, j, k)] = f[m][IX(i, j, k)] + dt * s[m][IX(i, j, k)];
                 }
-        oracle_wrap_halos(f[m], nx, ny, nz);
+        if (wrap) oracle_wrap_halos(f[m], nx, ny, nz);
     }
     return 0;
+}
+
+int oracle_step(double *u, double *v, double *w, double *scratch,
+                int64_t nx, int64_t ny, int64_t nz, double tcx, double tcy,
+                const double *tzc1, const double *tzc2, double dt, int engines)
+{
+    return step_impl(u, v, w, scratch, nx, ny, nz, tcx, tcy, tzc1, tzc2, dt, engines, 1);
+}
+
+int oracle_step_open(double *u, double *v, double *w, double *scratch,
+                     int64_t nx, int64_t ny, int64_t nz, double tcx, double tcy,
+                     const double *tzc1, const double *tzc2, double dt, int engines)
+{
+    return step_impl(u, v, w, scratch, nx, ny, nz, tcx, tcy, tzc1, tzc2, dt, engines, 0);
 }

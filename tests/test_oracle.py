@@ -84,3 +84,31 @@ def test_compare_semantics_signed_zero_and_ulp():
     assert not r["bitwise_equal"] and r["max_ulp_diff"] == 1
     b[0][1, 1, 1] = np.nextafter(0.0, 1.0)
     assert oracle.compare(a, b)["max_ulp_diff"] == 1
+
+
+def test_fill_box_is_the_periodic_padded_fill():
+    """oracle.fill_box (LCG skip-ahead per column) == cells of the full fill,
+    halo ring included, and periodic at any distance (boxes past the edge)."""
+    g = (9, 7, 6)
+    full = oracle.fill_random(*g, 42, baseline=True)
+    box = oracle.fill_box(*g, 42, 0, 0, g[0] + 2, g[1] + 2, baseline=True)
+    assert all(np.array_equal(a, b) for a, b in zip(full, box))
+    box = oracle.fill_box(*g, 42, -12, 5, 30, 25, baseline=True)
+    ii = (np.arange(-12, 18) - 1) % g[0] + 1
+    jj = (np.arange(5, 30) - 1) % g[1] + 1
+    assert all(np.array_equal(b, a[np.ix_(ii, jj)]) for a, b in zip(full, box))
+
+
+@pytest.mark.parametrize("steps,i0,j0,ti,tj", [(1, 1, 1, 9, 7), (3, 2, 6, 4, 3), (5, 8, 7, 3, 2)])
+def test_lightcone_tile_equals_periodic_stepping(steps, i0, j0, ti, tj):
+    """The light-cone check's CPU side: stepping only the n-cell neighbourhood
+    of a tile (open box, no wrap) reproduces the periodic full-grid steps."""
+    g = (9, 7, 6)
+    co = oracle.baseline_coefficients(42, g[2])
+    u, v, w = oracle.fill_random(*g, 42, baseline=True)
+    oracle.step(u, v, w, co["tcx"], co["tcy"], co["tzc1"], co["tzc2"], 0.1, steps)
+    tile = oracle.lightcone_tile(*g, 42, co, 0.1, steps, i0, j0, ti, tj)
+    ii = (np.arange(i0, i0 + ti) - 1) % g[0] + 1
+    jj = (np.arange(j0, j0 + tj) - 1) % g[1] + 1
+    for got, full in zip(tile, (u, v, w)):
+        assert np.array_equal(got.view(np.int64), full[np.ix_(ii, jj)].view(np.int64))
