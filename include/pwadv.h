@@ -55,6 +55,7 @@ enum {
 #define PWADV_FLAG_FMA 1u           /* contract into DFMA (not bit-exact; <=1e-12 normwise) */
 #define PWADV_FLAG_SIMPLE 2u        /* force the one-thread-per-point kernel */
 #define PWADV_FLAG_RIM 16u          /* only the one-cell rim of the box (one launch; multi-GPU overlap) */
+#define PWADV_FLAG_GENERIC 32u      /* X-march with a run-time tile layout even for nz = 64 / 128 */
 /* ablation switches for profiling only (results are NOT the PW sources):
  * skip the PW arithmetic / skip the output stores of the X-march kernel */
 #define PWADV_FLAG_DEBUG_NO_COMPUTE 0x100u

@@ -36,6 +36,7 @@ PWADV_E_ALIGN = -6
 FLAG_FMA = 1
 FLAG_SIMPLE = 2
 FLAG_RIM = 16
+FLAG_GENERIC = 32
 
 
 class Opts(ctypes.Structure):

@@ -263,10 +263,11 @@ __device__ __forceinline__ unsigned long long gtime()
 // Issue the bulk copies of plane q (3 fields, one contiguous run each) into
 // stage st, completing on full[st]. A table lookup and one multiply-add: the
 // warp that issues must not fall behind the others (it gates the next refill).
+template <bool TRACE = true>
 __device__ __forceinline__ void issue_plane(const RingState *rs, const BoxArgs &a, int q, int st,
                                             int CS, double *ring, uint64_t *full)
 {
-    if (a.trace && blockIdx.x == 0 && q < 4096) a.trace[2 * q] = gtime();
+    if (TRACE && a.trace && blockIdx.x == 0 && q < 4096) a.trace[2 * q] = gtime();
     int k = 0;
     while (rs->first[k + 1] <= q) ++k;
     const uint32_t bytes = rs->bytes[k];
@@ -292,13 +293,19 @@ __device__ __forceinline__ void issue_plane(const RingState *rs, const BoxArgs &
 // resident CTAs per SM for a thread budget (each CTA keeps <= 168 registers)
 __host__ __device__ constexpr int ctas_per_sm(int maxt) { return maxt <= 128 ? 3 : (maxt <= 192 ? 2 : 1); }
 
-template <bool FMA, bool STEP, int MAXT, bool FIX>
+// NZC > 0 (warp-specialised kernel only): nz, TJ and the tile layout are
+// compile-time constants, so every staged operand is one LDS at an immediate
+// offset from a per-plane base register (the BASELINE nz = 64 / 128 cases).
+template <bool FMA, bool STEP, int MAXT, bool FIX, int NZC = 0>
 __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     k_advect_xmarch(const __grid_constant__ BoxArgs a, const __grid_constant__ TileCfg t)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int S = t.stages, TJ = t.tj, KP = t.kp;
-    const int nz = (int)a.nz;
+    static_assert(NZC == 0 || (MAXT == 512 && 384 % (NZC / 2) == 0), "compile-time layout: WS only");
+    const int S = t.stages;
+    const int TJ = NZC ? 384 / (NZC / 2) : t.tj;
+    const int KP = NZC ? NZC / 2 : t.kp;
+    const int nz = NZC ? NZC : (int)a.nz;
     const int CS = (TJ + 2) * nz;  // doubles per field per tile-plane
     double *ring = reinterpret_cast<double *>(smem_raw);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)S * 3 * CS * sizeof(double));
@@ -352,7 +359,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
         }
         fence_mbar_init();
         const int n0 = q < S ? q : S;
-        for (int n = 0; n < n0; ++n) issue_plane(rs, a, n, n, CS, ring, full);
+        for (int n = 0; n < n0; ++n) issue_plane<NZC == 0>(rs, a, n, n, CS, ring, full);
     }
     __syncthreads();
     const int total = rs->total;
@@ -365,7 +372,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
                     const int st = q % S;
                     mbar_wait(&empty[st], (uint32_t)(((q / S) - 1) & 1));
                     fence_proxy_async();
-                    issue_plane(rs, a, q, st, CS, ring, full);
+                    issue_plane<NZC == 0>(rs, a, q, st, CS, ring, full);
                 }
             }
             return;
@@ -392,14 +399,17 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
                 rs->released[st] = 0;
                 if (seq + S < total) {
                     fence_proxy_async();
-                    issue_plane(rs, a, seq + S, st, CS, ring, full);
+                    issue_plane<NZC == 0>(rs, a, seq + S, st, CS, ring, full);
                 }
             }
         }
     };
     auto wait_next = [&]() -> const double * {
         mbar_wait(&full[cst], cph);
-        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && cseq < 4096) a.trace[2 * cseq + 1] = gtime();
+        if constexpr (NZC == 0) {  // plane-arrival stamps (tools/trace.py): generic kernel only
+            if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && cseq < 4096)
+                a.trace[2 * cseq + 1] = gtime();
+        }
         return ring + (size_t)cst * 3 * CS;
     };
     auto advance = [&]() {
@@ -610,8 +620,24 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         t.nstrips = plan.nstrips;
         void (*kern)(BoxArgs, TileCfg) = nullptr;
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
+        // compile-time layout for the BASELINE depths at the default tile
+        const int nzc = (plan.maxt == 512 && plan.tj * plan.kp == 384 &&
+                         (L.nz == 64 || L.nz == 128) && !(L.flags & PWADV_FLAG_GENERIC))
+                            ? (int)L.nz : 0;
+#define PWADV_PICK_NZ(NZ, FX)                                                    \
+    if (nzc == NZ) {                                                             \
+        if (L.step)                                                              \
+            kern = fma ? k_advect_xmarch<true, true, 512, FX, NZ>                \
+                       : k_advect_xmarch<false, true, 512, FX, NZ>;              \
+        else                                                                     \
+            kern = fma ? k_advect_xmarch<true, false, 512, FX, NZ>               \
+                       : k_advect_xmarch<false, false, 512, FX, NZ>;             \
+    }
+        PWADV_PICK_NZ(64, false)
+        PWADV_PICK_NZ(128, true)
+#undef PWADV_PICK_NZ
 #define PWADV_PICK(MT, FX)                                                       \
-    if (plan.maxt == MT && fix == FX) {                                          \
+    if (!kern && plan.maxt == MT && fix == FX) {                                 \
         if (L.step)                                                              \
             kern = fma ? k_advect_xmarch<true, true, MT, FX>                     \
                        : k_advect_xmarch<false, true, MT, FX>;                   \

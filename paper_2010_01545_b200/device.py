@@ -89,7 +89,9 @@ def _as_device_coeffs(coeffs, device) -> DeviceCoefficients:
 def make_opts(variant: str = "xmarch", *, tile_j: int = 0, stages: int = 0, grid: int = 0,
               max_threads: int = 0, chunks: int = 0) -> _lib.Opts:
     """Kernel selection: "xmarch" (bulk-copy plane ring, default), "simple"
-    (one thread per point); suffix "_fma" for the DFMA (not bit-exact) build."""
+    (one thread per point), "xmarch_generic" (the X-march with a run-time
+    tile layout even where a compile-time one exists); suffix "_fma" for the
+    DFMA (not bit-exact) build."""
     flags = 0
     base = variant
     if variant.endswith("_fma"):
@@ -97,6 +99,8 @@ def make_opts(variant: str = "xmarch", *, tile_j: int = 0, stages: int = 0, grid
         base = variant[:-4]
     if base == "simple":
         flags |= _lib.FLAG_SIMPLE
+    elif base == "xmarch_generic":
+        flags |= _lib.FLAG_GENERIC
     elif base != "xmarch":
         raise ValueError(f"unknown kernel variant {variant!r}")
     return _lib.Opts(flags, tile_j, stages, grid, max_threads, chunks, None)

@@ -21,7 +21,7 @@ def run(cfg, **kw):
     co = device.DeviceCoefficients.from_host(pw.baseline_coefficients(42, nz), fields[0].device)
     out = device.alloc_fields(dims, fields[0].device)
     dbg = kw.pop("debug", 0)
-    opts = device.make_opts("xmarch", **kw)
+    opts = device.make_opts("xmarch_generic", **kw)  # stamps exist in the generic kernel only
     opts.flags |= dbg << 8
     for _ in range(3):
         device.advect(*fields, co, out, opts=opts)
