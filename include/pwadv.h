@@ -57,7 +57,8 @@ enum {
 #define PWADV_FLAG_RIM 16u          /* only the one-cell rim of the box (one launch; multi-GPU overlap) */
 #define PWADV_FLAG_GENERIC 32u      /* X-march with a run-time tile layout even for nz = 64 / 128 */
 /* ablation switches for profiling only (results are NOT the PW sources):
- * skip the PW arithmetic / skip the output stores of the X-march kernel */
+ * skip the PW arithmetic / skip the output stores of the X-march kernel
+ * (they select the run-time-layout X-march, as PWADV_FLAG_GENERIC) */
 #define PWADV_FLAG_DEBUG_NO_COMPUTE 0x100u
 #define PWADV_FLAG_DEBUG_NO_STORE 0x400u
 

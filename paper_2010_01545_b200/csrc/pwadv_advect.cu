@@ -212,6 +212,9 @@ __global__ void __launch_bounds__(256) k_advect_simple(BoxArgs a)
 // warp boundary inside a column, FIX only) straight from the shared plane.
 // When columns straddle warps (FIX, e.g. nz = 128) the neighbour is read from
 // the staged plane instead (measured faster there than shuffles + fix-ups).
+#ifndef PWADV_PRODUCER_SLEEP_NS
+#define PWADV_PRODUCER_SLEEP_NS 0
+#endif
 #ifndef PWADV_NBR_SMEM
 #define PWADV_NBR_SMEM 0
 #endif
@@ -370,7 +373,11 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
             if (tid == 32 * kComputeWarps) {
                 for (int q = (total < S ? total : S); q < total; ++q) {
                     const int st = q % S;
+#if PWADV_PRODUCER_SLEEP_NS > 0
+                    mbar_wait_sleep(&empty[st], (uint32_t)(((q / S) - 1) & 1), PWADV_PRODUCER_SLEEP_NS);
+#else
                     mbar_wait(&empty[st], (uint32_t)(((q / S) - 1) & 1));
+#endif
                     fence_proxy_async();
                     issue_plane<NZC == 0>(rs, a, q, st, CS, ring, full);
                 }
@@ -426,8 +433,14 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
         return pl + f * CS + (c + 1 + dy) * nz;
     };
 
-    double2 U0[3], V0[3], W0[3], U1[3], VM[3];
-    double U0M[3], W0M[3];
+    double2 U0[3], V0[3], W0[3], VM[3];
+    double W0M[3];
+    // x-direction operand sums carried from plane i-1 to plane i (the x+1 sum
+    // of one step is the x-1 sum of the next; IEEE addition is commutative):
+    // su  u(i-1)+u(i)                       (kernel.py:73-84, x-term)
+    // sv  u(i-1,j)+u(i-1,j+1)               (kernel.py:87-98, x-term)
+    // sw  u(i-1,k-1)+u(i-1,k)               (kernel.py:101-112, x-term)
+    double sxu_a, sxu_b, txu_a, txu_b, rxu_a, rxu_b;
 
     for (int k = 0; k < my_units; ++k) {
         const Unit wu = unit_at(a, t, (int64_t)blockIdx.x + (int64_t)k * G);
@@ -440,12 +453,16 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
         {
             const double *pl = wait_next();
             U0[2] = P(pl, 0, 0);
-            U1[2] = P(pl, 0, 1);
+            const double2 u1 = P(pl, 0, 1);
             V0[2] = P(pl, 1, 0);
             W0[2] = P(pl, 2, 0);
-            U0M[2] = nbr_m<FIX>(U0[2], colp(pl, 0, 0), k0, fixM);
+            const double u0M = nbr_m<FIX>(U0[2], colp(pl, 0, 0), k0, fixM);
             release(cseq, cst);
             advance();
+            txu_a = __dadd_rn(U0[2].x, u1.x);
+            txu_b = __dadd_rn(U0[2].y, u1.y);
+            rxu_a = __dadd_rn(u0M, U0[2].x);
+            rxu_b = __dadd_rn(U0[2].x, U0[2].y);
         }
         // plane ib -> slot 0 (items read from the leading plane)
         int pst = cst;  // stage of the current x plane, released one step later
@@ -457,6 +474,8 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
             VM[0] = P(pl, 1, -1);
             W0M[0] = nbr_m<FIX>(W0[0], colp(pl, 2, 0), k0, fixM);
             advance();
+            sxu_a = __dadd_rn(U0[0].x, U0[2].x);
+            sxu_b = __dadd_rn(U0[0].y, U0[2].y);
         }
 
         double *o0 = a.o0 + (ib * ny2 + (j0 + c)) * (int64_t)nz + k0;
@@ -476,10 +495,10 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
             W0[rp] = P(L, 2, 0);
             VM[rp] = P(L, 1, -1);
             W0M[rp] = nbr_m<FIX>(W0[rp], colp(L, 2, 0), k0, fixM);
-            U1[r] = P(C, 0, 1);
+            const double2 u1c = P(C, 0, 1);
             const double2 umc = P(C, 0, -1), v1c = P(C, 1, 1), w1c = P(C, 2, 1), wmc = P(C, 2, -1);
             const double w1cM = nbr_m<FIX>(w1c, colp(C, 2, 1), k0, fixM);
-            U0M[r] = nbr_m<FIX>(U0[r], colp(C, 0, 0), k0, fixM);
+            const double u0cM = nbr_m<FIX>(U0[r], colp(C, 0, 0), k0, fixM);
             const double u0cQ = nbr_q<FIX>(U0[r], colp(C, 0, 0), k0, fixQ, nz);
             const double v0cM = nbr_m<FIX>(V0[r], colp(C, 1, 0), k0, fixM);
             const double v0cQ = nbr_q<FIX>(V0[r], colp(C, 1, 0), k0, fixQ, nz);
@@ -490,37 +509,53 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
             const double2 u0m = U0[rm], u0c = U0[r], u0p = U0[rp];
             const double2 v0m = V0[rm], v0c = V0[r], v0p = V0[rp];
             const double2 w0m = W0[rm], w0c = W0[r], w0p = W0[rp];
-            const double2 u1m = U1[rm], u1c = U1[r], vmc = VM[r], vmp = VM[rp];
-            const double u0mM = U0M[rm], u0cM = U0M[r], w0cM = W0M[r], w0pM = W0M[rp];
+            const double2 vmc = VM[r], vmp = VM[rp];
+            const double w0cM = W0M[r], w0pM = W0M[rp];
+
+            // sums shared with the next plane (x-carry) or within the k-pair
+            const double nsxu_a = __dadd_rn(u0c.x, u0p.x), nsxu_b = __dadd_rn(u0c.y, u0p.y);
+            const double ntxu_a = __dadd_rn(u0c.x, u1c.x), ntxu_b = __dadd_rn(u0c.y, u1c.y);
+            const double nrxu_a = __dadd_rn(u0cM, u0c.x), nrxu_b = __dadd_rn(u0c.x, u0c.y);
+            const double szu = __dadd_rn(w0c.x, w0p.x);  // su: B(k0) = A(k1)
+            const double szv = __dadd_rn(w0c.x, w1c.x);  // sv: B(k0) = A(k1)
+            const double szw = __dadd_rn(w0c.x, w0c.y);  // sw: B(k0) = A(k1) (commuted)
 
             double su_a, sv_a, sw_a, su_b, sv_b, sw_b;
-            if (t.debug & 1) {  // ablation: touch every staged operand, no PW arithmetic
+            if (NZC == 0 && (t.debug & 1)) {  // ablation (generic kernel): no PW arithmetic
                 su_a = sv_a = sw_a = su_b = sv_b = sw_b =
                     (u0c.x + u0p.x) + (umc.x + u1c.x) + (v1c.x + w1c.x) + (wmc.x + vmp.x) +
-                    (v0m.x + w0m.y) + (u1m.y + vmc.y) + (w0cM + w0pM) + (u0cQ + v0cQ) +
-                    (w0cQ + vmcM) + (v0cM + w1cM) + (u0mM + u0cM) + (v0p.y + w0p.x);
+                    (v0m.x + w0m.y) + (vmc.y + v0p.y) + (w0cM + w0pM) + (u0cQ + v0cQ) +
+                    (w0cQ + vmcM) + (v0cM + w1cM) + (u0cM + w0p.x);
             } else {
-    // level k0 (never the top; level 0 is identically zero)
-                su_a = su_formula<FMA>(tcx, tcy, c1a, c2a, u0c.x, u0m.x, u0p.x, umc.x, u1c.x,
-                                              u0cM, u0c.y, vmc.x, vmp.x, v0c.x, v0p.x, w0cM, w0pM,
-                                              w0c.x, w0p.x, false);
-                sv_a = sv_formula<FMA>(tcx, tcy, c1a, c2a, v0c.x, v0m.x, v0p.x, vmc.x, v1c.x,
-                                              v0cM, v0c.y, u0m.x, u1m.x, u0c.x, u1c.x, w0cM, w1cM,
-                                              w0c.x, w1c.x, false);
-                sw_a = sw_formula<FMA>(tcx, tcy, c1a, c2a, w0c.x, w0m.x, w0p.x, wmc.x, w1c.x,
-                                              w0cM, w0c.y, u0mM, u0m.x, u0cM, u0c.x, vmcM, vmc.x,
-                                              v0cM, v0c.x, false);
+                // level k0 (never the top; level 0 is identically zero).
+                // pw_sums(x1, x2+x3, x4, x5+x6, y1, .., z1, z2+z3, z4, z5+z6)
+                // with the operand wiring of kernel.py:117-128
+                su_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, u0m.x, sxu_a, u0p.x, nsxu_a,
+                                    umc.x, __dadd_rn(vmc.x, vmp.x), u1c.x, __dadd_rn(v0c.x, v0p.x),
+                                    u0cM, __dadd_rn(w0cM, w0pM), u0c.y, szu, false);
+                sv_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, v0m.x, txu_a, v0p.x, ntxu_a,
+                                    vmc.x, __dadd_rn(v0c.x, vmc.x), v1c.x, __dadd_rn(v0c.x, v1c.x),
+                                    v0cM, __dadd_rn(w0cM, w1cM), v0c.y, szv, false);
+                sw_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, w0m.x, rxu_a, w0p.x, nrxu_a,
+                                    wmc.x, __dadd_rn(vmcM, vmc.x), w1c.x, __dadd_rn(v0cM, v0c.x),
+                                    w0cM, __dadd_rn(w0c.x, w0cM), w0c.y, szw, false);
                 // level k1 (the top when k1 == nz-1)
-                su_b = su_formula<FMA>(tcx, tcy, c1b, c2b, u0c.y, u0m.y, u0p.y, umc.y, u1c.y,
-                                              u0c.x, u0cQ, vmc.y, vmp.y, v0c.y, v0p.y, w0c.x, w0p.x,
-                                              w0c.y, w0p.y, top_b);
-                sv_b = sv_formula<FMA>(tcx, tcy, c1b, c2b, v0c.y, v0m.y, v0p.y, vmc.y, v1c.y,
-                                              v0c.x, v0cQ, u0m.y, u1m.y, u0c.y, u1c.y, w0c.x, w1c.x,
-                                              w0c.y, w1c.y, top_b);
-                sw_b = sw_formula<FMA>(tcx, tcy, c1b, c2b, w0c.y, w0m.y, w0p.y, wmc.y, w1c.y,
-                                              w0c.x, w0cQ, u0m.x, u0m.y, u0c.x, u0c.y, vmc.x, vmc.y,
-                                              v0c.x, v0c.y, top_b);
+                su_b = pw_sums<FMA>(tcx, tcy, c1b, c2b, u0m.y, sxu_b, u0p.y, nsxu_b,
+                                    umc.y, __dadd_rn(vmc.y, vmp.y), u1c.y, __dadd_rn(v0c.y, v0p.y),
+                                    u0c.x, szu, u0cQ, __dadd_rn(w0c.y, w0p.y), top_b);
+                sv_b = pw_sums<FMA>(tcx, tcy, c1b, c2b, v0m.y, txu_b, v0p.y, ntxu_b,
+                                    vmc.y, __dadd_rn(v0c.y, vmc.y), v1c.y, __dadd_rn(v0c.y, v1c.y),
+                                    v0c.x, szv, v0cQ, __dadd_rn(w0c.y, w1c.y), top_b);
+                sw_b = pw_sums<FMA>(tcx, tcy, c1b, c2b, w0m.y, rxu_b, w0p.y, nrxu_b,
+                                    wmc.y, __dadd_rn(vmc.x, vmc.y), w1c.y, __dadd_rn(v0c.x, v0c.y),
+                                    w0c.x, szw, w0cQ, __dadd_rn(w0c.y, w0cQ), top_b);
             }
+            sxu_a = nsxu_a;
+            sxu_b = nsxu_b;
+            txu_a = ntxu_a;
+            txu_b = ntxu_b;
+            rxu_a = nrxu_a;
+            rxu_b = nrxu_b;
             if (lvl0) {
                 su_a = 0.0;
                 sv_a = 0.0;
@@ -534,7 +569,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
                 sw_a = fwd_update(w0c.x, dt, sw_a);
                 sw_b = fwd_update(w0c.y, dt, sw_b);
             }
-            if (active && !(t.debug & 4)) {
+            if (active && !(NZC == 0 && (t.debug & 4))) {
                 store2(o0, su_a, su_b);
                 store2(o1, sv_a, sv_b);
                 store2(o2, sw_a, sw_b);
@@ -622,7 +657,9 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
         // compile-time layout for the BASELINE depths at the default tile
         const int nzc = (plan.maxt == 512 && plan.tj * plan.kp == 384 &&
-                         (L.nz == 64 || L.nz == 128) && !(L.flags & PWADV_FLAG_GENERIC))
+                         (L.nz == 64 || L.nz == 128) &&
+                         !(L.flags & (PWADV_FLAG_GENERIC | PWADV_FLAG_DEBUG_NO_COMPUTE |
+                                      PWADV_FLAG_DEBUG_NO_STORE)))
                             ? (int)L.nz : 0;
 #define PWADV_PICK_NZ(NZ, FX)                                                    \
     if (nzc == NZ) {                                                             \

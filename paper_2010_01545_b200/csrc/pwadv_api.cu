@@ -740,7 +740,7 @@ int pwadv_ctx_advect_host(pwadv_ctx *c, const double *u, const double *v, const 
     if (!u || !v || !w || !su || !sv || !sw || !tzc1 || !tzc2)
         return set_error(PWADV_E_NULL, "null pointer argument");
     DeviceGuard g(c->device);
-    const int64_t nx = c->nx, ny = c->ny, nz = c->nz;
+    const int64_t nx = c->nx, nz = c->nz;
     if (chunks < 1) chunks = 1;
     if (chunks > nx) chunks = (int32_t)nx;
     const double *hin[3] = {u, v, w};

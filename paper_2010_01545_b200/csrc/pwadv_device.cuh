@@ -16,6 +16,34 @@ namespace pwadv {
 //     + ((c1*z1)*(z2+z3) - (c2*z4)*(z5+z6))          [mid level]
 //     + ((c1*z1)*(z2+z3))                              [top level, k = nz-1]
 // su/sv/sw are this expression with the operand wiring of kernel.py:117-128.
+// The same expression from precomputed operand sums sx1 = x2+x3, sx2 = x5+x6,
+// sy1, sy2, sz1, sz2 (a sum may be shared between neighbouring points: IEEE
+// addition is commutative, so x+y computed once serves as both x+y and y+x).
+template <bool FMA>
+__device__ __forceinline__ double pw_sums(double tcx, double tcy, double c1, double c2,
+                                          double x1, double sx1, double x4, double sx2,
+                                          double y1, double sy1, double y4, double sy2,
+                                          double z1, double sz1, double z4, double sz2, bool top)
+{
+    if constexpr (!FMA) {
+        double X = __dmul_rn(tcx, __dsub_rn(__dmul_rn(x1, sx1), __dmul_rn(x4, sx2)));
+        double Y = __dmul_rn(tcy, __dsub_rn(__dmul_rn(y1, sy1), __dmul_rn(y4, sy2)));
+        double s = __dadd_rn(X, Y);
+        double A = __dmul_rn(__dmul_rn(c1, z1), sz1);
+        if (top) return __dadd_rn(s, A);
+        double B = __dmul_rn(__dmul_rn(c2, z4), sz2);
+        return __dadd_rn(s, __dsub_rn(A, B));
+    } else {
+        double xd = __fma_rn(x1, sx1, -__dmul_rn(x4, sx2));
+        double yd = __fma_rn(y1, sy1, -__dmul_rn(y4, sy2));
+        double s = __fma_rn(tcx, xd, __dmul_rn(tcy, yd));
+        double c1z = __dmul_rn(c1, z1);
+        if (top) return __dadd_rn(s, __dmul_rn(c1z, sz1));
+        double B = __dmul_rn(__dmul_rn(c2, z4), sz2);
+        return __dadd_rn(s, __fma_rn(c1z, sz1, -B));
+    }
+}
+
 template <bool FMA>
 __device__ __forceinline__ double pw_expr(double tcx, double tcy, double c1, double c2,
                                           double x1, double x2, double x3, double x4,
@@ -24,24 +52,9 @@ __device__ __forceinline__ double pw_expr(double tcx, double tcy, double c1, dou
                                           double z1, double z2, double z3, double z4,
                                           double z5, double z6, bool top)
 {
-    if constexpr (!FMA) {
-        double X = __dmul_rn(tcx, __dsub_rn(__dmul_rn(x1, __dadd_rn(x2, x3)),
-                                            __dmul_rn(x4, __dadd_rn(x5, x6))));
-        double Y = __dmul_rn(tcy, __dsub_rn(__dmul_rn(y1, __dadd_rn(y2, y3)),
-                                            __dmul_rn(y4, __dadd_rn(y5, y6))));
-        double s = __dadd_rn(X, Y);
-        double A = __dmul_rn(__dmul_rn(c1, z1), __dadd_rn(z2, z3));
-        double B = __dmul_rn(__dmul_rn(c2, z4), __dadd_rn(z5, z6));
-        return top ? __dadd_rn(s, A) : __dadd_rn(s, __dsub_rn(A, B));
-    } else {
-        double xd = __fma_rn(x1, __dadd_rn(x2, x3), -__dmul_rn(x4, __dadd_rn(x5, x6)));
-        double yd = __fma_rn(y1, __dadd_rn(y2, y3), -__dmul_rn(y4, __dadd_rn(y5, y6)));
-        double s = __fma_rn(tcx, xd, __dmul_rn(tcy, yd));
-        double c1z = __dmul_rn(c1, z1);
-        double B = __dmul_rn(__dmul_rn(c2, z4), __dadd_rn(z5, z6));
-        double zd = top ? __dmul_rn(c1z, __dadd_rn(z2, z3)) : __fma_rn(c1z, __dadd_rn(z2, z3), -B);
-        return __dadd_rn(s, zd);
-    }
+    return pw_sums<FMA>(tcx, tcy, c1, c2, x1, __dadd_rn(x2, x3), x4, __dadd_rn(x5, x6),
+                        y1, __dadd_rn(y2, y3), y4, __dadd_rn(y5, y6),
+                        z1, __dadd_rn(z2, z3), z4, __dadd_rn(z5, z6), top);
 }
 
 // su_formula (kernel.py:73-84): argument order as the reference.
@@ -145,6 +158,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
         "@!P1 bra.uni WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
+        : "memory");
+}
+
+// As mbar_wait, with a suspend-time hint: the waiting thread may sleep up to
+// `ns` nanoseconds per try instead of re-polling (the producer's wait).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra.uni WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(ns)
         : "memory");
 }
 
