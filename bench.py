@@ -162,6 +162,29 @@ def ncu_traffic(key: str):
     return None
 
 
+def pcie_concurrent(hin, hout, dev):
+    """GB/s each way with H2D and D2H running at once (the e2e path's bound),
+    measured on the same pinned buffers right before the e2e run."""
+    import torch
+    d_in = [torch.empty_like(h, device=dev) for h in hin]
+    d_out = [torch.empty_like(h, device=dev) for h in hout]
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    nbytes = sum(h.numel() * 8 for h in hin)
+    best = 0.0
+    for _ in range(3):
+        torch.cuda.synchronize(dev)
+        t = time.perf_counter()
+        with torch.cuda.stream(s1):
+            for d, h in zip(d_in, hin):
+                d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            for h, d in zip(hout, d_out):
+                h.copy_(d, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        best = max(best, nbytes / (time.perf_counter() - t) / 1e9)
+    return best
+
+
 def cpu_baseline_arm(nx, ny, nz, reps=3, max_seconds=20.0):
     """The oracle port (C restatement, oracle/) on all host threads, min of reps."""
     from oracle import oracle  # checker / CPU baseline only
@@ -356,6 +379,7 @@ def run_ours(args):
         for h, f in zip(hin, fields):
             h.copy_(f)
         tz = [co.tz[0].cpu().numpy(), co.tz[1].cpu().numpy()]
+        pcie_gbs = pcie_concurrent(hin, hout, dev)
         ke = max(3, min(args.steps, args.e2e_steps))
         for _ in range(2):
             ctx.advect_host(*hin, *hout, co.tcx, co.tcy, *tz, chunks=args.chunks)
@@ -378,10 +402,14 @@ def run_ours(args):
         ctx.close()
         same = all(torch.equal(a.view(torch.int64), b.cpu().view(torch.int64)) for a, b in zip(hout, out))
         e2e = {"value": dims.cells * ke / (t1 - t0) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "steps": ke, "chunks": args.chunks,
+               "d2h_bytes_per_step": d2h, "steps": ke, "chunks": args.chunks or "auto",
                "api": "pwadv_ctx_submit_host + pwadv_ctx_sync (C ABI; pinned host buffers; "
                       "H2D/K1/D2H pipelined across chunks and grids)",
                "value_sync_call": sync_rate,
+               # PCIe bound of this path on this box: every point moves 24 B each way
+               "pcie_concurrent_GBs_each_way": round(pcie_gbs, 1),
+               "pcie_bound": round(pcie_gbs * 1e9 / (h2d / dims.cells) / 1e9, 3),
+               "frac_of_pcie_bound": round(dims.cells * ke / (t1 - t0) / (pcie_gbs * 1e9 / (h2d / dims.cells)), 3),
                "bitwise_equal_to_device_run": bool(same)}
 
     cpu = None
@@ -458,8 +486,9 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--variant", default="xmarch",
                     choices=("xmarch", "simple", "xmarch_fma", "simple_fma"))
-    ap.add_argument("--chunks", type=int, default=16, help="X-slab chunks of the e2e pipeline")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--chunks", type=int, default=0,
+                    help="X-slab chunks of the e2e pipeline (0 = the library's automatic choice)")
+    ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--full-c4", action="store_true", help="c4 on one GPU at the full 4096x4096x128")

@@ -218,6 +218,8 @@ int pwadv_wrap_axis3_f64(double *u, double *v, double *w, int64_t nx, int64_t ny
  * chunk c+1, the K1 launch on chunk c and the D2H copy of chunk c-1 overlap
  * (the paper's proposed future work). Synchronous: returns after
  * the outputs are in host memory. Output halos and level 0 are +0.0.
+ * chunks <= 0 picks the count automatically (1 for fields under 32 MiB, else 16;
+ * for pwadv_ctx_submit_host about 64 MiB per field and chunk, at most 16).
  */
 typedef struct pwadv_ctx pwadv_ctx;
 int pwadv_ctx_create(pwadv_ctx **out, int device, int64_t nx, int64_t ny, int64_t nz);

@@ -399,6 +399,23 @@ int pwadv_unpack_xface3_f64(double *u, double *v, double *w, const double *buf, 
 }
 
 // ---------------------------------------------------------------------------
+// Automatic X-slab chunk count for the host-buffer path (measured on B200,
+// tools/e2e_sweep.py, tools/pcie.py): a single synchronous call needs ~16
+// chunks for its H2D / K1 / D2H pipeline to fill; a stream of submissions
+// already overlaps one grid's H2D with the previous grid's D2H, so there the
+// copies only need to stay large (~64 MiB per field and chunk).
+static int32_t auto_chunks(int64_t nx, int64_t plane_doubles, bool streamed)
+{
+    const double field_bytes = (double)(nx + 2) * (double)plane_doubles * sizeof(double);
+    int64_t n;
+    if (streamed) n = (int64_t)(field_bytes / (64.0 * 1024 * 1024) + 0.5);
+    else n = field_bytes < 32.0 * 1024 * 1024 ? 1 : 16;
+    if (n < 1) n = 1;
+    if (n > 16) n = 16;
+    if (n > nx) n = nx;
+    return (int32_t)n;
+}
+
 // host-buffer context: pipelined H2D / K1 / D2H over X-slab chunks
 
 namespace pwadv {
@@ -741,7 +758,7 @@ int pwadv_ctx_advect_host(pwadv_ctx *c, const double *u, const double *v, const 
         return set_error(PWADV_E_NULL, "null pointer argument");
     DeviceGuard g(c->device);
     const int64_t nx = c->nx, nz = c->nz;
-    if (chunks < 1) chunks = 1;
+    if (chunks < 1) chunks = auto_chunks(nx, (c->ny + 2) * nz, false);
     if (chunks > nx) chunks = (int32_t)nx;
     const double *hin[3] = {u, v, w};
     double *hout[3] = {su, sv, sw};
@@ -803,7 +820,7 @@ int pwadv_ctx_submit_host(pwadv_ctx *c, const double *u, const double *v, const 
         if (e == cudaSuccess) e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return set_cuda_error("second buffer set", e);
     }
-    if (chunks < 1) chunks = 1;
+    if (chunks < 1) chunks = auto_chunks(nx, (c->ny + 2) * nz, true);
     if (chunks > nx) chunks = (int32_t)nx;
     const int set = (int)(c->submits & 1);
     ++c->submits;

@@ -240,7 +240,8 @@ class HostContext:
 
     def advect_host(self, u, v, w, su, sv, sw, tcx, tcy, tzc1, tzc2, chunks: int = 0,
                     opts: _lib.Opts | None = None) -> tuple[int, int]:
-        """Host in, host out: pipelined H2D / K1 / D2H. Returns (h2d, d2h) bytes."""
+        """Host in, host out: pipelined H2D / K1 / D2H. Returns (h2d, d2h) bytes.
+        chunks <= 0: automatic (1 below 32 MiB per field, else 16)."""
         d = self.dims
         for a in (u, v, w, su, sv, sw):
             if tuple(a.shape) != d.padded_shape:
@@ -249,9 +250,6 @@ class HostContext:
         tz2 = np.ascontiguousarray(tzc2, dtype=np.float64)
         if tz1.shape != (d.nz,) or tz2.shape != (d.nz,):
             raise ValueError(f"coefficient length {tz1.shape} != nz {d.nz}")
-        if chunks <= 0:
-            # pipeline only when transfers are large enough to overlap
-            chunks = 1 if d.padded_len * 8 < (32 << 20) else min(16, d.nx)
         _lib.check(_lib.lib().pwadv_ctx_advect_host(
             self._h, self._hp(u), self._hp(v), self._hp(w), self._hp(su), self._hp(sv),
             self._hp(sw), float(tcx), float(tcy), ctypes.c_void_p(tz1.ctypes.data),
@@ -260,10 +258,11 @@ class HostContext:
         _lib.check(_lib.lib().pwadv_ctx_last_bytes(self._h, ctypes.byref(a), ctypes.byref(b)))
         return int(a.value), int(b.value)
 
-    def submit_host(self, u, v, w, su, sv, sw, tcx, tcy, tzc1, tzc2, chunks: int = 16,
+    def submit_host(self, u, v, w, su, sv, sw, tcx, tcy, tzc1, tzc2, chunks: int = 0,
                     opts: _lib.Opts | None = None) -> tuple[int, int]:
         """Asynchronous advect_host for page-locked buffers (consecutive submissions
-        pipeline H2D / K1 / D2H across grids); call sync() before reading outputs."""
+        pipeline H2D / K1 / D2H across grids); call sync() before reading outputs.
+        chunks <= 0: automatic (about 64 MiB per field and chunk)."""
         d = self.dims
         tz1 = np.ascontiguousarray(tzc1, dtype=np.float64)
         tz2 = np.ascontiguousarray(tzc2, dtype=np.float64)
