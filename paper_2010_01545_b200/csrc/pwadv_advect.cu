@@ -645,6 +645,16 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
 
     XmarchPlan plan;
     const bool tiled = plan_xmarch(L, *dev, &plan);
+    if (tiled && plan.rounds > kMaxUnitsPerCta) {
+        // more strips than one launch's unit tables hold (very long y): split
+        // the box along y at a strip boundary and launch the halves in order
+        const int64_t half = (nby / 2 + plan.tj - 1) / plan.tj * plan.tj;
+        BoxLaunch lo = L, hi = L;
+        lo.y1 = L.y0 + half;
+        hi.y0 = L.y0 + half;
+        const int rc = launch_box(lo, stream);
+        return rc != PWADV_OK ? rc : launch_box(hi, stream);
+    }
     if (tiled) {
         TileCfg t;
         t.tj = plan.tj;
@@ -795,6 +805,7 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     int64_t grid = units < g0 ? units : g0;
     if (grid < 1) grid = 1;
     p->grid = (int)grid;
+    p->rounds = (units + grid - 1) / grid;
     return true;
 }
 

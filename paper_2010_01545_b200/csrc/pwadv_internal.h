@@ -34,6 +34,7 @@ struct XmarchPlan {
     int maxt, tj, kp, stages, threads, grid, nchunks;
     size_t smem;
     int64_t nstrips;
+    int64_t rounds;  // units per CTA (the kernel's unit table holds kMaxUnitsPerCta)
 };
 
 // cached attributes of the current device (lazily filled, thread-safe)

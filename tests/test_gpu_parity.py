@@ -420,6 +420,31 @@ def test_tall_and_odd_columns_bitwise(shape):
     assert plan["kernel"] == ("xmarch" if nz in (300, 512) else "simple")
 
 
+@pytest.mark.parametrize("shape", [(3, 120000, 64), (2, 60010, 128)])
+def test_long_y_domain_splits_the_launch(shape):
+    """More strips than one launch's per-CTA unit tables hold: the box is split
+    along y into several X-march launches; advection and the fused step stay
+    bit-exact against the oracle."""
+    u, v, w = oracle.fill_random(*shape, 23, baseline=True)
+    co = oracle.baseline_coefficients(23, shape[2])
+    args = (co["tcx"], co["tcy"], co["tzc1"], co["tzc2"])
+    dims = pw.make_grid(*shape)
+    du, dv, dw = to_dev(u, v, w)
+    dco = pw.AdvectionCoefficients(*args)
+    _lib.reset_launch_count()
+    out = device.advect(du, dv, dw, dco)
+    torch.cuda.synchronize()
+    assert _lib.launch_count() > 1  # split
+    want = oracle.advect(u, v, w, *args, engines=oracle.host_threads())
+    assert_bitwise([t.cpu().numpy() for t in out], want, shape)
+    nxt = device.alloc_fields(dims, "cuda")
+    device.step(du, dv, dw, dco, 0.1, nxt)
+    for got, f, s in zip(nxt, (u, v, w), want):
+        ref = f + 0.1 * s  # numpy: mul then add, no contraction
+        assert np.array_equal(got.cpu().numpy()[1:-1, 1:-1].view(np.int64),
+                              ref[1:-1, 1:-1].view(np.int64))
+
+
 @pytest.mark.parametrize("variant", ["xmarch", "xmarch_fma"])
 def test_interior_plus_rim_launch_equals_full(variant):
     dims, fields, co = baseline_case(23, 19, 64, seed=4)
