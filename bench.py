@@ -400,12 +400,21 @@ def run_ours(args):
         ctx.sync()
         t1 = time.perf_counter()
         ctx.close()
+        # the numpy drop-in (pageable inputs, as a reference user calls it)
+        fs_np = pw.FieldSet(*(pw.Field3D(dims, h.numpy().copy()) for h in hin))
+        co_host = pw.baseline_coefficients(SEED, nz)
+        pw.run_reference(fs_np, co_host)
+        t2 = time.perf_counter()
+        for _ in range(min(ke, 10)):
+            pw.run_reference(fs_np, co_host)
+        dropin_rate = dims.cells * min(ke, 10) / (time.perf_counter() - t2) / 1e9
         same = all(torch.equal(a.view(torch.int64), b.cpu().view(torch.int64)) for a, b in zip(hout, out))
         e2e = {"value": dims.cells * ke / (t1 - t0) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": ke, "chunks": args.chunks or "auto",
                "api": "pwadv_ctx_submit_host + pwadv_ctx_sync (C ABI; pinned host buffers; "
                       "H2D/K1/D2H pipelined across chunks and grids)",
                "value_sync_call": sync_rate,
+               "value_numpy_dropin": round(dropin_rate, 3),  # run_reference on pageable numpy
                # PCIe bound of this path on this box: every point moves 24 B each way
                "pcie_concurrent_GBs_each_way": round(pcie_gbs, 1),
                "pcie_bound": round(pcie_gbs * 1e9 / (h2d / dims.cells) / 1e9, 3),

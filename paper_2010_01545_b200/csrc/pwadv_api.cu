@@ -437,22 +437,38 @@ class CopyPool {
         cv_.notify_all();
         for (auto &t : workers_) t.join();
     }
-    void memcpy_parallel(void *dst, const void *src, size_t bytes)
+    struct Copy {
+        void *dst;
+        const void *src;
+        size_t bytes;
+    };
+    // All copies of a batch split into ~1 MiB pieces spread over the workers
+    // and the calling thread; returns when every piece is done.
+    void memcpy_batch(const Copy *cps, int n)
     {
-        const size_t parts = std::min(workers_.size() + 1, std::max<size_t>(1, bytes >> 21));
-        const size_t step = (bytes / parts + 63) & ~size_t(63);
-        std::vector<std::pair<size_t, size_t>> spans;
-        for (size_t off = 0; off < bytes; off += step) spans.push_back({off, std::min(step, bytes - off)});
+        constexpr size_t kPiece = size_t(1) << 20;
+        std::vector<Copy> pieces;
+        for (int i = 0; i < n; ++i)
+            for (size_t off = 0; off < cps[i].bytes; off += kPiece)
+                pieces.push_back({(char *)cps[i].dst + off, (const char *)cps[i].src + off,
+                                  std::min(kPiece, cps[i].bytes - off)});
+        if (pieces.empty()) return;
+        const size_t nt = workers_.size() + 1;
+        const size_t per = (pieces.size() + nt - 1) / nt;
+        auto job = [pieces, per](size_t t) {
+            for (size_t k = t * per; k < std::min(pieces.size(), (t + 1) * per); ++k)
+                memcpy(pieces[k].dst, pieces[k].src, pieces[k].bytes);
+        };
+        const size_t used = (pieces.size() + per - 1) / per;
         {
             std::lock_guard<std::mutex> lk(mu_);
-            for (size_t k = 1; k < spans.size(); ++k) {
-                const auto sp = spans[k];
-                tasks_.push_back([=] { memcpy((char *)dst + sp.first, (const char *)src + sp.first, sp.second); });
+            for (size_t t = 1; t < used; ++t) {
+                tasks_.push_back([job, t] { job(t); });
                 ++pending_;
             }
         }
         cv_.notify_all();
-        memcpy(dst, src, spans.empty() ? 0 : spans[0].second);  // the caller copies the first span
+        job(0);
         std::unique_lock<std::mutex> lk(mu_);
         done_.wait(lk, [this] { return pending_ == 0; });
     }
@@ -594,16 +610,20 @@ static bool is_pinned(const void *p)
 // pinned staging. Per chunk the host threads copy the inputs into staging
 // while the previous chunk's H2D, K1 and D2H run, then copy the previous
 // chunk's outputs out of staging.
+// Inputs or outputs in pageable memory: the pageable side goes through two
+// page-locked staging buffers filled / drained by the host copy pool while
+// the DMA engines work on the other buffer; a page-locked side is copied
+// directly (in_direct / out_direct).
 static int advect_host_staged(pwadv_ctx *c, const double *const hin[3], double *const hout[3],
                               double tcx, double tcy, const pwadv_opts *o, uint64_t *h2d,
-                              uint64_t *d2h)
+                              uint64_t *d2h, bool in_direct, bool out_direct)
 {
     const int64_t nx = c->nx, ny = c->ny, nz = c->nz;
     const size_t plane = (size_t)(ny + 2) * nz;
     const size_t pb = plane * sizeof(double);
     cudaError_t e;
     if (!c->pool) {
-        const int64_t target = (int64_t)(24u << 20) / (int64_t)(3 * pb);  // ~24 MB per buffer
+        const int64_t target = (int64_t)(48u << 20) / (int64_t)(3 * pb);  // ~48 MB per buffer
         c->pin_planes = std::max<int64_t>(3, std::min<int64_t>(target, nx + 2));
         for (int b = 0; b < 2; ++b) {
             e = cudaHostAlloc(&c->pin_in[b], 3 * c->pin_planes * pb, cudaHostAllocDefault);
@@ -627,11 +647,14 @@ static int advect_host_staged(pwadv_ctx *c, const double *const hin[3], double *
     int64_t copied = 0;
     int64_t prev_o0 = 0, prev_o1 = 0;
     auto drain = [&](int ch, int64_t o0, int64_t o1) -> int {
+        if (out_direct) return PWADV_OK;
         const int b = ch & 1;
         cudaError_t err = cudaEventSynchronize(c->ev_d2h[b]);
         if (err != cudaSuccess) return set_cuda_error("D2H wait", err);
+        pwadv::CopyPool::Copy cps[3];
         for (int m = 0; m < 3; ++m)
-            c->pool->memcpy_parallel(hout[m] + o0 * plane, c->pin_out[b] + m * P * plane, (o1 - o0) * pb);
+            cps[m] = {hout[m] + o0 * plane, c->pin_out[b] + m * P * plane, (size_t)(o1 - o0) * pb};
+        c->pool->memcpy_batch(cps, 3);
         return PWADV_OK;
     };
     for (int ch = 0; ch < chunks; ++ch) {
@@ -639,16 +662,21 @@ static int advect_host_staged(pwadv_ctx *c, const double *const hin[3], double *
         const int64_t x0 = 1 + (int64_t)ch * per;
         const int64_t x1 = std::min<int64_t>(nx + 1, x0 + per);
         const int64_t need = (ch == chunks - 1) ? nx + 2 : x1 + 1;
-        if (ch >= 2) {
+        if (ch >= 2 && !in_direct) {
             e = cudaEventSynchronize(c->ev_h2d[b]);  // staging b no longer read by its H2D
             if (e != cudaSuccess) return set_cuda_error("H2D wait", e);
         }
         const int64_t n_in = need - copied;
-        for (int m = 0; m < 3; ++m)
-            c->pool->memcpy_parallel(c->pin_in[b] + m * P * plane, hin[m] + copied * plane, n_in * pb);
+        if (!in_direct) {
+            pwadv::CopyPool::Copy cps[3];
+            for (int m = 0; m < 3; ++m)
+                cps[m] = {c->pin_in[b] + m * P * plane, hin[m] + copied * plane, (size_t)n_in * pb};
+            c->pool->memcpy_batch(cps, 3);
+        }
         for (int m = 0; m < 3; ++m) {
-            e = cudaMemcpyAsync(c->d_in[m] + copied * plane, c->pin_in[b] + m * P * plane, n_in * pb,
-                                cudaMemcpyHostToDevice, c->s_h2d);
+            const double *src = in_direct ? hin[m] + copied * plane : c->pin_in[b] + m * P * plane;
+            e = cudaMemcpyAsync(c->d_in[m] + copied * plane, src, n_in * pb, cudaMemcpyHostToDevice,
+                                c->s_h2d);
             if (e != cudaSuccess) return set_cuda_error("H2D", e);
         }
         *h2d += 3 * (uint64_t)n_in * pb;
@@ -664,8 +692,9 @@ static int advect_host_staged(pwadv_ctx *c, const double *const hin[3], double *
         const int64_t o0 = (ch == 0) ? 0 : x0;
         const int64_t o1 = (ch == chunks - 1) ? nx + 2 : x1;
         for (int m = 0; m < 3; ++m) {
-            e = cudaMemcpyAsync(c->pin_out[b] + m * P * plane, c->d_out[m] + o0 * plane, (o1 - o0) * pb,
-                                cudaMemcpyDeviceToHost, c->s_d2h);
+            double *dst = out_direct ? hout[m] + o0 * plane : c->pin_out[b] + m * P * plane;
+            e = cudaMemcpyAsync(dst, c->d_out[m] + o0 * plane, (o1 - o0) * pb, cudaMemcpyDeviceToHost,
+                                c->s_d2h);
             if (e != cudaSuccess) return set_cuda_error("D2H", e);
         }
         *d2h += 3 * (uint64_t)(o1 - o0) * pb;
@@ -674,7 +703,12 @@ static int advect_host_staged(pwadv_ctx *c, const double *const hin[3], double *
         prev_o0 = o0;
         prev_o1 = o1;
     }
-    return drain(chunks - 1, prev_o0, prev_o1);
+    int rc = drain(chunks - 1, prev_o0, prev_o1);
+    if (rc == PWADV_OK && out_direct) {
+        e = cudaStreamSynchronize(c->s_d2h);
+        if (e != cudaSuccess) return set_cuda_error("D2H wait", e);
+    }
+    return rc;
 }
 
 // Page-locked host buffers: H2D, K1 and D2H of X-slab chunks on three streams
@@ -772,15 +806,18 @@ int pwadv_ctx_advect_host(pwadv_ctx *c, const double *u, const double *v, const 
     if (e != cudaSuccess) return set_cuda_error("coefficient upload", e);
     h2d += 2 * nz * sizeof(double);
     pwadv_opts o = opts ? *opts : pwadv_opts{0u, 0, 0, 0, 0, 0, nullptr};
-    bool all_pinned = true;
-    for (int m = 0; m < 3; ++m) all_pinned = all_pinned && is_pinned(hin[m]) && is_pinned(hout[m]);
-    if (!all_pinned) {
+    bool in_pinned = true, out_pinned = true;
+    for (int m = 0; m < 3; ++m) {
+        in_pinned = in_pinned && is_pinned(hin[m]);
+        out_pinned = out_pinned && is_pinned(hout[m]);
+    }
+    if (!(in_pinned && out_pinned)) {
         if (c->set_used[0]) {  // an earlier asynchronous submission may still use set 0
             cudaStreamWaitEvent(c->s_h2d, c->ev_in_free[0], 0);
             cudaStreamWaitEvent(c->s_cmp, c->ev_out_free[0], 0);
         }
         uint64_t sh2d = 0, sd2h = 0;
-        int rc = advect_host_staged(c, hin, hout, tcx, tcy, &o, &sh2d, &sd2h);
+        int rc = advect_host_staged(c, hin, hout, tcx, tcy, &o, &sh2d, &sd2h, in_pinned, out_pinned);
         if (rc) return rc;
         c->last_h2d = h2d + sh2d;
         c->last_d2h = sd2h;

@@ -136,15 +136,29 @@ def _host_array(f, dims):
     return a
 
 
+def _output_array(shape) -> np.ndarray:
+    """A new float64 output array in page-locked memory (torch's caching host
+    allocator: blocks of released results are reused, and the D2H copies
+    land in it directly instead of through staging and first-touch page
+    faults); plain numpy memory if pinning is unavailable."""
+    import torch
+    try:
+        return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    except RuntimeError:
+        return np.empty(shape)
+
+
 def run_reference(fields, coeffs) -> SourceSet:
-    """Whole-grid PW advection; pure function of its inputs (reference kernel.py:175-185)."""
+    """Whole-grid PW advection; pure function of its inputs (reference kernel.py:175-185).
+    Like the reference (zeros_sources, grid.py:129-130) the callee allocates the
+    outputs; here they are page-locked numpy arrays."""
     dims = fields.dims
     nz_c = len(coeffs.tzc1)
     if nz_c != dims.nz:
         raise ValueError(f"coefficient length {nz_c} != nz {dims.nz}")
     gd = GridDims(dims.nx, dims.ny, dims.nz)
     u, v, w = (_host_array(f, dims) for f in (fields.u, fields.v, fields.w))
-    outs = [np.empty(gd.padded_shape) for _ in range(3)]
+    outs = [_output_array(gd.padded_shape) for _ in range(3)]
     _context(gd).advect_host(u, v, w, *outs, coeffs.tcx, coeffs.tcy, coeffs.tzc1, coeffs.tzc2)
     return SourceSet(*(Field3D(gd, o) for o in outs))
 
