@@ -37,6 +37,7 @@ FLAG_FMA = 1
 FLAG_SIMPLE = 2
 FLAG_RIM = 16
 FLAG_GENERIC = 32
+FLAG_L2_UNIT_HEAD = 64
 
 
 class Opts(ctypes.Structure):

@@ -108,6 +108,7 @@ struct TileCfg {
     int stages;       // ring depth
     int nchunks;      // X chunks per strip; work unit = (chunk, strip)
     int debug;        // ablation bits (PWADV_FLAG_DEBUG_*): 1 = no PW arithmetic, 4 = no stores
+    int l2hint;       // 1: load each unit's first two planes with L2 evict_last
     int64_t nstrips;  // ceil((y1-y0)/tj)
 };
 
@@ -253,6 +254,7 @@ struct RingState {
     int first[kMaxUnitsPerCta + 1];   // first sequence number of each unit
     uint32_t bytes[kMaxUnitsPerCta];  // bytes per field per plane of each unit
     int64_t src[kMaxUnitsPerCta];     // element offset of the unit's first plane tile
+    int l2hint;                       // TileCfg::l2hint
     int released[16];                 // per stage: warps done with its current plane
 };
 
@@ -277,6 +279,15 @@ __device__ __forceinline__ void issue_plane(const RingState *rs, const BoxArgs &
     const int64_t off = rs->src[k] + (int64_t)(q - rs->first[k]) * ((a.ny + 2) * a.nz);
     mbar_arrive_expect_tx(&full[st], 3 * bytes);
     double *dst = ring + (size_t)st * 3 * CS;
+    // the first two planes of a unit are read again, much later, by the unit
+    // of the previous X chunk (as its last two planes): keep them in L2
+    if (rs->l2hint && q - rs->first[k] < 2) {
+        const uint64_t pol = policy_evict_last();
+        bulk_g2s_hint(dst, a.u + off, bytes, &full[st], pol);
+        bulk_g2s_hint(dst + CS, a.v + off, bytes, &full[st], pol);
+        bulk_g2s_hint(dst + 2 * CS, a.w + off, bytes, &full[st], pol);
+        return;
+    }
     bulk_g2s(dst, a.u + off, bytes, &full[st]);
     bulk_g2s(dst + CS, a.v + off, bytes, &full[st]);
     bulk_g2s(dst + 2 * CS, a.w + off, bytes, &full[st]);
@@ -355,6 +366,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
         rs->first[k] = q;
         rs->total = q;
         rs->nunits = k;
+        rs->l2hint = t.l2hint;
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kComputeWarps);
@@ -662,6 +674,7 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         t.stages = plan.stages;
         t.nchunks = plan.nchunks;
         t.debug = (int)((L.flags >> 8) & 5u);
+        t.l2hint = (L.flags & PWADV_FLAG_L2_UNIT_HEAD) ? 1 : 0;
         t.nstrips = plan.nstrips;
         void (*kern)(BoxArgs, TileCfg) = nullptr;
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
@@ -780,25 +793,31 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
               sizeof(RingState);
     p->nstrips = (nby + tj - 1) / tj;
     // X chunking of the (chunk, strip) work units dealt round-robin to the
-    // grid. Measured on B200 (tools/sweep.py, profiles/): long units stream
-    // faster per plane than short ones, so take the fewest chunks whose
-    // units fill >= 90% of the grid's CTA slots over all rounds (C1 -> 10
-    // chunks, 2048-plane grids -> 4); if none does, the best filling one.
+    // grid, chosen by a cost model fitted on B200 (tools/sweep.py --rounds,
+    // profiles/README.md): a round of n concurrent units takes
+    // (planes per unit + 1) x max(n, A) plane-times, where A = g0 / 1.15 is
+    // the number of CTAs that already saturate HBM (fewer CTAs stream at
+    // their own latency-bound rate) and the +1 is the x-1 / x+1 planes a
+    // unit re-reads from DRAM. Picks 3 chunks at 512x512x64 (one round of
+    // 129 CTAs), 5 at 1024^2, 6 at 2048^2 (and 2048x1024x128).
     const int64_t g0 = L.grid > 0 ? L.grid : (int64_t)dev.sms * per_sm;  // one wave of resident CTAs
+    const int64_t sat = (g0 * 100 + 114) / 115;
     int64_t best_nch = 1;
-    double best_fill = -1.0;
+    double best_cost = -1.0;
     const int64_t nch_max = nbx < 4096 ? nbx : 4096;
     for (int64_t nch = L.chunks > 0 ? (L.chunks < nch_max ? L.chunks : nch_max) : 1; nch <= nch_max;
          ++nch) {
         const int64_t units = p->nstrips * nch;
         const int64_t rounds = (units + g0 - 1) / g0;
         if (rounds > kMaxUnitsPerCta) break;
-        const double fill = (double)units / (double)(rounds * g0);
-        if (fill > best_fill + 1e-9) {
-            best_fill = fill;
+        const int64_t full = units / g0, last = units % g0;
+        const double active = (double)(full * g0) + (last ? (double)(last > sat ? last : sat) : 0.0);
+        const double cost = ((double)((nbx + nch - 1) / nch) + 1.0) * active;
+        if (best_cost < 0.0 || cost < best_cost * (1.0 - 1e-9)) {
+            best_cost = cost;
             best_nch = nch;
         }
-        if (L.chunks > 0 || fill >= 0.9) break;
+        if (L.chunks > 0) break;
     }
     p->nchunks = (int)best_nch;
     const int64_t units = p->nstrips * best_nch;

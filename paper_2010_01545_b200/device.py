@@ -87,12 +87,11 @@ def _as_device_coeffs(coeffs, device) -> DeviceCoefficients:
 
 
 def make_opts(variant: str = "xmarch", *, tile_j: int = 0, stages: int = 0, grid: int = 0,
-              max_threads: int = 0, chunks: int = 0) -> _lib.Opts:
+              max_threads: int = 0, chunks: int = 0, flags: int = 0) -> _lib.Opts:
     """Kernel selection: "xmarch" (bulk-copy plane ring, default), "simple"
     (one thread per point), "xmarch_generic" (the X-march with a run-time
     tile layout even where a compile-time one exists); suffix "_fma" for the
     DFMA (not bit-exact) build."""
-    flags = 0
     base = variant
     if variant.endswith("_fma"):
         flags |= _lib.FLAG_FMA

@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--config", default="c1")
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--ablate", action="store_true")
+    ap.add_argument("--rounds", type=int, default=1)
     ap.add_argument("--variants", default="", help="JSON list of variant dicts (overrides)")
     args = ap.parse_args()
     nx, ny, nz = SHAPES[args.config]
@@ -60,26 +61,41 @@ def main():
             variants += [dict(variant="xmarch", stages=st, debug=5), dict(variant="xmarch", stages=st, debug=4)]
         for mt in (192, 128):
             variants += [dict(variant="xmarch", max_threads=mt, debug=5)]
-    for v in variants:
-        kw = dict(v)
-        name = kw.pop("variant")
-        dbg = kw.pop("debug", 0)
-        opts = device.make_opts(name, **kw)
-        opts.flags |= (dbg << 8)
-        try:
-            plan = device.describe_plan(dims, None, opts)
-            ms = time_it(lambda: device.advect(*fields, co, out, opts=opts), args.reps)
-        except Exception as e:  # noqa: BLE001
-            print(json.dumps({"variant": v, "error": str(e)}))
+    # --rounds R: the variants are timed round-robin R times (cancels clock and
+    # power-cap drift across the sweep); the line reports the median and best
+    timings = {i: [] for i in range(len(variants))}
+    meta = {}
+    for _ in range(args.rounds):
+        for i, v in enumerate(variants):
+            kw = dict(v)
+            name = kw.pop("variant")
+            dbg = kw.pop("debug", 0)
+            opts = device.make_opts(name, **kw)
+            opts.flags |= (dbg << 8)
+            try:
+                plan = device.describe_plan(dims, None, opts)
+                ms = time_it(lambda: device.advect(*fields, co, out, opts=opts), args.reps)
+            except Exception as e:  # noqa: BLE001
+                meta[i] = {"error": str(e)}
+                continue
+            snap = [o.clone() for o in out]
+            if ref is None:
+                ref = snap
+            same = all(torch.equal(a.view(torch.int64), b.view(torch.int64)) for a, b in zip(ref, snap))
+            timings[i].append(ms)
+            meta[i] = {"plan": plan, "same": same and meta.get(i, {}).get("same", True)}
+    for i, v in enumerate(variants):
+        if not timings[i]:
+            print(json.dumps({"variant": v, **meta.get(i, {})}))
             continue
-        snap = [o.clone() for o in out]
-        if ref is None:
-            ref = snap
-        same = all(torch.equal(a.view(torch.int64), b.view(torch.int64)) for a, b in zip(ref, snap))
+        ts = sorted(timings[i])
+        ms = ts[len(ts) // 2]
         gbs = 48 * dims.cells / (ms / 1e3) / 1e9
         print(json.dumps({"config": args.config, "variant": v, "ms": round(ms, 4),
-                          "gpts": round(dims.cells / ms / 1e6, 2), "GBs": round(gbs, 1),
-                          "bitwise_same_as_first": same, "plan": plan}), flush=True)
+                          "gpts": round(dims.cells / ms / 1e6, 2),
+                          "gpts_best": round(dims.cells / ts[0] / 1e6, 2), "GBs": round(gbs, 1),
+                          "bitwise_same_as_first": meta[i]["same"], "plan": meta[i]["plan"]}),
+              flush=True)
     # fused step K4
     nxt = device.alloc_fields(dims, fields[0].device)
     ms = time_it(lambda: device.step(*fields, co, 0.1, nxt), args.reps)
