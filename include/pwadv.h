@@ -115,7 +115,8 @@ typedef struct pwadv_plan_info {
     int32_t kernel;        /* 1 = X-march (bulk-copy plane ring), 2 = one-thread-per-point */
     int32_t tile_j, threads_per_column, stages, threads, grid;
     int64_t smem_bytes, strips;
-    int32_t chunks, reserved;
+    int32_t chunks;        /* X chunks of the strips after the full rounds */
+    int32_t long_strips;   /* strips run as whole-X units (full rounds of the grid) */
 } pwadv_plan_info;
 int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz,
                         int64_t x_begin, int64_t x_end, int64_t y_begin, int64_t y_end,

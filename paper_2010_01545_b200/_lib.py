@@ -56,7 +56,7 @@ class PlanInfo(ctypes.Structure):
                 ("threads_per_column", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("threads", ctypes.c_int32), ("grid", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_int64), ("strips", ctypes.c_int64),
-                ("chunks", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("chunks", ctypes.c_int32), ("long_strips", ctypes.c_int32)]
 
 
 class Peers(ctypes.Structure):

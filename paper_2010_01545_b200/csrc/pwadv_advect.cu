@@ -110,25 +110,35 @@ struct TileCfg {
     int debug;        // ablation bits (PWADV_FLAG_DEBUG_*): 1 = no PW arithmetic, 4 = no stores
     int l2hint;       // 1: load each unit's first two planes with L2 evict_last
     int64_t nstrips;  // ceil((y1-y0)/tj)
+    int64_t nlong;    // strips 0..nlong-1 are whole-X units (full rounds); the rest are chunked
 };
 
-// Work units are (chunk, strip) pairs numbered chunk-major,
-// u = chunk * nstrips + strip, dealt round-robin to the CTAs: CTA b runs units
+// Work units (unit_at) are dealt round-robin to the CTAs: CTA b runs units
 // b, b+G, b+2G, ... All CTAs start a round together and march at the same
 // rate, so CTAs on adjacent strips stand on the same X planes at the same
 // time and each strip's two halo columns (the neighbours' edge columns) are
-// served from L2 instead of HBM; the plane before a chunk was streamed by the
-// previous round for the same strip and is an L2 hit as well.
+// served from L2 instead of HBM.
 struct Unit {
     int64_t strip, ib, ie;  // outputs i in [ib, ie) of this strip
 };
 
+// Units 0..nlong-1 are whole strips (the full rounds: every CTA marches the
+// whole X range, all CTAs in step); the remaining strips are cut into
+// nchunks X chunks so the last rounds keep the grid busy.
 __device__ __forceinline__ Unit unit_at(const BoxArgs &a, const TileCfg &t, int64_t u)
 {
-    const int64_t chunk = u / t.nstrips;
     const int64_t nxr = a.x1 - a.x0;
     Unit w;
-    w.strip = u - chunk * t.nstrips;
+    if (u < t.nlong) {
+        w.strip = u;
+        w.ib = a.x0;
+        w.ie = a.x1;
+        return w;
+    }
+    const int64_t tail = t.nstrips - t.nlong;
+    const int64_t v = u - t.nlong;
+    const int64_t chunk = v / tail;
+    w.strip = t.nlong + (v - chunk * tail);
     w.ib = a.x0 + (nxr * chunk) / t.nchunks;
     w.ie = a.x0 + (nxr * (chunk + 1)) / t.nchunks;
     return w;
@@ -348,7 +358,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     const double c2a = __ldg(a.tzc2 + k0), c2b = __ldg(a.tzc2 + k1);
 
     const int64_t ny2 = a.ny + 2;
-    const int64_t nunits = t.nstrips * t.nchunks;
+    const int64_t nunits = t.nlong + (t.nstrips - t.nlong) * t.nchunks;
     const int64_t G = gridDim.x;
     if ((int64_t)blockIdx.x >= nunits) return;
 
@@ -676,6 +686,7 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         t.debug = (int)((L.flags >> 8) & 5u);
         t.l2hint = (L.flags & PWADV_FLAG_L2_UNIT_HEAD) ? 1 : 0;
         t.nstrips = plan.nstrips;
+        t.nlong = plan.nlong;
         void (*kern)(BoxArgs, TileCfg) = nullptr;
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
         // compile-time layout for the BASELINE depths at the default tile
@@ -792,23 +803,30 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     p->smem = (size_t)stages * 3 * (tj + 2) * nz * sizeof(double) + 2 * stages * sizeof(uint64_t) +
               sizeof(RingState);
     p->nstrips = (nby + tj - 1) / tj;
-    // X chunking of the (chunk, strip) work units dealt round-robin to the
-    // grid, chosen by a cost model fitted on B200 (tools/sweep.py --rounds,
-    // profiles/README.md): a round of n concurrent units takes
-    // (planes per unit + 1) x max(n, A) plane-times, where A = g0 / 1.15 is
-    // the number of CTAs that already saturate HBM (fewer CTAs stream at
-    // their own latency-bound rate) and the +1 is the x-1 / x+1 planes a
-    // unit re-reads from DRAM. Picks 3 chunks at 512x512x64 (one round of
-    // 129 CTAs), 5 at 1024^2, 6 at 2048^2 (and 2048x1024x128).
+    // Work units dealt round-robin to one wave of CTAs. Whole strips fill
+    // as many full rounds as there are (long units keep all CTAs marching in
+    // step: at 4096x4096x128, 36 short units per CTA instead of 5 long ones
+    // drifted apart and ran 39% slower at the same DRAM bytes); the strips
+    // left over are cut into X chunks chosen by a cost model fitted on B200
+    // (tools/sweep.py --rounds, profiles/README.md): a round of n concurrent
+    // units takes (planes per unit + 1) x max(n, A) plane-times, A = g0/1.15
+    // being the CTAs that already saturate HBM (fewer stream at their own
+    // latency-bound rate) and +1 the plane pair a unit re-reads. E.g. 3 chunks
+    // at 512x512x64 (one round of 129 CTAs), 5 at 1024^2; at 2048^2 one full
+    // round plus 23 strips in 32 chunks. opts.chunks > 0 forces uniform
+    // chunking of every strip.
     const int64_t g0 = L.grid > 0 ? L.grid : (int64_t)dev.sms * per_sm;  // one wave of resident CTAs
     const int64_t sat = (g0 * 100 + 114) / 115;
+    const int64_t full_rounds = L.chunks > 0 ? 0 : p->nstrips / g0;
+    p->nlong = full_rounds * g0;
+    const int64_t tail = p->nstrips - p->nlong;
     int64_t best_nch = 1;
     double best_cost = -1.0;
     const int64_t nch_max = nbx < 4096 ? nbx : 4096;
-    for (int64_t nch = L.chunks > 0 ? (L.chunks < nch_max ? L.chunks : nch_max) : 1; nch <= nch_max;
-         ++nch) {
-        const int64_t units = p->nstrips * nch;
-        const int64_t rounds = (units + g0 - 1) / g0;
+    for (int64_t nch = L.chunks > 0 ? (L.chunks < nch_max ? L.chunks : nch_max) : 1;
+         tail > 0 && nch <= nch_max; ++nch) {
+        const int64_t units = tail * nch;
+        const int64_t rounds = full_rounds + (units + g0 - 1) / g0;
         if (rounds > kMaxUnitsPerCta) break;
         const int64_t full = units / g0, last = units % g0;
         const double active = (double)(full * g0) + (last ? (double)(last > sat ? last : sat) : 0.0);
@@ -820,7 +838,7 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
         if (L.chunks > 0) break;
     }
     p->nchunks = (int)best_nch;
-    const int64_t units = p->nstrips * best_nch;
+    const int64_t units = p->nlong + tail * best_nch;
     int64_t grid = units < g0 ? units : g0;
     if (grid < 1) grid = 1;
     p->grid = (int)grid;

@@ -300,6 +300,7 @@ int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz, int64_t x0, int64_t 
         out->smem_bytes = (int64_t)p.smem;
         out->strips = p.nstrips;
         out->chunks = p.nchunks;
+        out->long_strips = (int32_t)p.nlong;
     } else {
         out->kernel = 2;
         out->threads = 256;

@@ -35,6 +35,7 @@ struct XmarchPlan {
     size_t smem;
     int64_t nstrips;
     int64_t rounds;  // units per CTA (the kernel's unit table holds kMaxUnitsPerCta)
+    int64_t nlong;   // strips run as whole-X units (full rounds)
 };
 
 // cached attributes of the current device (lazily filled, thread-safe)

@@ -15,7 +15,7 @@ import paper_2010_01545_b200 as pw  # noqa: E402
 from paper_2010_01545_b200 import device  # noqa: E402
 
 SHAPES = {"c1": (512, 512, 64), "c2": (1024, 1024, 64), "c3": (2048, 2048, 64),
-          "c4blk": (2048, 1024, 128), "c0": (64, 64, 64)}
+          "c4blk": (2048, 1024, 128), "c0": (64, 64, 64), "c4full": (4096, 4096, 128)}
 
 
 def time_it(fn, reps):
@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--ablate", action="store_true")
     ap.add_argument("--rounds", type=int, default=1)
+    ap.add_argument("--step", action="store_true", help="time the fused step K4 (ping-pong) instead of K1")
     ap.add_argument("--variants", default="", help="JSON list of variant dicts (overrides)")
     args = ap.parse_args()
     nx, ny, nz = SHAPES[args.config]
@@ -74,14 +75,18 @@ def main():
             opts.flags |= (dbg << 8)
             try:
                 plan = device.describe_plan(dims, None, opts)
-                ms = time_it(lambda: device.advect(*fields, co, out, opts=opts), args.reps)
+                if args.step:
+                    ms = time_it(lambda: device.step(*fields, co, 0.1, out, opts=opts), args.reps)
+                else:
+                    ms = time_it(lambda: device.advect(*fields, co, out, opts=opts), args.reps)
             except Exception as e:  # noqa: BLE001
                 meta[i] = {"error": str(e)}
                 continue
-            snap = [o.clone() for o in out]
+            # digest of the output bits (no full-size copy: c4full fills HBM)
+            snap = [int(o.view(torch.int64).sum().item()) for o in out]
             if ref is None:
                 ref = snap
-            same = all(torch.equal(a.view(torch.int64), b.view(torch.int64)) for a, b in zip(ref, snap))
+            same = snap == ref
             timings[i].append(ms)
             meta[i] = {"plan": plan, "same": same and meta.get(i, {}).get("same", True)}
     for i, v in enumerate(variants):
@@ -96,6 +101,8 @@ def main():
                           "gpts_best": round(dims.cells / ts[0] / 1e6, 2), "GBs": round(gbs, 1),
                           "bitwise_same_as_first": meta[i]["same"], "plan": meta[i]["plan"]}),
               flush=True)
+    if args.step:
+        return
     # fused step K4
     nxt = device.alloc_fields(dims, fields[0].device)
     ms = time_it(lambda: device.step(*fields, co, 0.1, nxt), args.reps)
