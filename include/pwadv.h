@@ -170,6 +170,28 @@ int pwadv_ipc_export(const void *dev_ptr, unsigned char handle[64], uint64_t *of
 int pwadv_ipc_open(const unsigned char handle[64], uint64_t offset, void **dev_ptr);
 int pwadv_ipc_close(void *dev_ptr, uint64_t offset);
 
+/*
+ * K6 — the reference's array-level entry points (device pointers):
+ * compute_block (kernel.py:139-162): roles[17] are the COMPUTE_ROLES arrays
+ * (kernel.py:134-136, sorted (field, dx, dy) order: u(-1,0) u(-1,1) u(0,-1)
+ * u(0,0) u(0,1) u(1,0) v(-1,0) v(0,-1) v(0,0) v(0,1) v(1,-1) v(1,0) w(-1,0)
+ * w(0,-1) w(0,0) w(0,1) w(1,0)), each ncols contiguous columns of nz levels;
+ * su/sv/sw get level 0 = +0.0, the mid formula at 1..nz-2 and the top formula
+ * at nz-1, exactly as compute_block. flags: PWADV_FLAG_FMA or 0.
+ */
+int pwadv_compute_block_f64(const double *const *roles, double *su, double *sv, double *sw,
+                            int64_t ncols, int64_t nz, double tcx, double tcy,
+                            const double *tzc1, const double *tzc2, uint32_t flags, void *stream);
+/*
+ * su_formula / sv_formula / sw_formula (kernel.py:73-112; which = 0 / 1 / 2)
+ * elementwise over n points: args[19] = tcx, tcy, tzc1_k, tzc2_k and the 15
+ * operands in the reference's parameter order, each read at index i*stride
+ * (stride 0 = a broadcast scalar, 1 = an array); top selects the k = nz
+ * branch for all points.
+ */
+int pwadv_formula_f64(int32_t which, const double *const *args, const int64_t *strides, int64_t n,
+                      int32_t top, double *out, uint32_t flags, void *stream);
+
 /* K2 — periodic halo wrap in place (grid.py:203-208: X then Y semantics). */
 int pwadv_wrap_halos_f64(double *f, int64_t nx, int64_t ny, int64_t nz, void *stream);
 /* K2 on three fields in one launch. */

@@ -209,6 +209,57 @@ def advect_numpy(u, v, w, tcx, tcy, tzc1, tzc2):
     return tuple(outs)
 
 
+# array-level API restated (reference kernel.py:73-162)
+
+ROLES = (("u", -1, 0), ("u", -1, 1), ("u", 0, -1), ("u", 0, 0), ("u", 0, 1), ("u", 1, 0),
+         ("v", -1, 0), ("v", 0, -1), ("v", 0, 0), ("v", 0, 1), ("v", 1, -1), ("v", 1, 0),
+         ("w", -1, 0), ("w", 0, -1), ("w", 0, 0), ("w", 0, 1), ("w", 1, 0))
+# (role index, k offset) of each formula operand, kernel.py:117-128
+WIRING = (
+    ((3, 0), (0, 0), (5, 0), (2, 0), (4, 0), (3, -1), (3, 1), (7, 0), (10, 0), (8, 0), (11, 0),
+     (14, -1), (16, -1), (14, 0), (16, 0)),
+    ((8, 0), (6, 0), (11, 0), (7, 0), (9, 0), (8, -1), (8, 1), (0, 0), (1, 0), (3, 0), (4, 0),
+     (14, -1), (15, -1), (14, 0), (15, 0)),
+    ((14, 0), (12, 0), (16, 0), (13, 0), (15, 0), (14, -1), (14, 1), (0, -1), (0, 0), (3, -1),
+     (3, 0), (7, -1), (7, 0), (8, -1), (8, 0)),
+)
+
+
+def formula_numpy(which: int, args, top: bool = False):
+    """su/sv/sw_formula (kernel.py:73-112) as one generic expression: the three
+    formulas differ only in which operands fill the X, Y and Z slots."""
+    tcx, tcy, c1, c2 = args[:4]
+    o = args[4:]
+    # (x1, x2, x3, x4, x5, x6, y1..y6, z1..z6) positions in the operand list
+    slots = (
+        (1, 0, 1, 2, 0, 2, 3, 7, 8, 4, 9, 10, 5, 11, 12, 6, 13, 14),   # su
+        (1, 7, 8, 2, 9, 10, 3, 0, 3, 4, 0, 4, 5, 11, 12, 6, 13, 14),   # sv
+        (1, 7, 8, 2, 9, 10, 3, 11, 12, 4, 13, 14, 5, 0, 5, 6, 0, 6),   # sw
+    )[which]
+    x1, x2, x3, x4, x5, x6, y1, y2, y3, y4, y5, y6, z1, z2, z3, z4, z5, z6 = (o[i] for i in slots)
+    s = tcx * (x1 * (x2 + x3) - x4 * (x5 + x6))
+    s = s + tcy * (y1 * (y2 + y3) - y4 * (y5 + y6))
+    if top:
+        return s + c1 * z1 * (z2 + z3)
+    return s + (c1 * z1 * (z2 + z3) - c2 * z4 * (z5 + z6))
+
+
+def compute_block_numpy(tcx, tcy, tzc1, tzc2, roles):
+    """compute_block (kernel.py:139-162) over role arrays listed in ROLES order."""
+    nz = roles[3].shape[-1]
+    t = nz - 1
+    outs = []
+    for which in range(3):
+        s = np.zeros_like(roles[3])
+        if nz > 2:
+            ops = [roles[r][..., 1 + dk:nz - 1 + dk] for r, dk in WIRING[which]]
+            s[..., 1:nz - 1] = formula_numpy(which, [tcx, tcy, tzc1[1:nz - 1], tzc2[1:nz - 1]] + ops)
+        ops = [roles[r][..., t - 1 if dk == -1 else t] for r, dk in WIRING[which]]
+        s[..., t] = formula_numpy(which, [tcx, tcy, float(tzc1[t]), float(tzc2[t])] + ops, top=True)
+        outs.append(s)
+    return tuple(outs)
+
+
 def step(u, v, w, tcx, tcy, tzc1, tzc2, dt: float, steps: int, engines: int = 1):
     """Composed forward-Euler oracle: in place on u, v, w."""
     nx, ny, nz = u.shape[0] - 2, u.shape[1] - 2, u.shape[2]

@@ -1,9 +1,11 @@
 """B200-native PW-advection hot path of arXiv 2010.01545 (drop-in for pwadvect's stencil).
 
 Import surface mirrors the reference package facade for the hot path
-(pkg/src/pwadvect/__init__.py:11-34: grid, kernel and schedules names) and
-adds the device-resident API (`device`), the x-y decomposition with halo
-exchange (`decomp`) and the fused time-stepping driver (`stepper`).
+(pkg/src/pwadvect/__init__.py:11-34: grid, kernel and schedules names; the
+submodules `grid`, `kernel` and `schedules` mirror the reference modules of
+those names) and adds the device-resident API (`device`), the x-y
+decomposition with halo exchange (`decomp`) and the fused time-stepping
+driver (`stepper`).
 All compute runs in libpwadv.so (hand-written sm_100a CUDA); there is no CPU
 fallback.
 """

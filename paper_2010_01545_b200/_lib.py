@@ -85,6 +85,10 @@ SIGNATURES = {
     "pwadv_ipc_export": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_uint64)]),
     "pwadv_ipc_open": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.POINTER(_P)]),
     "pwadv_ipc_close": (ctypes.c_int, [_P, ctypes.c_uint64]),
+    "pwadv_compute_block_f64": (ctypes.c_int, [_P] * 4 + [_I64, _I64, _D, _D, _P, _P,
+                                                           ctypes.c_uint32, _P]),
+    "pwadv_formula_f64": (ctypes.c_int, [ctypes.c_int32, _P, _P, _I64, ctypes.c_int32, _P,
+                                         ctypes.c_uint32, _P]),
     "pwadv_wrap_halos_f64": (ctypes.c_int, [_P, _I64, _I64, _I64, _P]),
     "pwadv_wrap_halos3_f64": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, _P]),
     "pwadv_wrap_axis3_f64": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, ctypes.c_int32, _P]),

@@ -11,7 +11,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpwadv.so"
-SOURCES = ["pwadv_advect.cu", "pwadv_aux.cu", "pwadv_api.cu"]
+SOURCES = ["pwadv_advect.cu", "pwadv_aux.cu", "pwadv_roles.cu", "pwadv_api.cu"]
 HEADERS = ["pwadv_device.cuh", "pwadv_internal.h"]
 
 

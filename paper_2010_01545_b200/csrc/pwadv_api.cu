@@ -308,6 +308,41 @@ int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz, int64_t x0, int64_t 
     return PWADV_OK;
 }
 
+int pwadv_compute_block_f64(const double *const *roles, double *su, double *sv, double *sw,
+                            int64_t ncols, int64_t nz, double tcx, double tcy,
+                            const double *tzc1, const double *tzc2, uint32_t flags, void *stream)
+{
+    if (!roles) return set_error(PWADV_E_NULL, "null role table");
+    if (ncols < 0) return set_error(PWADV_E_DIMS, "ncols %lld < 0", (long long)ncols);
+    if (nz < 2) return set_error(PWADV_E_DIMS, "nz %lld < 2", (long long)nz);
+    for (int m = 0; m < 17; ++m) {
+        int rc = check_ptrs({roles[m]});
+        if (rc) return rc;
+    }
+    int rc = check_ptrs({su, sv, sw, tzc1, tzc2});
+    if (rc) return rc;
+    return pwadv::launch_compute_block(roles, su, sv, sw, ncols, nz, tcx, tcy, tzc1, tzc2,
+                                       (flags & PWADV_FLAG_FMA) != 0, (cudaStream_t)stream);
+}
+
+int pwadv_formula_f64(int32_t which, const double *const *args, const int64_t *strides, int64_t n,
+                      int32_t top, double *out, uint32_t flags, void *stream)
+{
+    if (which < 0 || which > 2) return set_error(PWADV_E_ARG, "formula %d (0 su, 1 sv, 2 sw)", which);
+    if (!args || !strides) return set_error(PWADV_E_NULL, "null argument table");
+    if (n < 0) return set_error(PWADV_E_DIMS, "n %lld < 0", (long long)n);
+    for (int m = 0; m < 19; ++m) {
+        int rc = check_ptrs({args[m]});
+        if (rc) return rc;
+        if (strides[m] != 0 && strides[m] != 1)
+            return set_error(PWADV_E_ARG, "argument %d stride %lld (0 or 1)", m, (long long)strides[m]);
+    }
+    int rc = check_ptrs({out});
+    if (rc) return rc;
+    return pwadv::launch_formula(which, args, strides, n, top, out, (flags & PWADV_FLAG_FMA) != 0,
+                                 (cudaStream_t)stream);
+}
+
 int pwadv_wrap_halos_f64(double *f, int64_t nx, int64_t ny, int64_t nz, void *stream)
 {
     int rc = check_dims(nx, ny, nz);

@@ -46,6 +46,11 @@ int set_cuda_error(const char *what, cudaError_t e);
 void count_launch();
 
 bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p);
+int launch_compute_block(const double *const roles[17], double *su, double *sv, double *sw,
+                         int64_t ncols, int64_t nz, double tcx, double tcy, const double *tzc1,
+                         const double *tzc2, bool fma, cudaStream_t s);
+int launch_formula(int which, const double *const args[19], const int64_t strides[19], int64_t n,
+                   int top, double *out, bool fma, cudaStream_t s);
 int launch_box(const BoxLaunch &L, cudaStream_t stream);
 
 // auxiliary kernels (pwadv_aux.cu)

@@ -88,8 +88,9 @@ COMPUTE_ROLES: tuple[tuple[str, int, int], ...] = (
 
 # Per formula and point: multiplications, add/subs, operand reads, as the
 # reference's symbolic census reports them (kernel.py:254-267): 10/11/18 below
-# the top level, 8/9/15 at k = nz. The device kernel performs exactly these
-# DMUL/DADD operations (63 per point below the top).
+# the top level, 8/9/15 at k = nz (63 operations per point). K1 produces the
+# same bits with 57: the x-direction sums it carries from plane to plane and
+# the z-sums shared by a thread's two levels are computed once.
 _CENSUS = {False: {"muls": 10, "adds": 11, "loads": 18}, True: {"muls": 8, "adds": 9, "loads": 15}}
 
 
@@ -99,6 +100,139 @@ def operation_census(top: bool = False) -> dict:
 
 def reads_per_point(top: bool = False) -> int:
     return 3 * _CENSUS[bool(top)]["loads"]
+
+
+# ---------------------------------------------------------------------------
+# array-level API (reference kernel.py:73-172), executed by K6 on the GPU
+
+# Operand wiring (field, dx, dy, dk) per positional formula argument
+# (kernel.py:117-128).
+_SU_ARGS = (("u", 0, 0, 0), ("u", -1, 0, 0), ("u", 1, 0, 0), ("u", 0, -1, 0), ("u", 0, 1, 0),
+            ("u", 0, 0, -1), ("u", 0, 0, 1), ("v", 0, -1, 0), ("v", 1, -1, 0), ("v", 0, 0, 0),
+            ("v", 1, 0, 0), ("w", 0, 0, -1), ("w", 1, 0, -1), ("w", 0, 0, 0), ("w", 1, 0, 0))
+_SV_ARGS = (("v", 0, 0, 0), ("v", -1, 0, 0), ("v", 1, 0, 0), ("v", 0, -1, 0), ("v", 0, 1, 0),
+            ("v", 0, 0, -1), ("v", 0, 0, 1), ("u", -1, 0, 0), ("u", -1, 1, 0), ("u", 0, 0, 0),
+            ("u", 0, 1, 0), ("w", 0, 0, -1), ("w", 0, 1, -1), ("w", 0, 0, 0), ("w", 0, 1, 0))
+_SW_ARGS = (("w", 0, 0, 0), ("w", -1, 0, 0), ("w", 1, 0, 0), ("w", 0, -1, 0), ("w", 0, 1, 0),
+            ("w", 0, 0, -1), ("w", 0, 0, 1), ("u", -1, 0, -1), ("u", -1, 0, 0), ("u", 0, 0, -1),
+            ("u", 0, 0, 0), ("v", 0, -1, -1), ("v", 0, -1, 0), ("v", 0, 0, -1), ("v", 0, 0, 0))
+
+
+def _device():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("the B200 path has no CPU fallback: a CUDA device is required")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _formula(which: int, args, top: bool):
+    import ctypes
+    import torch
+    from . import _lib
+    from .device import _stream_handle
+    if len(args) != 19:
+        raise TypeError(f"formula takes 19 positional arguments ({len(args)} given)")
+    arrs = [np.asarray(a, dtype=np.float64) for a in args]
+    shape = np.broadcast_shapes(*(a.shape for a in arrs))
+    n = int(np.prod(shape, dtype=np.int64))
+    dev = _device()
+    keep, ptrs, strides = [], (ctypes.c_void_p * 19)(), (ctypes.c_int64 * 19)()
+    for m, a in enumerate(arrs):
+        if a.size == 1:
+            t = torch.tensor([float(a.reshape(-1)[0])], dtype=torch.float64, device=dev)
+            strides[m] = 0
+        else:
+            full = np.array(np.broadcast_to(a, shape), dtype=np.float64, order="C")  # writable copy
+            t = torch.from_numpy(full.reshape(-1)).to(dev)
+            strides[m] = 1
+        keep.append(t)
+        ptrs[m] = t.data_ptr()
+    out = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().pwadv_formula_f64(which, ptrs, strides, n, 1 if top else 0,
+                                            ctypes.c_void_p(out.data_ptr()), 0,
+                                            _stream_handle(None, dev)))
+    res = out[:n].cpu().numpy().reshape(shape)
+    if all(np.ndim(a) == 0 and not isinstance(a, np.ndarray) for a in args):
+        return float(res)
+    return res
+
+
+def su_formula(tcx, tcy, tzc1_k, tzc2_k, u_c, u_xm1, u_xp1, u_jm1, u_jp1, u_km1, u_kp1,
+               v_jm1, v_jm1_xp1, v_c, v_xp1, w_km1, w_km1_xp1, w_c, w_xp1, top=False):
+    """su at broadcast points (kernel.py:73-84); the top branch drops the tzc2 half."""
+    return _formula(0, (tcx, tcy, tzc1_k, tzc2_k, u_c, u_xm1, u_xp1, u_jm1, u_jp1, u_km1, u_kp1,
+                        v_jm1, v_jm1_xp1, v_c, v_xp1, w_km1, w_km1_xp1, w_c, w_xp1), top)
+
+
+def sv_formula(tcx, tcy, tzc1_k, tzc2_k, v_c, v_xm1, v_xp1, v_jm1, v_jp1, v_km1, v_kp1,
+               u_xm1, u_xm1_jp1, u_c, u_jp1, w_km1, w_km1_jp1, w_c, w_jp1, top=False):
+    """sv at broadcast points (kernel.py:87-98)."""
+    return _formula(1, (tcx, tcy, tzc1_k, tzc2_k, v_c, v_xm1, v_xp1, v_jm1, v_jp1, v_km1, v_kp1,
+                        u_xm1, u_xm1_jp1, u_c, u_jp1, w_km1, w_km1_jp1, w_c, w_jp1), top)
+
+
+def sw_formula(tcx, tcy, tzc1_k, tzc2_k, w_c, w_xm1, w_xp1, w_jm1, w_jp1, w_km1, w_kp1,
+               u_xm1_km1, u_xm1, u_km1, u_c, v_jm1_km1, v_jm1, v_km1, v_c, top=False):
+    """sw at broadcast points (kernel.py:101-112)."""
+    return _formula(2, (tcx, tcy, tzc1_k, tzc2_k, w_c, w_xm1, w_xp1, w_jm1, w_jp1, w_km1, w_kp1,
+                        u_xm1_km1, u_xm1, u_km1, u_c, v_jm1_km1, v_jm1, v_km1, v_c), top)
+
+
+_FORMULAS = ((su_formula, _SU_ARGS), (sv_formula, _SV_ARGS), (sw_formula, _SW_ARGS))
+
+
+def compute_block(coeffs, roles: dict):
+    """su/sv/sw of columns given their 17 role arrays (kernel.py:139-162).
+
+    `roles` maps each COMPUTE_ROLES key to an array shaped (..., nz) with a
+    common leading shape; returns three arrays of that shape with level 0
+    zeroed, the mid formula at levels 1..nz-2 and the top formula at nz-1.
+    Runs as one K6 launch on the GPU."""
+    import ctypes
+    import torch
+    from . import _lib
+    from .device import _stream_handle
+    base = np.asarray(roles[("u", 0, 0)])
+    shape = base.shape
+    if len(shape) < 1:
+        raise ValueError("role arrays must be shaped (..., nz)")
+    nz = shape[-1]
+    if nz < 2:
+        raise ValueError(f"nz {nz} < 2")
+    tz1 = np.ascontiguousarray(coeffs.tzc1, dtype=np.float64)
+    tz2 = np.ascontiguousarray(coeffs.tzc2, dtype=np.float64)
+    if tz1.shape != (nz,) or tz2.shape != (nz,):
+        raise ValueError(f"coefficient length {tz1.shape[0]} != nz {nz}")
+    ncols = int(np.prod(shape[:-1], dtype=np.int64))
+    dev = _device()
+    keep, ptrs = [], (ctypes.c_void_p * 17)()
+    for m, key in enumerate(COMPUTE_ROLES):
+        a = np.asarray(roles[key], dtype=np.float64)
+        if a.shape != shape:
+            raise ValueError(f"role {key} shape {a.shape} != {shape}")
+        if a.size:
+            host = a if a.flags.c_contiguous and a.flags.writeable else np.array(a, order="C")
+            t = torch.from_numpy(host.reshape(-1)).to(dev)
+        else:
+            t = torch.empty(1, dtype=torch.float64, device=dev)
+        keep.append(t)
+        ptrs[m] = t.data_ptr()
+    tz = torch.from_numpy(np.concatenate([tz1, tz2])).to(dev)
+    outs = [torch.empty(max(ncols * nz, 1), dtype=torch.float64, device=dev) for _ in range(3)]
+    _lib.check(_lib.lib().pwadv_compute_block_f64(
+        ptrs, *(ctypes.c_void_p(o.data_ptr()) for o in outs), ncols, nz, float(coeffs.tcx),
+        float(coeffs.tcy), ctypes.c_void_p(tz.data_ptr()), ctypes.c_void_p(tz.data_ptr() + 8 * nz),
+        0, _stream_handle(None, dev)))
+    return tuple(o[:ncols * nz].cpu().numpy().reshape(shape) for o in outs)
+
+
+def grid_roles(fields, x0: int, x1: int) -> dict:
+    """Role views over interior columns i in [x0, x1) (1-based), full Y range
+    (kernel.py:165-172): zero-copy strided views of the padded fields."""
+    arrs = {"u": fields.u.data, "v": fields.v.data, "w": fields.w.data}
+    ny = fields.dims.ny
+    return {(f, dx, dy): arrs[f][x0 + dx:x1 + dx, 1 + dy:1 + dy + ny, :]
+            for f, dx, dy in COMPUTE_ROLES}
 
 
 # ---------------------------------------------------------------------------

@@ -15,7 +15,11 @@ inputs built with the reference's own generator (`fill_fields` /
 * tests/golden/small.npz — full padded input/output arrays of the small cases;
 * tests/golden/steps.json — digests of a composed time-stepping oracle built
   from the reference's `run_reference` + numpy `f + dt*s` + `wrap_halos`
-  (the reference has no time integration).
+  (the reference has no time integration, SPEC.md:188; SURVEY.md §8f1);
+* tests/golden/arrays.npz — the array-level API: the reference's
+  `compute_block` (kernel.py:139-162) on independent random role arrays and
+  on `grid_roles` views, and `su/sv/sw_formula` (kernel.py:73-112) on
+  broadcast scalar/array arguments, mid and top branches.
 
 The BASELINE.json value distributions are applied on top of
 the reference LCG: x*20.0-10.0 (numpy mul then sub), w=0 at k=0 and k=nz-1,
@@ -35,7 +39,8 @@ sys.path.insert(0, str(REF / "src"))
 from pwadvect.grid import (FieldSet, Field3D, GeneratorSpec, checksum,  # noqa: E402
                            fill_fields, lcg_doubles, make_grid, wrap_halos)
 from pwadvect.kernel import (COMPUTE_ROLES, AdvectionCoefficients,  # noqa: E402
-                             operation_census, reads_per_point, run_reference)
+                             compute_block, grid_roles, operation_census, reads_per_point,
+                             run_reference, su_formula, sv_formula, sw_formula)
 
 OUT = Path(__file__).resolve().parent
 
@@ -161,7 +166,41 @@ def main():
                           "fields": {"u": checksum(fields.u), "v": checksum(fields.v),
                                      "w": checksum(fields.w)}})
     (OUT / "steps.json").write_text(json.dumps({"cases": steps_out}, indent=1))
-    print(f"{len(cases)} cases, {len(small)} arrays, {len(steps_out)} stepping cases")
+
+    # 7. array-level API: compute_block on independent role arrays (leading
+    # shapes (2, 3), (5,), (0, 4)), on grid_roles views, and the formulas
+    arrays = {}
+    rng = np.random.default_rng(2010)
+    for n, (lead, nz) in enumerate((((2, 3), 9), ((5,), 2), ((3, 2), 3), ((0, 4), 4))):
+        roles = {r: rng.uniform(-10.0, 10.0, lead + (nz,)) for r in COMPUTE_ROLES}
+        co = AdvectionCoefficients(float(rng.uniform(0, 1)), float(rng.uniform(0, 1)),
+                                   rng.uniform(0, 1, nz), rng.uniform(0, 1, nz))
+        outs = compute_block(co, roles)
+        arrays[f"cb{n}/coeffs"] = np.concatenate([[co.tcx, co.tcy], co.tzc1, co.tzc2])
+        for m, r in enumerate(COMPUTE_ROLES):
+            arrays[f"cb{n}/role{m}"] = roles[r]
+        for name, o in zip(("su", "sv", "sw"), outs):
+            arrays[f"cb{n}/{name}"] = o
+    dims = make_grid(7, 6, 5)
+    fields = fill_fields(dims, GeneratorSpec.random(99))
+    co = AdvectionCoefficients(0.3, 0.7, rng.uniform(0, 1, 5), rng.uniform(0, 1, 5))
+    for name, o in zip(("su", "sv", "sw"), compute_block(co, grid_roles(fields, 2, 6))):
+        arrays[f"gr/{name}"] = o
+    arrays["gr/coeffs"] = np.concatenate([[co.tcx, co.tcy], co.tzc1, co.tzc2])
+    for which, fn in enumerate((su_formula, sv_formula, sw_formula)):
+        for top in (False, True):
+            args = [float(rng.uniform(0, 1)), float(rng.uniform(0, 1)), rng.uniform(0, 1, 5),
+                    float(rng.uniform(0, 1))]
+            args += [rng.uniform(-10, 10, (4, 5)) if m % 3 else rng.uniform(-10, 10, 5)
+                     for m in range(15)]
+            out = fn(*args, top=top)
+            key = f"f{which}{int(top)}"
+            for m, a in enumerate(args):
+                arrays[f"{key}/arg{m}"] = np.asarray(a, dtype=np.float64)
+            arrays[f"{key}/out"] = out
+    np.savez_compressed(OUT / "arrays.npz", **arrays)
+    print(f"{len(cases)} cases, {len(small)} arrays, {len(steps_out)} stepping cases, "
+          f"{len(arrays)} array-API arrays")
 
 
 if __name__ == "__main__":

@@ -60,3 +60,37 @@ def case_inputs(case):
     if gen["mode"] == "baseline":
         return oracle.fill_random(nx, ny, nz, gen["seed"], baseline=True)
     raise ValueError(gen)
+
+
+@lru_cache(maxsize=1)
+def array_api_fixtures():
+    """arrays.npz: the reference's compute_block / grid_roles / *_formula outputs."""
+    with np.load(GOLDEN / "arrays.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+def compute_block_cases():
+    z = array_api_fixtures()
+    out = []
+    n = 0
+    while f"cb{n}/coeffs" in z:
+        roles = [z[f"cb{n}/role{m}"] for m in range(17)]
+        nz = roles[0].shape[-1]
+        c = z[f"cb{n}/coeffs"]
+        out.append({"tcx": float(c[0]), "tcy": float(c[1]), "tzc1": c[2:2 + nz],
+                    "tzc2": c[2 + nz:], "roles": roles,
+                    "want": tuple(z[f"cb{n}/{k}"] for k in ("su", "sv", "sw"))})
+        n += 1
+    return out
+
+
+def formula_cases():
+    z = array_api_fixtures()
+    out = []
+    for which in range(3):
+        for top in (0, 1):
+            key = f"f{which}{top}"
+            args = [z[f"{key}/arg{m}"] for m in range(19)]
+            args = [float(a) if a.ndim == 0 else a for a in args]
+            out.append({"which": which, "top": bool(top), "args": args, "want": z[f"{key}/out"]})
+    return out

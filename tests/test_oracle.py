@@ -112,3 +112,35 @@ def test_lightcone_tile_equals_periodic_stepping(steps, i0, j0, ti, tj):
     jj = (np.arange(j0, j0 + tj) - 1) % g[1] + 1
     for got, full in zip(tile, (u, v, w)):
         assert np.array_equal(got.view(np.int64), full[np.ix_(ii, jj)].view(np.int64))
+
+
+def test_array_api_oracle_matches_reference_fixtures():
+    """compute_block / su,sv,sw_formula restated in numpy (oracle) == the
+    reference's own outputs (tests/golden/arrays.npz), bit for bit."""
+    from tests.golden_data import compute_block_cases, formula_cases
+    for c in compute_block_cases():
+        got = oracle.compute_block_numpy(c["tcx"], c["tcy"], c["tzc1"], c["tzc2"], c["roles"])
+        for g, w in zip(got, c["want"]):
+            assert g.shape == w.shape and np.array_equal(g.view(np.int64), w.view(np.int64))
+    for c in formula_cases():
+        got = np.asarray(oracle.formula_numpy(c["which"], c["args"], c["top"]))
+        assert np.array_equal(got.view(np.int64), c["want"].view(np.int64))
+
+
+def test_grid_roles_views_reproduce_reference_compute_block():
+    """grid_roles (kernel.py:165-172) are views of the padded fields; fed to
+    compute_block they give the reference's fixture for columns 2..5."""
+    import paper_2010_01545_b200 as pw
+    from paper_2010_01545_b200.stencil import COMPUTE_ROLES, grid_roles
+    from tests.golden_data import array_api_fixtures
+    z = array_api_fixtures()
+    d = pw.make_grid(7, 6, 5)
+    u, v, w = oracle.fill_random(7, 6, 5, 99)
+    f = pw.FieldSet(*(pw.Field3D(d, a) for a in (u, v, w)))
+    roles = grid_roles(f, 2, 6)
+    assert all(np.shares_memory(roles[r], {"u": u, "v": v, "w": w}[r[0]]) for r in COMPUTE_ROLES)
+    assert roles[("v", 1, -1)].shape == (4, 6, 5)
+    c = z["gr/coeffs"]
+    got = oracle.compute_block_numpy(c[0], c[1], c[2:7], c[7:], [roles[r] for r in COMPUTE_ROLES])
+    for g, name in zip(got, ("su", "sv", "sw")):
+        assert np.array_equal(g.view(np.int64), z[f"gr/{name}"].view(np.int64))

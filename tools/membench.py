@@ -5,7 +5,6 @@
 import ctypes
 import json
 import subprocess
-import sys
 from pathlib import Path
 
 import torch
