@@ -117,14 +117,16 @@ def plan_traffic(dims: GridDims, box, plan: dict) -> TrafficReport:
         # 27 distinct operands per point at k >= 1 (9 per field), via L1/L2
         tr.external_reads = 27 * nbx * nby * (nz - 1)
         return tr
-    tj, g, nch = plan["tile_j"], plan["grid"], plan.get("chunks", 1)
-    nstrips = plan["strips"]
+    tj, nch = plan["tile_j"], plan.get("chunks", 1)
+    nstrips, nlong = plan["strips"], plan.get("long_strips", 0)
     widths = [min(tj, nby - s * tj) for s in range(nstrips)]
-    planes = 0
-    for u in range(nstrips * nch):  # (chunk, strip) units, each streams its chunk + 2 planes
-        chunk, s = divmod(u, nstrips)
-        ib, ie = nbx * chunk // nch, nbx * (chunk + 1) // nch
-        planes += (ie - ib + 2) * (widths[s] + 2)
+    # work units (pwadv_advect.cu unit_at): strips 0..nlong-1 whole, the rest
+    # in nch X chunks; each unit streams its planes + one on each side
+    planes = sum((nbx + 2) * (widths[s] + 2) for s in range(nlong))
+    for s in range(nlong, nstrips):
+        for chunk in range(nch):
+            ib, ie = nbx * chunk // nch, nbx * (chunk + 1) // nch
+            planes += (ie - ib + 2) * (widths[s] + 2)
     tr.external_reads = 3 * nz * planes
     tr.local_writes = tr.external_reads
     # 9 paired shared loads per thread per plane step (2 points) = 9 per point

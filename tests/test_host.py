@@ -217,6 +217,16 @@ def test_plan_traffic_accounting():
     assert tr.external_writes == interior_in
     simple = plan_traffic(dims, (1, 513, 1, 513), {"kernel": "simple"})
     assert simple.external_reads == 27 * 512 * 512 * 63
+    # two-phase schedule (whole strips for the full rounds, the rest chunked):
+    # 2048^2 -> 148 whole strips + 23 strips in 6 chunks; closed form
+    d3 = pw.make_grid(2048, 2048, 64)
+    p3 = {"kernel": "xmarch", "tile_j": 12, "strips": 171, "long_strips": 148, "chunks": 6,
+          "smem_bytes": 0}
+    t3 = plan_traffic(d3, (1, 2049, 1, 2049), p3)
+    widths = [12] * 170 + [2048 - 170 * 12]
+    want = 2050 * sum(w + 2 for w in widths[:148])
+    want += sum((2048 * (c + 1) // 6 - 2048 * c // 6 + 2) * (w + 2) for w in widths[148:] for c in range(6))
+    assert t3.external_reads == 3 * 64 * want
 
 
 def test_cli_parser_and_schedule_names():
