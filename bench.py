@@ -256,6 +256,7 @@ def run_ours(args):
     co = device.DeviceCoefficients.from_host(pw.baseline_coefficients(SEED, nz), dev)
     out = device.alloc_fields(dims, dev)
 
+    step_path = None
     if ws == 1:
         if stepping:
             from paper_2010_01545_b200.stepper import Stepper
@@ -272,13 +273,26 @@ def run_ours(args):
         if stepping:
             # K4 with the exchange fused in: boundary values stored into the
             # neighbours' halos over NVLink (CUDA IPC), one NCCL barrier per step
-            st = decomp.PushStepper(dec, fields, co, 0.1, decomp.IpcPeerRegistry(dec),
-                                    decomp.NcclBarrier(dev), opts=opts,
-                                    initial_exchange=lambda f: exch.exchange(f, stream=stream))
-            st.step(1, stream=stream)
-
-            def one_step():
+            try:
+                st = decomp.PushStepper(dec, fields, co, 0.1, decomp.IpcPeerRegistry(dec),
+                                        decomp.NcclBarrier(dev), opts=opts,
+                                        initial_exchange=lambda f: exch.exchange(f, stream=stream))
                 st.step(1, stream=stream)
+                step_path = "K4 + peer stores (CUDA IPC) + NCCL barrier"
+
+                def one_step():
+                    st.step(1, stream=stream)
+            except _lib.PwadvError as exc:
+                # no CUDA IPC for these allocations (e.g. expandable segments):
+                # NCCL halo exchange overlapped with K4 on the interior
+                from paper_2010_01545_b200.stepper import Stepper
+                print(f"bench: fused peer-store step unavailable ({exc}); NCCL exchange step",
+                      file=sys.stderr)
+                st = Stepper(fields, co, 0.1, opts=opts, exchanger=exch)
+                step_path = "NCCL exchange overlapped with K4 (interior), then K4 rim"
+
+                def one_step():
+                    st._one(stream)
         else:
             def one_step():
                 exch.advect_overlapped(fields, co, out, opts=opts, stream=stream)
@@ -436,6 +450,7 @@ def run_ours(args):
             "config": {"workload": desc, "nx": nx, "ny": ny, "nz": nz,
                        "global_grid": f"{gx}x{gy}x{nz}", "points_per_gpu": pts_rank,
                        "decomposition": f"{px}x{py}", "variant": args.variant,
+                       **({"multi_gpu_step": step_path} if step_path else {}),
                        "bit_exact": not args.variant.endswith("_fma"),
                        "l2": f"inputs larger than L2 ({3 * dims.padded_len * 8 / 1e6:.0f} MB read per "
                              f"step vs 126 MB L2); no flush", "plan": plan},
