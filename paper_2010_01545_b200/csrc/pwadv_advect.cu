@@ -16,10 +16,17 @@
 //    the j+-1 neighbours from the shared plane. su, sv and sw are produced in
 //    the same pass, so each input byte crosses HBM about once and each output
 //    byte once (48 B per point). fp64 CUDA cores only: this is
-//    not a contraction, no tensor cores.
-//    Work distribution: (X chunk, strip) units dealt round-robin to a
-//    persistent grid of one CTA per SM (see Unit below); a CTA moving to its
-//    next unit just continues its plane sequence (the ring never drains).
+//    not a contraction, no tensor cores. 512 threads: three compute
+//    warpgroups and a producer warpgroup (one thread issues every refill when
+//    the stage's empty mbarrier completes; setmaxnreg moves its registers to
+//    the compute warps). For nz = 64 / 128 the tile layout is a template
+//    constant (immediate-offset shared loads). The x-direction operand sums
+//    are carried from plane to plane and three z-sums are shared by the
+//    k-pair: 57 fp64 operations per point for the reference's 63, same bits.
+//    Work distribution: whole strips for every full round of a persistent
+//    grid of one CTA per SM, the leftover strips in X chunks (see unit_at and
+//    plan_xmarch); a CTA moving to its next unit just continues its plane
+//    sequence (the ring never drains).
 //
 //  * k_advect_simple — one thread per output point, direct global loads. Used
 //    for shapes the X-march does not cover (odd nz, misaligned pointers, very
@@ -308,11 +315,12 @@ __device__ __forceinline__ void issue_plane(const RingState *rs, const BoxArgs &
 // the step body is instantiated for the three rotations and unrolled, with no
 // register moves.
 //
-// Ring protocol (no producer warp): each warp, once it has read everything it
-// needs from plane q, bumps released[q % S]; the warp that completes the count
-// resets it and immediately issues plane q+S into the freed stage. Refills
-// happen in sequence order (every warp releases q before q+1), and no single
-// warp paces the pipeline. Planes q+1 .. q+S-1 are resident or in flight
+// Ring protocol. MAXT == 512 (default): each compute warp, once it has read
+// everything it needs from plane q, arrives on empty[q % S]; the producer
+// thread waits for the stage's 12 arrivals and issues plane q+S into it.
+// Other thread budgets (no producer warp): each warp bumps released[q % S]
+// and the warp that completes the count issues the refill. Either way refills
+// happen in sequence order and planes q+1 .. q+S-1 are resident or in flight
 // when q is released.
 // resident CTAs per SM for a thread budget (each CTA keeps <= 168 registers)
 __host__ __device__ constexpr int ctas_per_sm(int maxt) { return maxt <= 128 ? 3 : (maxt <= 192 ? 2 : 1); }
