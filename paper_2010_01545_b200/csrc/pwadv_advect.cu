@@ -478,6 +478,23 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
         const int64_t j0 = a.y0 + wu.strip * TJ;
         const int64_t tjs = (a.y1 - j0) < TJ ? (a.y1 - j0) : TJ;
         const bool active = in_tile && c < tjs;
+        // fused step with the halo push: a thread on the y = 1 or y = ny face
+        // stores its pair into one neighbour's halo column every plane — a
+        // fixed target, resolved here once per unit (the x faces, corners and
+        // the ny == 1 case take the general out-of-line path below)
+        int ydir = -1;
+        int64_t ypj = 0, ystr = 0;
+        if constexpr (STEP) {
+            if (a.push && active && a.ny > 1) {
+                if (j0 + c == 1) {
+                    ydir = PWADV_NB_YM;
+                    ypj = a.peers.ny[PWADV_NB_YM] + 1;
+                } else if (j0 + c == a.ny) {
+                    ydir = PWADV_NB_YP;
+                }
+                if (ydir >= 0) ystr = a.peers.ny[ydir] + 2;
+            }
+        }
 
         // plane ib-1 -> slot 2 (the x-1 window of the first step)
         {
@@ -605,9 +622,17 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
                 store2(o2, sw_a, sw_b);
             }
             if constexpr (STEP) {
-                if (a.push && active &&
-                    (ci == 1 || ci == a.nx || j0 + c == 1 || j0 + c == a.ny))
-                    push_pair(&a, ci, j0 + c, k0, su_a, su_b, sv_a, sv_b, sw_a, sw_b);
+                if (a.push && active) {
+                    if (ci == 1 || ci == a.nx || a.ny == 1) {
+                        if (ci == 1 || ci == a.nx || j0 + c == 1 || j0 + c == a.ny)
+                            push_pair(&a, ci, j0 + c, k0, su_a, su_b, sv_a, sv_b, sw_a, sw_b);
+                    } else if (ydir >= 0) {
+                        const int64_t off = (ci * ystr + ypj) * (int64_t)nz + k0;
+                        store2(a.peers.u[ydir] + off, su_a, su_b);
+                        store2(a.peers.v[ydir] + off, sv_a, sv_b);
+                        store2(a.peers.w[ydir] + off, sw_a, sw_b);
+                    }
+                }
             }
             ++ci;
             o0 += ostep;
