@@ -36,7 +36,9 @@
 #include "pwadv_device.cuh"
 #include "pwadv_internal.h"
 
+#include <mutex>
 #include <type_traits>
+#include <vector>
 
 namespace pwadv {
 
@@ -665,6 +667,35 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
 
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+// and size: it costs a driver call per launch otherwise (host overhead that
+// shows at small per-GPU blocks).
+static cudaError_t ensure_smem_attr(const void *kern, int device, int bytes)
+{
+    struct Entry {
+        const void *kern;
+        int device, bytes;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> done;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (const Entry &x : done)
+            if (x.kern == kern && x.device == device && x.bytes >= bytes) return cudaSuccess;
+    }
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(mu);
+        for (Entry &x : done)
+            if (x.kern == kern && x.device == device) {
+                if (bytes > x.bytes) x.bytes = bytes;
+                return e;
+            }
+        done.push_back({kern, device, bytes});
+    }
+    return e;
+}
+
 int launch_box(const BoxLaunch &L, cudaStream_t stream)
 {
     BoxArgs a;
@@ -761,8 +792,7 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         PWADV_PICK(128, true)
 #undef PWADV_PICK
         if (!kern) return set_error(PWADV_E_ARG, "unsupported thread budget %d", plan.maxt);
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)plan.smem);
+        cudaError_t e = ensure_smem_attr((const void *)kern, dev->device, (int)plan.smem);
         if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute", e);
         kern<<<plan.grid, plan.threads, plan.smem, stream>>>(a, t);
     } else {

@@ -161,6 +161,39 @@ def step(u, v, w, coeffs, dt: float, out, *, box=None, opts: _lib.Opts | None = 
     return out
 
 
+class BoundLaunch:
+    """A K1 (advect) or K4 (dt given: step) launch on one box with every
+    argument validated and converted once; calling it costs one ctypes call.
+    For loops that launch the same box on the same buffers many times (the
+    multi-GPU interior / rim launches), where per-call Python overhead would
+    otherwise exceed the kernel time of a small per-GPU block."""
+
+    def __init__(self, fields, coeffs, out, *, box=None, opts: _lib.Opts | None = None,
+                 dt: float | None = None):
+        u, v, w = fields
+        dims = dims_of(u)
+        for t, n in zip(tuple(fields) + tuple(out), ("u", "v", "w", "o0", "o1", "o2")):
+            _check_field(t, dims, n)
+        dc = _as_device_coeffs(coeffs, u.device)
+        if dc.nz != dims.nz:
+            raise ValueError(f"coefficient length {dc.nz} != nz {dims.nz}")
+        x0, x1, y0, y1 = _box(dims, box)
+        self._keep = (tuple(fields), tuple(out), dc, opts)
+        self.device = u.device
+        L = _lib.lib()
+        head = [_p(u), _p(v), _p(w), _p(out[0]), _p(out[1]), _p(out[2]), dims.nx, dims.ny,
+                dims.nz, dc.tcx, dc.tcy, _p(dc.tz[0]), _p(dc.tz[1])]
+        if dt is None:
+            self._fn = L.pwadv_advect_box_f64
+            self._args = head + [x0, x1, y0, y1, _lib.opts_ptr(opts)]
+        else:
+            self._fn = L.pwadv_step_box_f64
+            self._args = head + [float(dt), x0, x1, y0, y1, _lib.opts_ptr(opts)]
+
+    def __call__(self, stream=None) -> None:
+        _lib.check(self._fn(*self._args, _stream_handle(stream, self.device)))
+
+
 def wrap_halos(*fields, stream=None) -> None:
     """K2: periodic halo wrap in place (reference grid.py:203-208)."""
     if not fields:
