@@ -230,6 +230,16 @@ int pwadv_pack_xface3_f64(const double *u, const double *v, const double *w, dou
                           int64_t nx, int64_t ny, int64_t nz, int64_t i, void *stream);
 int pwadv_unpack_xface3_f64(double *u, double *v, double *w, const double *buf,
                             int64_t nx, int64_t ny, int64_t nz, int64_t i, void *stream);
+/* Both faces of one axis in one launch (the exchange's per-axis step):
+ * pack: interior face 1 -> buf_lo, face n -> buf_hi (n = nx for axis 0,
+ * ny for axis 1; buffers as above); unpack: buf_lo -> halo 0, buf_hi ->
+ * halo n+1. */
+int pwadv_pack_faces3_f64(const double *u, const double *v, const double *w, double *buf_lo,
+                          double *buf_hi, int64_t nx, int64_t ny, int64_t nz, int32_t axis,
+                          void *stream);
+int pwadv_unpack_faces3_f64(double *u, double *v, double *w, const double *buf_lo,
+                            const double *buf_hi, int64_t nx, int64_t ny, int64_t nz, int32_t axis,
+                            void *stream);
 /* Local periodic copy of one axis (an undivided axis of the decomposition):
  * axis 0 = X faces (planes), axis 1 = Y faces (columns, all i incl. halos). */
 int pwadv_wrap_axis3_f64(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,

@@ -89,6 +89,8 @@ SIGNATURES = {
                                                            ctypes.c_uint32, _P]),
     "pwadv_formula_f64": (ctypes.c_int, [ctypes.c_int32, _P, _P, _I64, ctypes.c_int32, _P,
                                          ctypes.c_uint32, _P]),
+    "pwadv_pack_faces3_f64": (ctypes.c_int, [_P] * 5 + [_I64] * 3 + [ctypes.c_int32, _P]),
+    "pwadv_unpack_faces3_f64": (ctypes.c_int, [_P] * 5 + [_I64] * 3 + [ctypes.c_int32, _P]),
     "pwadv_wrap_halos_f64": (ctypes.c_int, [_P, _I64, _I64, _I64, _P]),
     "pwadv_wrap_halos3_f64": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, _P]),
     "pwadv_wrap_axis3_f64": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, ctypes.c_int32, _P]),

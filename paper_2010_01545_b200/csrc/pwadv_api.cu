@@ -434,6 +434,32 @@ int pwadv_unpack_xface3_f64(double *u, double *v, double *w, const double *buf, 
     return face(u, v, w, const_cast<double *>(buf), nx, ny, nz, 0, i, false, stream);
 }
 
+int pwadv_pack_faces3_f64(const double *u, const double *v, const double *w, double *buf_lo,
+                          double *buf_hi, int64_t nx, int64_t ny, int64_t nz, int32_t axis,
+                          void *stream)
+{
+    int rc = check_dims(nx, ny, nz);
+    if (rc) return rc;
+    if ((rc = check_ptrs({u, v, w, buf_lo, buf_hi}))) return rc;
+    if (axis != 0 && axis != 1) return set_error(PWADV_E_ARG, "axis must be 0 or 1");
+    const int64_t n = axis == 0 ? nx : ny;
+    return launch_faces3(const_cast<double *>(u), const_cast<double *>(v), const_cast<double *>(w),
+                         buf_lo, buf_hi, nx, ny, nz, axis, 1, n, true, (cudaStream_t)stream);
+}
+
+int pwadv_unpack_faces3_f64(double *u, double *v, double *w, const double *buf_lo,
+                            const double *buf_hi, int64_t nx, int64_t ny, int64_t nz, int32_t axis,
+                            void *stream)
+{
+    int rc = check_dims(nx, ny, nz);
+    if (rc) return rc;
+    if ((rc = check_ptrs({u, v, w, buf_lo, buf_hi}))) return rc;
+    if (axis != 0 && axis != 1) return set_error(PWADV_E_ARG, "axis must be 0 or 1");
+    const int64_t n = axis == 0 ? nx : ny;
+    return launch_faces3(u, v, w, const_cast<double *>(buf_lo), const_cast<double *>(buf_hi), nx, ny,
+                         nz, axis, 0, n + 1, false, (cudaStream_t)stream);
+}
+
 // ---------------------------------------------------------------------------
 // Automatic X-slab chunk count for the host-buffer path (measured on B200,
 // tools/e2e_sweep.py, tools/pcie.py): a single synchronous call needs ~16

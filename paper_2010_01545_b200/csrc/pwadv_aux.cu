@@ -118,6 +118,37 @@ __global__ void k_face3(double *f0, double *f1, double *f2, double *buf, int64_t
     }
 }
 
+// Both faces of an axis in one launch: buffer a <-> index ia, buffer b <-> index ib.
+__global__ void k_faces3(double *f0, double *f1, double *f2, double *buf_a, double *buf_b,
+                         int64_t nx, int64_t ny, int64_t nz, int axis, int64_t ia, int64_t ib,
+                         int pack)
+{
+    const int64_t ny2 = ny + 2;
+    const int64_t per = axis == 0 ? ny2 * nz : (nx + 2) * nz;
+    const int64_t total = 6 * per;
+    double *fs[3] = {f0, f1, f2};
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const bool second = idx >= 3 * per;
+        const int64_t r = second ? idx - 3 * per : idx;
+        const int m = (int)(r / per);
+        const int64_t e = r - m * per;
+        const int64_t index = second ? ib : ia;
+        int64_t off;
+        if (axis == 0) {
+            off = index * ny2 * nz + e;
+        } else {
+            const int64_t i = e / nz, k = e % nz;
+            off = (i * ny2 + index) * nz + k;
+        }
+        double *buf = second ? buf_b : buf_a;
+        if (pack)
+            buf[r] = fs[m][off];
+        else
+            fs[m][off] = buf[r];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K5
 
@@ -231,6 +262,15 @@ int launch_face3(double *u, double *v, double *w, double *buf, int64_t nx, int64
     k_face3<<<grid_for(3 * per, 256), 256, 0, s>>>(u, v, w, buf, nx, ny, nz, axis, index,
                                                    pack ? 1 : 0);
     return check_launch(pack ? "pack_face" : "unpack_face");
+}
+
+int launch_faces3(double *u, double *v, double *w, double *buf_a, double *buf_b, int64_t nx,
+                  int64_t ny, int64_t nz, int axis, int64_t ia, int64_t ib, bool pack, cudaStream_t s)
+{
+    const int64_t per = axis == 0 ? (ny + 2) * nz : (nx + 2) * nz;
+    k_faces3<<<grid_for(6 * per, 256), 256, 0, s>>>(u, v, w, buf_a, buf_b, nx, ny, nz, axis, ia, ib,
+                                                    pack ? 1 : 0);
+    return check_launch(pack ? "pack_faces" : "unpack_faces");
 }
 
 int launch_fill(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz, int mode,

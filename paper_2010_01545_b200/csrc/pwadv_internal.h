@@ -63,6 +63,8 @@ int launch_fill(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t
 int launch_fill_box(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
                     int64_t gnx, int64_t gny, int64_t x_off, int64_t y_off, int mode, uint64_t seed,
                     double a, double b, double c, cudaStream_t s);
+int launch_faces3(double *u, double *v, double *w, double *buf_a, double *buf_b, int64_t nx,
+                  int64_t ny, int64_t nz, int axis, int64_t ia, int64_t ib, bool pack, cudaStream_t s);
 int launch_face3(double *u, double *v, double *w, double *buf, int64_t nx, int64_t ny,
                  int64_t nz, int axis, int64_t index, bool pack, cudaStream_t s);
 

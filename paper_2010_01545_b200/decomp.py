@@ -146,6 +146,16 @@ class TorchFaceOps:
             dst = f[index] if axis == 0 else f[:, index]
             dst.copy_(buf[m].view_as(dst))
 
+    @classmethod
+    def pack2(cls, fields, buf_lo, buf_hi, axis: int, n: int, stream=None) -> None:
+        cls.pack(fields, buf_lo, axis, 1, stream)
+        cls.pack(fields, buf_hi, axis, n, stream)
+
+    @classmethod
+    def unpack2(cls, fields, buf_lo, buf_hi, axis: int, n: int, stream=None) -> None:
+        cls.unpack(fields, buf_hi, axis, n + 1, stream)
+        cls.unpack(fields, buf_lo, axis, 0, stream)
+
     @staticmethod
     def wrap_axis(fields, axis: int, stream=None) -> None:
         for f in fields:
@@ -177,6 +187,24 @@ class CudaFaceOps:
     def unpack(cls, fields, buf, axis, index, stream=None):
         cls._call("pwadv_unpack_xface3_f64" if axis == 0 else "pwadv_unpack_yface3_f64",
                   fields, buf, axis, index, stream)
+
+    @staticmethod
+    def _call2(name, fields, buf_lo, buf_hi, axis, stream):
+        from . import _lib, device as dv
+        d = dv.dims_of(fields[0])
+        _lib.check(getattr(_lib.lib(), name)(
+            dv._p(fields[0]), dv._p(fields[1]), dv._p(fields[2]), dv._p(buf_lo), dv._p(buf_hi),
+            d.nx, d.ny, d.nz, int(axis), dv._stream_handle(stream, fields[0].device)))
+
+    @classmethod
+    def pack2(cls, fields, buf_lo, buf_hi, axis, n, stream=None):
+        """faces 1 and n of `axis` in one launch (pwadv_pack_faces3_f64)."""
+        cls._call2("pwadv_pack_faces3_f64", fields, buf_lo, buf_hi, axis, stream)
+
+    @classmethod
+    def unpack2(cls, fields, buf_lo, buf_hi, axis, n, stream=None):
+        """halos 0 and n+1 of `axis` in one launch (pwadv_unpack_faces3_f64)."""
+        cls._call2("pwadv_unpack_faces3_f64", fields, buf_lo, buf_hi, axis, stream)
 
     @staticmethod
     def wrap_axis(fields, axis, stream=None):
@@ -321,8 +349,7 @@ class HaloExchanger:
         if p == 1:
             self.faceops.wrap_axis(fields, axis, stream)
             return []
-        self.faceops.pack(fields, b["send_m"], axis, 1, stream)
-        self.faceops.pack(fields, b["send_p"], axis, n, stream)
+        self.faceops.pack2(fields, b["send_m"], b["send_p"], axis, n, stream)
         # order matters when both neighbours are one rank (p == 2): the peer
         # receives my first message into its plus-side halo
         return [("send", b["send_m"], m, 0), ("send", b["send_p"], pl, 1),
@@ -332,8 +359,7 @@ class HaloExchanger:
         p, n, _, _, b = self._axis(axis)
         if p == 1:
             return
-        self.faceops.unpack(fields, b["recv_p"], axis, n + 1, stream)
-        self.faceops.unpack(fields, b["recv_m"], axis, 0, stream)
+        self.faceops.unpack2(fields, b["recv_m"], b["recv_p"], axis, n, stream)
 
     def exchange(self, fields, stream=None) -> None:
         """Refresh the halos of `fields` (X phase, then Y phase)."""

@@ -130,3 +130,26 @@ def test_emulated_fused_push_stepping(px, py, shape):
     for dec, final in run_ranks(n, rank):
         for f, w in zip(final, want):
             assert torch.equal(f.view(torch.int64), dec.local_view(w).contiguous().view(torch.int64)), dec.rank
+
+
+@pytest.mark.parametrize("axis", [0, 1])
+def test_cuda_face_ops_match_tensor_slicing(axis):
+    """pwadv_pack/unpack_faces3_f64 (both faces of an axis in one launch) ==
+    the tensor-slicing reference implementation, bitwise."""
+    from paper_2010_01545_b200.decomp import CudaFaceOps, TorchFaceOps
+    d = pw.make_grid(7, 5, 6)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = [torch.randn(d.padded_shape, dtype=torch.float64, device="cuda", generator=g) for _ in range(3)]
+    b = [t.clone() for t in a]
+    n = d.nx if axis == 0 else d.ny
+    face = (d.ny + 2) * d.nz if axis == 0 else (d.nx + 2) * d.nz
+    bufs = [torch.empty((3, face), dtype=torch.float64, device="cuda") for _ in range(4)]
+    CudaFaceOps.pack2(a, bufs[0], bufs[1], axis, n)
+    TorchFaceOps.pack2(b, bufs[2], bufs[3], axis, n)
+    torch.cuda.synchronize()
+    assert torch.equal(bufs[0], bufs[2]) and torch.equal(bufs[1], bufs[3])
+    src_lo, src_hi = bufs[0] * 2.0, bufs[1] - 1.0
+    CudaFaceOps.unpack2(a, src_lo, src_hi, axis, n)
+    TorchFaceOps.unpack2(b, src_lo, src_hi, axis, n)
+    torch.cuda.synchronize()
+    assert all(torch.equal(x, y) for x, y in zip(a, b))
