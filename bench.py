@@ -381,6 +381,28 @@ def run_ours(args):
                   "normwise_rel_err": cmp["normwise_rel"], "tolerance": "bit-exact (default build); "
                   "normwise max|d|/max|ref| <= 1e-12 for _fma variants",
                   "checked": "planes 1-2 and nx-1..nx (all levels, all columns) vs oracle"}
+    elif rank == 0 and ws == 1 and stepping:
+        # one more forward step from the stepped state: the halos wrapped, K4
+        # on the device, the composed oracle (advect + f + dt*s) on X slabs
+        from oracle import oracle  # checker only
+        cur = st.a
+        device.wrap_halos(*cur, stream=stream)
+        device.step(*cur, co, 0.1, out, opts=opts, stream=stream)
+        torch.cuda.synchronize()
+        tz = (co.tz[0].cpu().numpy(), co.tz[1].cpu().numpy())
+        got_all, want_all = [], []
+        for x0, x1 in ((1, 3), (dims.nx - 1, dims.nx + 1)):
+            ins = [np.ascontiguousarray(f[x0 - 1:x1 + 1].cpu().numpy()) for f in cur]
+            oracle.step_open(*ins, co.tcx, co.tcy, *tz, 0.1, 1, engines=oracle.host_threads())
+            got_all += [o[x0:x1, 1:-1].cpu().numpy() for o in out]
+            want_all += [a[1:-1, 1:-1] for a in ins]
+        cmp = oracle.compare(got_all, want_all)
+        parity = {"bitwise_equal_slabs": cmp["bitwise_equal"], "max_ulp_diff": cmp["max_ulp_diff"],
+                  "normwise_rel_err": cmp["normwise_rel"],
+                  "tolerance": "bit-exact (default build)",
+                  "checked": "one step from the stepped state, planes 1-2 and nx-1..nx (interior "
+                             "columns, all levels) vs the composed oracle; full-size light-cone "
+                             "checks in tests/test_gpu_c4.py"}
 
     clocks = sampler.stop() if sampler else None
 
