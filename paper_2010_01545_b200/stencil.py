@@ -255,7 +255,13 @@ def _context(dims: GridDims):
         if ctx is None:
             ctx = HostContext(GridDims(dims.nx, dims.ny, dims.nz), dev)
             _CTX_CACHE[key] = ctx
-            while len(_CTX_CACHE) > _CTX_MAX:
+            # at most _CTX_MAX shapes, and their device buffers (6 padded
+            # fields each) within a quarter of the device memory
+            budget = torch.cuda.get_device_properties(dev).total_memory // 4
+
+            def held():
+                return sum(6 * 8 * (k[1] + 2) * (k[2] + 2) * k[3] for k in _CTX_CACHE)
+            while len(_CTX_CACHE) > 1 and (len(_CTX_CACHE) > _CTX_MAX or held() > budget):
                 _, old = _CTX_CACHE.popitem(last=False)
                 old.close()
         else:
