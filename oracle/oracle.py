@@ -158,6 +158,11 @@ def advect_into(u, v, w, su, sv, sw, tcx, tcy, tzc1, tzc2, engines: int = 1) -> 
 
 def advect_numpy(u, v, w, tcx, tcy, tzc1, tzc2):
     """Vectorised numpy transcription of compute_block/run_reference (kernel.py:139-185)."""
+    with np.errstate(invalid="ignore", over="ignore"):  # non-finite inputs propagate, as numpy's
+        return _advect_numpy(u, v, w, tcx, tcy, tzc1, tzc2)
+
+
+def _advect_numpy(u, v, w, tcx, tcy, tzc1, tzc2):
     nx, ny, nz = u.shape[0] - 2, u.shape[1] - 2, u.shape[2]
     tzc1 = np.asarray(tzc1, dtype=np.float64)
     tzc2 = np.asarray(tzc2, dtype=np.float64)

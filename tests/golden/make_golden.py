@@ -140,6 +140,19 @@ def main():
         add(f"baseline_{nx}x{ny}x{nz}_s{seed}", dims, {"mode": "baseline", "seed": seed},
             fields, coeffs, keep, {"tzd1": hexs(tzd1), "tzd2": hexs(tzd2)})
 
+    # 5b. non-finite inputs: a NaN with a payload and +-Inf propagate through
+    # the formulas exactly as numpy evaluates them (payloads included)
+    dims = make_grid(8, 7, 6)
+    fields = baseline_fields(dims, 3)
+    fields.u.data[3, 3, 2] = np.nan
+    fields.u.data[5, 5, 1] = np.frombuffer(np.uint64(0x7FF8000000000123).tobytes(), np.float64)[0]
+    fields.v.data[4, 2, 3] = np.inf
+    fields.w.data[2, 5, 4] = -np.inf
+    for f in (fields.u, fields.v, fields.w):
+        wrap_halos(f.data)
+    coeffs, _, _ = baseline_coeffs(3, 6)
+    add("nonfinite_8x7x6", dims, {"mode": "nonfinite"}, fields, coeffs, True)
+
     (OUT / "cases.json").write_text(json.dumps({
         "generated_by": "tests/golden/make_golden.py (imports reference pwadvect 0.1.0)",
         "reference_goldens_json": goldens,

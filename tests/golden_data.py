@@ -49,7 +49,7 @@ def case_inputs(case):
     from oracle import oracle
     nx, ny, nz = case["nx"], case["ny"], case["nz"]
     gen = case["generator"]
-    if case["arrays"] and gen["mode"] in ("trig",):
+    if case["arrays"] and gen["mode"] in ("trig", "nonfinite"):
         arrs = small_arrays()
         return tuple(arrs[f"{case['name']}/{k}"].copy() for k in "uvw")
     if gen["mode"] == "uniform":
