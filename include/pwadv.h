@@ -255,6 +255,8 @@ int pwadv_wrap_axis3_f64(double *u, double *v, double *w, int64_t nx, int64_t ny
  * chunks <= 0 picks the count automatically (1 for fields under 32 MiB, else 16;
  * for pwadv_ctx_submit_host about 64 MiB per field and chunk, at most 16).
  */
+/* A context serves one call at a time (its device buffers and streams are
+ * shared by its calls); use one context per host thread for concurrency. */
 typedef struct pwadv_ctx pwadv_ctx;
 int pwadv_ctx_create(pwadv_ctx **out, int device, int64_t nx, int64_t ny, int64_t nz);
 int pwadv_ctx_destroy(pwadv_ctx *ctx);

@@ -242,8 +242,12 @@ class HostContext:
     """pwadv_ctx: device buffers + 3 streams for host-buffer (end-to-end) calls."""
 
     def __init__(self, dims: GridDims, device: int = 0):
+        import threading
         self.dims = dims
         self.device = int(device)
+        # a pwadv_ctx takes one call at a time (its buffers and streams are
+        # shared); concurrent callers of one context are serialised here
+        self.lock = threading.RLock()
         h = ctypes.c_void_p()
         _lib.check(_lib.lib().pwadv_ctx_create(ctypes.byref(h), self.device, dims.nx, dims.ny,
                                                dims.nz))
@@ -282,12 +286,13 @@ class HostContext:
         tz2 = np.ascontiguousarray(tzc2, dtype=np.float64)
         if tz1.shape != (d.nz,) or tz2.shape != (d.nz,):
             raise ValueError(f"coefficient length {tz1.shape} != nz {d.nz}")
-        _lib.check(_lib.lib().pwadv_ctx_advect_host(
-            self._h, self._hp(u), self._hp(v), self._hp(w), self._hp(su), self._hp(sv),
-            self._hp(sw), float(tcx), float(tcy), ctypes.c_void_p(tz1.ctypes.data),
-            ctypes.c_void_p(tz2.ctypes.data), int(chunks), _lib.opts_ptr(opts)))
-        a, b = ctypes.c_uint64(), ctypes.c_uint64()
-        _lib.check(_lib.lib().pwadv_ctx_last_bytes(self._h, ctypes.byref(a), ctypes.byref(b)))
+        with self.lock:
+            _lib.check(_lib.lib().pwadv_ctx_advect_host(
+                self._h, self._hp(u), self._hp(v), self._hp(w), self._hp(su), self._hp(sv),
+                self._hp(sw), float(tcx), float(tcy), ctypes.c_void_p(tz1.ctypes.data),
+                ctypes.c_void_p(tz2.ctypes.data), int(chunks), _lib.opts_ptr(opts)))
+            a, b = ctypes.c_uint64(), ctypes.c_uint64()
+            _lib.check(_lib.lib().pwadv_ctx_last_bytes(self._h, ctypes.byref(a), ctypes.byref(b)))
         return int(a.value), int(b.value)
 
     def submit_host(self, u, v, w, su, sv, sw, tcx, tcy, tzc1, tzc2, chunks: int = 0,
@@ -300,14 +305,16 @@ class HostContext:
         tz2 = np.ascontiguousarray(tzc2, dtype=np.float64)
         if tz1.shape != (d.nz,) or tz2.shape != (d.nz,):
             raise ValueError(f"coefficient length {tz1.shape} != nz {d.nz}")
-        self._keep = (tz1, tz2)  # the coefficient upload is asynchronous
-        _lib.check(_lib.lib().pwadv_ctx_submit_host(
-            self._h, self._hp(u), self._hp(v), self._hp(w), self._hp(su), self._hp(sv),
-            self._hp(sw), float(tcx), float(tcy), ctypes.c_void_p(tz1.ctypes.data),
-            ctypes.c_void_p(tz2.ctypes.data), int(chunks), _lib.opts_ptr(opts)))
-        a, b = ctypes.c_uint64(), ctypes.c_uint64()
-        _lib.check(_lib.lib().pwadv_ctx_last_bytes(self._h, ctypes.byref(a), ctypes.byref(b)))
+        with self.lock:
+            self._keep = (tz1, tz2)  # the coefficient upload is asynchronous
+            _lib.check(_lib.lib().pwadv_ctx_submit_host(
+                self._h, self._hp(u), self._hp(v), self._hp(w), self._hp(su), self._hp(sv),
+                self._hp(sw), float(tcx), float(tcy), ctypes.c_void_p(tz1.ctypes.data),
+                ctypes.c_void_p(tz2.ctypes.data), int(chunks), _lib.opts_ptr(opts)))
+            a, b = ctypes.c_uint64(), ctypes.c_uint64()
+            _lib.check(_lib.lib().pwadv_ctx_last_bytes(self._h, ctypes.byref(a), ctypes.byref(b)))
         return int(a.value), int(b.value)
 
     def sync(self) -> None:
-        _lib.check(_lib.lib().pwadv_ctx_sync(self._h))
+        with self.lock:
+            _lib.check(_lib.lib().pwadv_ctx_sync(self._h))

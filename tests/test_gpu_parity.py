@@ -559,3 +559,30 @@ def test_compute_block_random_and_grid_roles_equal_run_reference():
         assert np.array_equal(b[..., 1:].view(np.int64), s.data[1:-1, 1:-1, 1:].view(np.int64))
     with pytest.raises(ValueError):
         pwkernel.compute_block(pw.default_coefficients(5), pwkernel.grid_roles(f, 1, 10))
+
+
+def test_concurrent_drop_in_calls_same_shape():
+    """run_reference from several host threads on one grid shape (one cached
+    context, serialised per call): every result bit-exact."""
+    import threading
+    dims = pw.make_grid(40, 36, 64)
+    errs, ok = [], {}
+
+    def work(seed):
+        try:
+            u, v, w = oracle.fill_random(40, 36, 64, seed, baseline=True)
+            co = pw.baseline_coefficients(seed, 64)
+            fs = pw.FieldSet(*(pw.Field3D(dims, a) for a in (u, v, w)))
+            for _ in range(3):
+                src = pw.run_reference(fs, co)
+            want = oracle.advect(u, v, w, co.tcx, co.tcy, co.tzc1, co.tzc2)
+            ok[seed] = oracle.compare((src.su.data, src.sv.data, src.sw.data), want)["bitwise_equal"]
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+    ts = [threading.Thread(target=work, args=(s,)) for s in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    assert ok == {s: True for s in range(6)}
