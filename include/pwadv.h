@@ -57,6 +57,7 @@ enum {
 #define PWADV_FLAG_RIM 16u          /* only the one-cell rim of the box (one launch; multi-GPU overlap) */
 #define PWADV_FLAG_GENERIC 32u      /* X-march with a run-time tile layout even for nz = 64 / 128 */
 #define PWADV_FLAG_L2_UNIT_HEAD 64u /* X-march: load each work unit's first two planes L2 evict_last */
+#define PWADV_FLAG_NO_PDL 128u      /* X-march: ordinary launch (default: programmatic dependent launch) */
 /* ablation switches for profiling only (results are NOT the PW sources):
  * skip the PW arithmetic / skip the output stores of the X-march kernel
  * (they select the run-time-layout X-march, as PWADV_FLAG_GENERIC) */

@@ -38,6 +38,7 @@ FLAG_SIMPLE = 2
 FLAG_RIM = 16
 FLAG_GENERIC = 32
 FLAG_L2_UNIT_HEAD = 64
+FLAG_NO_PDL = 128
 
 
 class Opts(ctypes.Structure):

@@ -336,6 +336,12 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     static_assert(NZC == 0 || (MAXT == 512 && 384 % (NZC / 2) == 0), "compile-time layout: WS only");
+    // programmatic dependent launch (launch_box): wait until the previous grid
+    // on the stream has completed and its writes are visible (they may be our
+    // inputs) before any global access, and let the next grid be scheduled
+    // as our CTAs retire. No-ops for an ordinary launch.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int S = t.stages;
     const int TJ = NZC ? 384 / (NZC / 2) : t.tj;
     const int KP = NZC ? NZC / 2 : t.kp;
@@ -794,7 +800,24 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         if (!kern) return set_error(PWADV_E_ARG, "unsupported thread budget %d", plan.maxt);
         cudaError_t e = ensure_smem_attr((const void *)kern, dev->device, (int)plan.smem);
         if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute", e);
-        kern<<<plan.grid, plan.threads, plan.smem, stream>>>(a, t);
+        if (L.flags & PWADV_FLAG_NO_PDL) {
+            kern<<<plan.grid, plan.threads, plan.smem, stream>>>(a, t);
+        } else {
+            // back-to-back launches overlap the next grid's launch with this
+            // grid's tail (the kernel waits on griddepcontrol before reading)
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)plan.grid);
+            cfg.blockDim = dim3((unsigned)plan.threads);
+            cfg.dynamicSmemBytes = plan.smem;
+            cfg.stream = stream;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            e = cudaLaunchKernelEx(&cfg, kern, a, t);
+            if (e != cudaSuccess) return set_cuda_error("advect launch", e);
+        }
     } else {
         const int64_t total = (a.rim ? 2 * nby + 2 * (nbx - 2) : nbx * nby) * L.nz;
         int64_t blocks = (total + 255) / 256;
