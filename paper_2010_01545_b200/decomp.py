@@ -335,6 +335,7 @@ class HaloExchanger:
         self.xbuf = {k: buf(xf) for k in ("send_m", "send_p", "recv_m", "recv_p")}
         self.ybuf = {k: buf(yf) for k in ("send_m", "send_p", "recv_m", "recv_p")}
         self._side = torch.cuda.Stream(device=dev) if dev.type == "cuda" else None
+        self._launch_cache: dict = {}
 
     # phase pieces (shared by the real transports and the loopback emulation)
     def _axis(self, axis):
@@ -393,7 +394,7 @@ class HaloExchanger:
         key = (tuple(t.data_ptr() for t in tuple(fields) + tuple(out)), id(coeffs),
                None if opts is None else (opts.flags, opts.tile_j, opts.stages, opts.grid,
                                           opts.max_threads, opts.chunks), dt)
-        cache = self.__dict__.setdefault("_launch_cache", {})
+        cache = self._launch_cache
         hit = cache.get(key)
         if hit is not None and hit[2] is coeffs:
             return hit[0], hit[1]
