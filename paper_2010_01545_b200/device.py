@@ -19,7 +19,7 @@ from . import _lib
 from .layout import GeneratorSpec, GridDims, GridError, make_grid
 
 __all__ = ["DeviceCoefficients", "make_opts", "advect", "step", "wrap_halos", "fill",
-           "describe_plan", "HostContext", "dims_of", "alloc_fields"]
+           "describe_plan", "HostContext", "BoundLaunch", "dims_of", "alloc_fields"]
 
 
 def _stream_handle(stream, device) -> ctypes.c_void_p:
