@@ -876,7 +876,11 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
         const size_t stage_bytes = (size_t)3 * (tj + 2) * nz * sizeof(double);
         int smax = (int)(smem_cap / stage_bytes);
         if (smax > 16) smax = 16;  // RingState::released
-        stages = L.stages > 0 ? (L.stages < smax ? L.stages : smax) : (smax < 5 ? smax : 5);  // 5 measured best (tools/sweep.py)
+        // default ring depth measured with interleaved sweeps (tools/sweep.py
+        // --rounds): 6 for the warp-specialised kernel (C1 sustained 124.7 vs
+        // 121.0 Gpts/s at 5, C3 / C4 level), 5 for the other thread budgets
+        const int sdef = maxt == 512 ? 6 : 5;
+        stages = L.stages > 0 ? (L.stages < smax ? L.stages : smax) : (smax < sdef ? smax : sdef);
         if (stages >= 3) break;
         if (tj == 1) return false;
         tj = tj / 2;
