@@ -876,11 +876,9 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
         const size_t stage_bytes = (size_t)3 * (tj + 2) * nz * sizeof(double);
         int smax = (int)(smem_cap / stage_bytes);
         if (smax > 16) smax = 16;  // RingState::released
-        // default ring depth measured with interleaved sweeps (tools/sweep.py
-        // --rounds): 6 for the warp-specialised kernel (C1 sustained 124.7 vs
-        // 121.0 Gpts/s at 5, C3 / C4 level), 5 for the other thread budgets
-        const int sdef = maxt == 512 ? 6 : 5;
-        stages = L.stages > 0 ? (L.stages < smax ? L.stages : smax) : (smax < sdef ? smax : sdef);
+        // default ring depth 5 (tools/sweep.py); single-round plans deepen it
+        // to 6 below
+        stages = L.stages > 0 ? (L.stages < smax ? L.stages : smax) : (smax < 5 ? smax : 5);
         if (stages >= 3) break;
         if (tj == 1) return false;
         tj = tj / 2;
@@ -933,6 +931,18 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     if (grid < 1) grid = 1;
     p->grid = (int)grid;
     p->rounds = (units + grid - 1) / grid;
+    // Ring depth measured with interleaved sweeps (tools/sweep.py --rounds,
+    // profiles/README.md): a plan that is one round of long units (C1: 129
+    // CTAs x 171 planes) streams better with 6 stages (124.7 vs 121.0 Gpts/s
+    // sustained); multi-round plans keep 5 (C2 129 vs 125; a cold C4 launch
+    // read 4% more DRAM with 6).
+    if (L.stages <= 0 && maxt == 512 && p->rounds == 1) {
+        const size_t stage_bytes = (size_t)3 * (tj + 2) * nz * sizeof(double);
+        if ((size_t)6 * stage_bytes <= smem_cap) {
+            p->stages = 6;
+            p->smem = (size_t)6 * stage_bytes + 2 * 6 * sizeof(uint64_t) + sizeof(RingState);
+        }
+    }
     return true;
 }
 
