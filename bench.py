@@ -540,9 +540,14 @@ def run_reference(args):
     co = oracle.baseline_coefficients(SEED, nz)
     outs = [np.zeros_like(u) for _ in range(3)]
     run = lambda: oracle.advect_into(u, v, w, *outs, co["tcx"], co["tcy"], co["tzc1"], co["tzc2"], threads)  # noqa: E731
-    for _ in range(min(args.warmup, 2)):
+    for _ in range(max(1, min(args.warmup, 3))):
         run()
-    steps = max(1, min(args.steps, 5))
+    # K steps as asked, each one evaluation of the bounded sample, unless that
+    # would exceed ~3 minutes of CPU time (then as many as fit, reported)
+    t_probe = time.perf_counter()
+    run()
+    per = time.perf_counter() - t_probe
+    steps = max(1, min(args.steps, int(180.0 / max(per, 1e-6))))
     t0 = time.perf_counter()
     for _ in range(steps):
         run()
@@ -550,7 +555,7 @@ def run_reference(args):
     pts = sx * ny * nz
     value = pts * steps / dt / 1e9
     line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": ws, "steps": steps,
-            "warmup": min(args.warmup, 2), "ms_per_step": round(dt / steps * 1e3, 3),
+            "warmup": max(1, min(args.warmup, 3)), "ms_per_step": round(dt / steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (same generator as our arm)", "impl": "reference",
             "config": {"workload": desc, "nx": nx, "ny": ny, "nz": nz, "sample_nx": sx},
