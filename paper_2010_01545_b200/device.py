@@ -19,7 +19,8 @@ from . import _lib
 from .layout import GeneratorSpec, GridDims, GridError, make_grid
 
 __all__ = ["DeviceCoefficients", "make_opts", "advect", "step", "wrap_halos", "fill",
-           "describe_plan", "HostContext", "BoundLaunch", "dims_of", "alloc_fields"]
+           "describe_plan", "HostContext", "BoundLaunch", "dims_of", "alloc_fields",
+           "save_field", "load_field"]
 
 
 def _stream_handle(stream, device) -> ctypes.c_void_p:
@@ -236,6 +237,37 @@ def describe_plan(dims: GridDims, box=None, opts: _lib.Opts | None = None, devic
             "threads_per_column": info.threads_per_column, "stages": info.stages,
             "threads": info.threads, "grid": info.grid, "smem_bytes": info.smem_bytes,
             "strips": info.strips, "chunks": info.chunks, "long_strips": info.long_strips}
+
+
+# ---------------------------------------------------------------------------
+# field files (the reference's format, grid.py:252-270) straight to / from
+# device tensors through a page-locked buffer
+
+def save_field(t: torch.Tensor, path) -> None:
+    """Write a padded device field as the reference's field file: 24-byte
+    little-endian (nx, ny, nz) header + the padded float64 data."""
+    from .layout import _HEADER
+    dims = dims_of(t)
+    _check_field(t, dims, "field")
+    host = torch.empty(dims.padded_shape, dtype=torch.float64, pin_memory=True)
+    host.copy_(t)
+    with open(path, "wb") as fh:
+        fh.write(_HEADER.pack(dims.nx, dims.ny, dims.nz))
+        fh.write(memoryview(host.numpy()).cast("B"))
+
+
+def load_field(path, device=None) -> torch.Tensor:
+    """Read a reference field file into a new device tensor (GridError on a
+    truncated file, as read_field)."""
+    from .layout import _HEADER
+    with open(path, "rb") as fh:
+        nx, ny, nz = _HEADER.unpack(fh.read(_HEADER.size))
+        dims = make_grid(nx, ny, nz)
+        host = torch.empty(dims.padded_shape, dtype=torch.float64, pin_memory=True)
+        got = fh.readinto(memoryview(host.numpy()).cast("B"))
+    if got != dims.padded_len * 8:
+        raise GridError(f"truncated field file {path}")
+    return host.to(device or "cuda")
 
 
 class HostContext:

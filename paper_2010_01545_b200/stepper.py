@@ -87,6 +87,42 @@ class Stepper:
         self.graph = g
         self.graph_steps = steps
 
+    # -- checkpoint / resume (the reference persists fields only
+    # as field files, grid.py:252-270; a checkpoint is u, v, w in that format
+    # plus the step count, dt and coefficients)
+    def save(self, directory) -> None:
+        import json
+        from pathlib import Path
+        d = Path(directory)
+        d.mkdir(parents=True, exist_ok=True)
+        for name, f in zip("uvw", self.fields):  # halos refreshed: a valid field file
+            device.save_field(f, d / f"{name}.field")
+        tz = self.coeffs.tz.cpu().numpy()
+        (d / "stepper.json").write_text(json.dumps({
+            "steps_done": self.steps_done, "dt": self.dt.hex(),
+            "tcx": float(self.coeffs.tcx).hex(), "tcy": float(self.coeffs.tcy).hex(),
+            "tzc1": [float(x).hex() for x in tz[0]], "tzc2": [float(x).hex() for x in tz[1]]}))
+
+    @classmethod
+    def load(cls, directory, device_=None, *, opts=None) -> "Stepper":
+        """Resume a checkpoint written by save(): continuing from it gives the
+        same bits as never having stopped."""
+        import json
+        from pathlib import Path
+
+        import numpy as np
+        d = Path(directory)
+        meta = json.loads((d / "stepper.json").read_text())
+        fields = tuple(device.load_field(d / f"{n}.field", device_) for n in "uvw")
+        unhex = np.vectorize(float.fromhex, otypes=[np.float64])
+        co = device.DeviceCoefficients.from_host(
+            type("C", (), {"tcx": float.fromhex(meta["tcx"]), "tcy": float.fromhex(meta["tcy"]),
+                           "tzc1": unhex(meta["tzc1"]), "tzc2": unhex(meta["tzc2"])}),
+            fields[0].device)
+        st = cls(fields, co, float.fromhex(meta["dt"]), opts=opts)
+        st.steps_done = int(meta["steps_done"])
+        return st
+
     @property
     def fields(self):
         """Current fields with their halos refreshed (as wrap_halos leaves them)."""

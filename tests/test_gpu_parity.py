@@ -646,3 +646,28 @@ def test_back_to_back_dependent_launches():
     oracle.step_open(*f2, *args, 0.1, 1)
     for g, wnt in zip(z, f2):
         assert np.array_equal(g.cpu().numpy()[1:-1, 1:-1].view(np.int64), wnt[1:-1, 1:-1].view(np.int64))
+
+
+def test_field_files_and_stepper_checkpoint_resume(tmp_path):
+    """Device field I/O in the reference's file format (readable by the host
+    read_field), and a stepper checkpoint: 3 steps + save + load + 4 steps ==
+    7 uninterrupted steps, bitwise."""
+    dims = pw.make_grid(30, 26, 64)
+    spec = pw.GeneratorSpec.baseline(12)
+    co = pw.baseline_coefficients(12, 64)
+    f = device.fill(dims, spec)
+    device.save_field(f[0], tmp_path / "u.field")
+    host = pw.read_field(tmp_path / "u.field")
+    assert np.array_equal(host.data.view(np.int64), f[0].cpu().numpy().view(np.int64))
+    back = device.load_field(tmp_path / "u.field")
+    assert torch.equal(back.view(torch.int64), f[0].view(torch.int64))
+    straight = Stepper(device.fill(dims, spec), co, 0.1)
+    straight.step(7)
+    part = Stepper(device.fill(dims, spec), co, 0.1)
+    part.step(3)
+    part.save(tmp_path / "ckpt")
+    resumed = Stepper.load(tmp_path / "ckpt")
+    assert resumed.steps_done == 3
+    resumed.step(4)
+    for a, b in zip(resumed.fields, straight.fields):
+        assert torch.equal(a.view(torch.int64), b.view(torch.int64))
