@@ -48,7 +48,8 @@ enum {
     PWADV_E_RANGE = -3,     /* sub-box outside the interior / bad slab */
     PWADV_E_CUDA = -4,      /* CUDA launch or runtime error */
     PWADV_E_ARG = -5,       /* other invalid argument (mode, tuning) */
-    PWADV_E_ALIGN = -6      /* pointer not 8-byte aligned */
+    PWADV_E_ALIGN = -6      /* pointer not 8-byte aligned (the X-march also wants 16 bytes;
+                               8-byte-aligned fields run on the one-thread-per-point kernel) */
 };
 
 /* flags for pwadv_opts.flags */
@@ -70,8 +71,10 @@ typedef struct pwadv_opts {
     int32_t tile_j;        /* columns per CTA strip for the X-march kernel (0 = auto) */
     int32_t stages;        /* smem plane-ring depth (0 = auto) */
     int32_t grid;          /* CTAs (0 = auto: SMs x resident CTAs) */
-    int32_t max_threads;   /* X-march CTA thread budget: 512, 448, 384 or 256 (0 = auto) */
-    int32_t chunks;        /* X chunks per strip (work unit = chunk x strip; 0 = auto) */
+    int32_t max_threads;   /* X-march CTA thread budget: 512 (warp-specialised: 3 compute + 1
+                              producer warpgroup), 384, 256, 192 or 128 (0 = auto = 512) */
+    int32_t chunks;        /* > 0: every strip in this many X chunks (work unit = chunk x strip);
+                              0 = auto (whole strips for the full rounds, the rest chunked) */
     void *trace;           /* profiling only: device buffer of 2x4096 u64 for CTA 0's
                               per-plane copy-issue / arrival %globaltimer stamps; NULL = off */
 } pwadv_opts;
