@@ -304,15 +304,19 @@ def run_reference(fields, coeffs) -> SourceSet:
 
 
 def _advect_point(which: int, fields, coeffs, i: int, j: int, k: int) -> float:
-    import torch
-    from . import device
+    """One point through the GPU formula kernel (K6) on its 15 operands, as
+    the reference's _advect_point (kernel.py:186-195): 1-based i, j and
+    k (2 <= k <= nz); at the top (k == nz) the k+1 operands are passed as 0.0.
+    Only the operands cross to the device, not the fields."""
     dims = fields.dims
     assert 1 <= i <= dims.nx and 1 <= j <= dims.ny and 2 <= k <= dims.nz
-    dev = torch.device("cuda")
-    u, v, w = (torch.from_numpy(_host_array(f, dims)).to(dev) for f in (fields.u, fields.v, fields.w))
-    out = device.alloc_fields(GridDims(dims.nx, dims.ny, dims.nz), dev)
-    device.advect(u, v, w, coeffs, out, box=(i, i + 1, j, j + 1), opts=device.make_opts("simple"))
-    return float(out[which][i, j, k - 1].item())
+    top = k == dims.nz
+    arrs = {"u": fields.u.data, "v": fields.v.data, "w": fields.w.data}
+    fn, spec = _FORMULAS[which]
+    ops = [0.0 if (top and dk == 1) else float(arrs[f][i + dx, j + dy, k - 1 + dk])
+           for f, dx, dy, dk in spec]
+    return float(fn(float(coeffs.tcx), float(coeffs.tcy), float(coeffs.tzc1[k - 1]),
+                    float(coeffs.tzc2[k - 1]), *ops, top=top))
 
 
 def advect_point_u(fields, coeffs, i: int, j: int, k: int) -> float:
