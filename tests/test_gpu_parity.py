@@ -698,3 +698,11 @@ def test_acceptance_criterion7_variants_by_engines():
                     out, _, _ = pw.run_schedule(fs, co, spec)
                     got = (out.su.data, out.sv.data, out.sw.data)
                 assert_bitwise(got, want, (nx, ny, nz, name, engines))
+
+
+def test_dropin_tour_example_runs():
+    """examples/dropin_tour.py: the reference's calls, unchanged, on the GPU."""
+    import runpy
+    from pathlib import Path
+    runpy.run_path(str(Path(__file__).resolve().parent.parent / "examples" / "dropin_tour.py"),
+                   run_name="__main__")
