@@ -116,7 +116,9 @@ int pwadv_advect_box_f64(const double *u, const double *v, const double *w,
 
 /* Launch plan the library would use for K1 on this box (for reports/benches). */
 typedef struct pwadv_plan_info {
-    int32_t kernel;        /* 1 = X-march (bulk-copy plane ring), 2 = one-thread-per-point */
+    int32_t kernel;        /* 1 = X-march (bulk-copy plane ring), 2 = one-thread-per-point,
+                              3 = general march (register x-window, cached loads: odd nz,
+                              8-byte alignment, tall columns) */
     int32_t tile_j, threads_per_column, stages, threads, grid;
     int64_t smem_bytes, strips;
     int32_t chunks;        /* X chunks of the strips after the full rounds */

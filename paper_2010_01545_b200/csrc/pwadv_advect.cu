@@ -154,6 +154,116 @@ __device__ __forceinline__ Unit unit_at(const BoxArgs &a, const TileCfg &t, int6
 }
 
 // ---------------------------------------------------------------------------
+// march kernel (K1m): the general X-march for shapes the TMA ring does not
+// take (odd nz, 8-byte-aligned fields, tall columns). A 32 x 4 thread block
+// owns a tile of 32 levels x 4 columns and marches through an X chunk with
+// the x-1/x/x+1 window of its own (j, k) in registers; j +- 1 operands are
+// read-only-cache loads (the neighbouring columns' own operands, mostly L1
+// hits), k +- 1 come from the neighbouring lanes by shuffles (lane 0 / 31
+// load across the tile edge), and the x-shifted diagonal operands are
+// carried from the previous plane. 10 loads per point instead of K1s's 27.
+
+template <bool FMA, bool STEP>
+__global__ void __launch_bounds__(128) k_advect_march(BoxArgs a, int64_t nchunks)
+{
+    const int64_t nz = a.nz, ny2 = a.ny + 2;
+    const int64_t nbx = a.x1 - a.x0, nby = a.y1 - a.y0;
+    const int64_t ktiles = (nz + 31) / 32;
+    const int64_t tile = blockIdx.x;
+    const int64_t kt = tile % ktiles, jt = tile / ktiles;
+    const int lane = threadIdx.x;
+    const int64_t k = kt * 32 + lane;
+    const int64_t j = a.y0 + jt * 4 + threadIdx.y;
+    const int64_t chunk = blockIdx.y;
+    const int64_t ib = a.x0 + nbx * chunk / nchunks, ie = a.x0 + nbx * (chunk + 1) / nchunks;
+    const bool kin = k < nz;
+    const bool active = kin && j < a.y1;
+    // loads of an inactive lane read a valid cell (its column clamped into the
+    // box, level clamped into the column); its results are never stored
+    const int64_t jj = j < a.y1 ? j : a.y1 - 1;
+    const int64_t kk = kin ? k : nz - 1;
+    const int64_t sI = ny2 * nz, sJ = nz;
+    const bool top = (k == nz - 1);
+    const bool lo_edge = lane == 0 && k > 0;            // k-1 lives in the previous tile
+    const bool hi_edge = lane == 31 && k + 1 < nz;      // k+1 lives in the next tile
+    const double tcx = a.tcx, tcy = a.tcy, dt = a.dt;
+    const double c1 = __ldg(a.tzc1 + kk), c2 = __ldg(a.tzc2 + kk);
+    const unsigned full = 0xffffffffu;
+    if (ib >= ie) return;
+
+    auto at = [&](const double *f, int64_t i, int64_t jx, int64_t kx) -> double {
+        return __ldg(f + (i * ny2 + jx) * nz + kx);
+    };
+    auto up = [&](double x, const double *f, int64_t i, int64_t jx) -> double {  // value at k-1
+        double m = __shfl_up_sync(full, x, 1);
+        if (lo_edge) m = at(f, i, jx, k - 1);
+        return m;
+    };
+    auto down = [&](double x, const double *f, int64_t i, int64_t jx) -> double {  // value at k+1
+        double q = __shfl_down_sync(full, x, 1);
+        if (hi_edge) q = at(f, i, jx, k + 1);
+        return q;
+    };
+
+    // plane ib-1 (x-1 window) and plane ib
+    double u_m = at(a.u, ib - 1, jj, kk), v_m = at(a.v, ib - 1, jj, kk), w_m = at(a.w, ib - 1, jj, kk);
+    double u_xm1_jp1 = at(a.u, ib - 1, jj + 1, kk);
+    double u_xm1_km1 = up(u_m, a.u, ib - 1, jj);
+    double u_c = at(a.u, ib, jj, kk), v_c = at(a.v, ib, jj, kk), w_c = at(a.w, ib, jj, kk);
+    for (int64_t i = ib; i < ie; ++i) {
+        // leading plane i+1 (a one-plane-ahead prefetch measured slower: the
+        // extra registers cost occupancy)
+        const double u_p = at(a.u, i + 1, jj, kk), v_p = at(a.v, i + 1, jj, kk);
+        const double w_p = at(a.w, i + 1, jj, kk);
+        const double v_p_jm1 = at(a.v, i + 1, jj - 1, kk);
+        // current plane i: j +- 1
+        const double u_jm1 = at(a.u, i, jj - 1, kk), u_jp1 = at(a.u, i, jj + 1, kk);
+        const double v_jm1 = at(a.v, i, jj - 1, kk), v_jp1 = at(a.v, i, jj + 1, kk);
+        const double w_jm1 = at(a.w, i, jj - 1, kk), w_jp1 = at(a.w, i, jj + 1, kk);
+        // k +- 1 from the neighbouring lanes
+        const double u_km1 = up(u_c, a.u, i, jj), u_kp1 = down(u_c, a.u, i, jj);
+        const double v_km1 = up(v_c, a.v, i, jj), v_kp1 = down(v_c, a.v, i, jj);
+        const double w_km1 = up(w_c, a.w, i, jj), w_kp1 = down(w_c, a.w, i, jj);
+        const double w_p_km1 = up(w_p, a.w, i + 1, jj);
+        const double w_jp1_km1 = up(w_jp1, a.w, i, jj + 1);
+        const double v_jm1_km1 = up(v_jm1, a.v, i, jj - 1);
+
+        double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+        if (k > 0) {
+            // operand wiring kernel.py:117-128 (the top level never reads k+1)
+            r0 = su_formula<FMA>(tcx, tcy, c1, c2, u_c, u_m, u_p, u_jm1, u_jp1, u_km1, u_kp1,
+                                 v_jm1, v_p_jm1, v_c, v_p, w_km1, w_p_km1, w_c, w_p, top);
+            r1 = sv_formula<FMA>(tcx, tcy, c1, c2, v_c, v_m, v_p, v_jm1, v_jp1, v_km1, v_kp1,
+                                 u_m, u_xm1_jp1, u_c, u_jp1, w_km1, w_jp1_km1, w_c, w_jp1, top);
+            r2 = sw_formula<FMA>(tcx, tcy, c1, c2, w_c, w_m, w_p, w_jm1, w_jp1, w_km1, w_kp1,
+                                 u_xm1_km1, u_m, u_km1, u_c, v_jm1_km1, v_jm1, v_km1, v_c, top);
+        }
+        if constexpr (STEP) {
+            r0 = fwd_update(u_c, dt, r0);
+            r1 = fwd_update(v_c, dt, r1);
+            r2 = fwd_update(w_c, dt, r2);
+        }
+        if (active) {
+            const int64_t o = (i * ny2 + j) * nz + k;
+            a.o0[o] = r0;
+            a.o1[o] = r1;
+            a.o2[o] = r2;
+        }
+        // roll the window; diagonal operands of the next plane
+        u_xm1_jp1 = u_jp1;
+        u_xm1_km1 = u_km1;
+        u_m = u_c;
+        v_m = v_c;
+        w_m = w_c;
+        u_c = u_p;
+        v_c = v_p;
+        w_c = w_p;
+    }
+    (void)sI;
+    (void)sJ;
+}
+
+// ---------------------------------------------------------------------------
 // simple kernel
 
 template <bool FMA, bool STEP>
@@ -817,6 +927,26 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
             cfg.numAttrs = 1;
             e = cudaLaunchKernelEx(&cfg, kern, a, t);
             if (e != cudaSuccess) return set_cuda_error("advect launch", e);
+        }
+    } else if (!a.rim && !a.push && !(L.flags & PWADV_FLAG_SIMPLE)) {
+        // K1m: the general march (odd nz, 8-byte alignment, tall columns)
+        const int64_t tiles = ((L.nz + 31) / 32) * ((nby + 3) / 4);
+        int64_t nch = ((int64_t)dev->sms * 16 + tiles - 1) / tiles;
+        const int64_t nch_max = nbx / 8 > 1 ? nbx / 8 : 1;
+        if (nch > nch_max) nch = nch_max;
+        if (nch > 65535) nch = 65535;
+        if (tiles > 0x7fffffff) return set_error(PWADV_E_DIMS, "box too large for the march kernel");
+        const dim3 grid((unsigned)tiles, (unsigned)nch), block(32, 4);
+        if (L.step) {
+            if (fma)
+                k_advect_march<true, true><<<grid, block, 0, stream>>>(a, nch);
+            else
+                k_advect_march<false, true><<<grid, block, 0, stream>>>(a, nch);
+        } else {
+            if (fma)
+                k_advect_march<true, false><<<grid, block, 0, stream>>>(a, nch);
+            else
+                k_advect_march<false, false><<<grid, block, 0, stream>>>(a, nch);
         }
     } else {
         const int64_t total = (a.rim ? 2 * nby + 2 * (nbx - 2) : nbx * nby) * L.nz;

@@ -301,6 +301,9 @@ int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz, int64_t x0, int64_t 
         out->strips = p.nstrips;
         out->chunks = p.nchunks;
         out->long_strips = (int32_t)p.nlong;
+    } else if (!(L.flags & (PWADV_FLAG_SIMPLE | PWADV_FLAG_RIM))) {
+        out->kernel = 3;  // the general march (launch_box)
+        out->threads = 128;
     } else {
         out->kernel = 2;
         out->threads = 256;

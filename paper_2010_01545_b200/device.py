@@ -233,7 +233,7 @@ def describe_plan(dims: GridDims, box=None, opts: _lib.Opts | None = None, devic
     info = _lib.PlanInfo()
     _lib.check(_lib.lib().pwadv_describe_plan(dims.nx, dims.ny, dims.nz, x0, x1, y0, y1,
                                               _lib.opts_ptr(opts), int(device), ctypes.byref(info)))
-    return {"kernel": {1: "xmarch", 2: "simple"}[info.kernel], "tile_j": info.tile_j,
+    return {"kernel": {1: "xmarch", 2: "simple", 3: "march"}[info.kernel], "tile_j": info.tile_j,
             "threads_per_column": info.threads_per_column, "stages": info.stages,
             "threads": info.threads, "grid": info.grid, "smem_bytes": info.smem_bytes,
             "strips": info.strips, "chunks": info.chunks, "long_strips": info.long_strips}

@@ -419,7 +419,10 @@ def test_tall_and_odd_columns_bitwise(shape):
     got, dims = gpu_advect(u, v, w, *args)
     assert_bitwise(got, oracle.advect(u, v, w, *args), shape)
     plan = device.describe_plan(dims)
-    assert plan["kernel"] == ("xmarch" if nz in (300, 512) else "simple")
+    assert plan["kernel"] == ("xmarch" if nz in (300, 512) else "march")
+    # and the one-thread-per-point kernel, forced, agrees
+    got_s, _ = gpu_advect(u, v, w, *args, "simple")
+    assert_bitwise(got_s, oracle.advect(u, v, w, *args), (shape, "simple"))
 
 
 @pytest.mark.parametrize("shape", [(3, 120000, 64), (2, 60010, 128)])
@@ -706,3 +709,50 @@ def test_dropin_tour_example_runs():
     from pathlib import Path
     runpy.run_path(str(Path(__file__).resolve().parent.parent / "examples" / "dropin_tour.py"),
                    run_name="__main__")
+
+
+@pytest.mark.parametrize("shape", [(9, 7, 3), (20, 13, 33), (37, 29, 63), (12, 9, 65), (6, 5, 127),
+                                   (3, 2, 1030), (40, 1, 2)])
+def test_general_march_kernel_bitwise(shape):
+    """K1m (odd nz, tall columns, 8-byte-aligned fields): whole grid, a sub-box,
+    the fused step and the FMA build against the oracle; its plan is 'march'."""
+    nx, ny, nz = shape
+    u, v, w = oracle.fill_random(nx, ny, nz, 31, baseline=True)
+    co = oracle.baseline_coefficients(31, nz)
+    args = (co["tcx"], co["tcy"], co["tzc1"], co["tzc2"])
+    dims = pw.make_grid(nx, ny, nz)
+    want = oracle.advect(u, v, w, *args)
+    got, _ = gpu_advect(u, v, w, *args)
+    if nz % 2:
+        assert device.describe_plan(dims)["kernel"] == "march"
+    assert_bitwise(got, want, shape)
+    # 8-byte (not 16-byte) aligned device fields: views one double into a buffer
+    n = (nx + 2) * (ny + 2) * nz
+    bufs = [torch.empty(n + 1, dtype=torch.float64, device="cuda") for _ in range(6)]
+    fin = [b[1:].view(dims.padded_shape) for b in bufs[:3]]
+    fout = [b[1:].view(dims.padded_shape) for b in bufs[3:]]
+    for t, a in zip(fin, (u, v, w)):
+        t.copy_(torch.from_numpy(a))
+    for t in fout:
+        t.zero_()
+    dco = pw.AdvectionCoefficients(*args)
+    device.advect(*fin, dco, fout)
+    assert_bitwise([t.cpu().numpy() for t in fout], want, (shape, "8-byte aligned"))
+    # a sub-box
+    box = (1 + nx // 3, nx + 1, 1, max(2, ny))
+    out = device.alloc_fields(dims, "cuda")
+    device.advect(*fin, dco, out, box=box)
+    for o, wnt in zip(out, want):
+        x0, x1, y0, y1 = box
+        assert np.array_equal(o.cpu().numpy()[x0:x1, y0:y1].view(np.int64),
+                              wnt[x0:x1, y0:y1].view(np.int64))
+    # the fused step
+    nxt = device.alloc_fields(dims, "cuda")
+    device.step(*fin, dco, 0.1, nxt)
+    for g, f, s in zip(nxt, (u, v, w), want):
+        assert np.array_equal(g.cpu().numpy()[1:-1, 1:-1].view(np.int64),
+                              (f + 0.1 * s)[1:-1, 1:-1].view(np.int64))
+    # FMA build within BASELINE's normwise tolerance
+    gf, _ = gpu_advect(u, v, w, *args, "xmarch_fma")
+    r = oracle.compare(gf, want)
+    assert r["normwise_rel"] <= 1e-12, r
