@@ -482,43 +482,59 @@ class IpcPeerRegistry:
         self.dec, self.group = dec, group
         self.sets: dict = {}
         self._opened: list = []
+        self._bases: dict = {}
 
     def publish(self, rank: int, sets) -> None:
         import torch.distributed as dist
-        from . import _lib
-        L = _lib.lib()
-        mine = []
-        for s in sets:
-            entry = []
-            for t in s:
-                h = (ctypes.c_ubyte * 64)()
-                off = ctypes.c_uint64()
-                _lib.check(L.pwadv_ipc_export(ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off)))
-                entry.append((bytes(h), int(off.value)))
-            mine.append(entry)
+        mine = [self.export(s) for s in sets]
         everyone = [None] * self.dec.size
         dist.all_gather_object(everyone, mine, group=self.group)
         self.sets[rank] = tuple(tuple(t.data_ptr() for t in s) for s in sets)
         for r in set(neighbour_ranks(self.dec)) - {rank}:
-            ptrs = []
-            for entry in everyone[r]:
-                row = []
-                for hb, off in entry:
+            self.sets[r] = self.map_remote(everyone[r])
+
+    def map_remote(self, exported):
+        """Device pointers for another process's exported buffers: each
+        distinct allocation handle is opened once (several tensors may live in
+        one allocation), plus the tensor's offset inside it."""
+        from . import _lib
+        L = _lib.lib()
+        ptrs = []
+        for entry in exported:
+            row = []
+            for hb, off in entry:
+                base = self._bases.get(hb)
+                if base is None:
                     p = ctypes.c_void_p()
-                    _lib.check(L.pwadv_ipc_open((ctypes.c_ubyte * 64)(*hb), off, ctypes.byref(p)))
-                    self._opened.append((p.value, off))
-                    row.append(p.value)
-                ptrs.append(tuple(row))
-            self.sets[r] = tuple(ptrs)
+                    _lib.check(L.pwadv_ipc_open((ctypes.c_ubyte * 64)(*hb), 0, ctypes.byref(p)))
+                    base = self._bases[hb] = p.value
+                    self._opened.append(base)
+                row.append(base + off)
+            ptrs.append(tuple(row))
+        return tuple(ptrs)
+
+    @staticmethod
+    def export(tensors):
+        """(handle bytes, offset) of each tensor, for another process's map_remote."""
+        from . import _lib
+        L = _lib.lib()
+        out = []
+        for t in tensors:
+            h = (ctypes.c_ubyte * 64)()
+            off = ctypes.c_uint64()
+            _lib.check(L.pwadv_ipc_export(ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off)))
+            out.append((bytes(h), int(off.value)))
+        return out
 
     def pointers(self, rank: int, set_index: int):
         return self.sets[rank][set_index]
 
     def close(self) -> None:
         from . import _lib
-        for p, off in self._opened:
-            _lib.lib().pwadv_ipc_close(ctypes.c_void_p(p), off)
+        for base in self._opened:
+            _lib.lib().pwadv_ipc_close(ctypes.c_void_p(base), 0)
         self._opened = []
+        self._bases = {}
 
 
 class NcclBarrier:

@@ -7,6 +7,7 @@ the in-process ThreadHubTransport instead of NCCL (kernels never wait on one
 another). Results must be bitwise identical to the single-domain evaluation.
 """
 
+import ctypes
 import threading
 
 import numpy as np
@@ -153,3 +154,52 @@ def test_cuda_face_ops_match_tensor_slicing(axis):
     TorchFaceOps.unpack2(b, src_lo, src_hi, axis, n)
     torch.cuda.synchronize()
     assert all(torch.equal(x, y) for x, y in zip(a, b))
+
+
+def _ipc_reader(q_in, q_out):
+    """Second process: map the first process's buffers and fill them with K5."""
+    try:
+        import paper_2010_01545_b200 as pw2
+        from paper_2010_01545_b200 import _lib, decomp as dc
+        torch.cuda.set_device(0)
+        exported, dims = q_in.get(timeout=120)
+        reg = dc.IpcPeerRegistry.__new__(dc.IpcPeerRegistry)
+        reg._opened, reg._bases = [], {}
+        (ptrs,) = reg.map_remote([exported])
+        g = pw2.make_grid(*dims)
+        _lib.check(_lib.lib().pwadv_fill_f64(*(ctypes.c_void_p(p) for p in ptrs), g.nx, g.ny, g.nz,
+                                             1, 77, 0.0, 0.0, 0.0, None))
+        torch.cuda.synchronize()
+        n_bases = len(reg._bases)
+        reg.close()
+        q_out.put(("ok", n_bases))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q_out.put(("error", repr(e)))
+
+
+def test_ipc_export_map_and_write_across_processes():
+    """CUDA IPC as the fused step uses it, between two processes on one GPU
+    (no kernel waits on another: the writer finishes before the owner reads):
+    three fields carved out of ONE allocation (shared handle, nonzero
+    offsets) are mapped by the other process, which writes them with K5; the
+    owner then sees exactly the K5 fields."""
+    import torch.multiprocessing as mp
+    from paper_2010_01545_b200.decomp import IpcPeerRegistry
+    d = pw.make_grid(20, 18, 16)
+    n = d.padded_len
+    block = torch.zeros(3 * n + 64, dtype=torch.float64, device="cuda")
+    fields = [block[8 + m * n: 8 + (m + 1) * n].view(d.padded_shape) for m in range(3)]
+    torch.cuda.synchronize()
+    ctx = mp.get_context("spawn")
+    q_in, q_out = ctx.Queue(), ctx.Queue()
+    p = ctx.Process(target=_ipc_reader, args=(q_in, q_out))
+    p.start()
+    q_in.put((IpcPeerRegistry.export(fields), (d.nx, d.ny, d.nz)))
+    status, info = q_out.get(timeout=180)
+    p.join(timeout=60)
+    assert status == "ok", info
+    assert info == 1  # one allocation, opened once
+    want = device.fill(d, pw.GeneratorSpec.baseline(77))
+    torch.cuda.synchronize()
+    for f, w in zip(fields, want):
+        assert torch.equal(f.view(torch.int64), w.view(torch.int64))
