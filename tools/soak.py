@@ -1,0 +1,63 @@
+"""Soak test of the ring protocol: many back-to-back launches must keep giving
+the same bits (a rare race in the mbarrier / refill protocol would show up as
+a changed digest or a hang). Prints one JSON line.
+
+    python tools/soak.py [--launches 100000] [--steps 3000]
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch  # noqa: E402
+
+import paper_2010_01545_b200 as pw  # noqa: E402
+from paper_2010_01545_b200 import device  # noqa: E402
+from paper_2010_01545_b200.stepper import Stepper  # noqa: E402
+
+
+def digest(ts):
+    return tuple(int(t.view(torch.int64).sum().item()) for t in ts)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--launches", type=int, default=100000)
+    ap.add_argument("--steps", type=int, default=3000)
+    a = ap.parse_args()
+    res = {}
+    # K1, C1: same inputs, same outputs, every 1000 launches compared
+    d = pw.make_grid(512, 512, 64)
+    f = device.fill(d, pw.GeneratorSpec.baseline(42))
+    co = device.DeviceCoefficients.from_host(pw.baseline_coefficients(42, 64), "cuda")
+    out = device.alloc_fields(d, "cuda")
+    device.advect(*f, co, out)
+    ref = digest(out)
+    bad = 0
+    t = time.perf_counter()
+    for n in range(a.launches):
+        device.advect(*f, co, out)
+        if n % 1000 == 999:
+            bad += digest(out) != ref
+    torch.cuda.synchronize()
+    res["k1_c1"] = {"launches": a.launches, "mismatches": bad, "s": round(time.perf_counter() - t, 1)}
+    # K4, C4 block: two identical runs of `steps` steps end in the same bits
+    d4 = pw.make_grid(2048, 1024, 128)
+    co4 = pw.baseline_coefficients(42, 128)
+    digests = []
+    t = time.perf_counter()
+    for _ in range(2):
+        st = Stepper(device.fill(d4, pw.GeneratorSpec.baseline(42)), co4, 0.01)
+        st.step(a.steps)
+        digests.append(digest(st.fields))
+        del st
+        torch.cuda.empty_cache()
+    res["k4_c4"] = {"steps": a.steps, "runs_equal": digests[0] == digests[1],
+                    "s": round(time.perf_counter() - t, 1)}
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
