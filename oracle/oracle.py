@@ -265,6 +265,46 @@ def compute_block_numpy(tcx, tcy, tzc1, tzc2, roles):
     return tuple(outs)
 
 
+def run_schedule_numpy(u, v, w, tcx, tcy, tzc1, tzc2, engines: int = 1, outs=None):
+    """The reference's own CPU path as written: run_schedule(..., "reference",
+    engines) (schedules.py:207-232) — balanced X slabs (partition_domain,
+    schedules.py:65-75), each engine thread evaluating compute_block on its
+    slab's grid_roles views (schedules.py:131-135, kernel.py:139-172) with
+    numpy ufuncs and scattering into the zeroed padded outputs. Same
+    arithmetic form and speed as the reference (4.06 vs 4.04 Mpts/s on one
+    thread in this container); bitwise equal to `advect`. `outs` (pre-zeroed
+    padded arrays) may be passed to reuse them."""
+    nx, ny, nz = u.shape[0] - 2, u.shape[1] - 2, u.shape[2]
+    engines = max(1, min(int(engines), nx))
+    tzc1 = np.asarray(tzc1, dtype=np.float64)
+    tzc2 = np.asarray(tzc2, dtype=np.float64)
+    if outs is None:
+        outs = tuple(np.zeros_like(u) for _ in range(3))
+    F = {"u": u, "v": v, "w": w}
+    base, rem = divmod(nx, engines)
+    slabs, x = [], 1
+    for e in range(engines):
+        wd = base + (1 if e < rem else 0)
+        slabs.append((x, x + wd))
+        x += wd
+
+    def slab(xb, xe):
+        roles = [F[f][xb + dx:xe + dx, 1 + dy:ny + 1 + dy, :] for f, dx, dy in ROLES]
+        with np.errstate(invalid="ignore", over="ignore"):
+            blocks = compute_block_numpy(tcx, tcy, tzc1, tzc2, roles)
+        for o, b in zip(outs, blocks):
+            o[xb:xe, 1:ny + 1, 1:] = b[..., 1:]
+
+    if engines == 1:
+        slab(*slabs[0])
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=engines) as pool:
+            for f in [pool.submit(slab, xb, xe) for xb, xe in slabs]:
+                f.result()
+    return tuple(outs)
+
+
 def step(u, v, w, tcx, tcy, tzc1, tzc2, dt: float, steps: int, engines: int = 1):
     """Composed forward-Euler oracle: in place on u, v, w."""
     nx, ny, nz = u.shape[0] - 2, u.shape[1] - 2, u.shape[2]

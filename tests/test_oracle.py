@@ -48,6 +48,9 @@ def test_oracle_engine_count_independence(engines):
     a = oracle.advect(u, v, w, co["tcx"], co["tcy"], co["tzc1"], co["tzc2"], engines=1)
     b = oracle.advect(u, v, w, co["tcx"], co["tcy"], co["tzc1"], co["tzc2"], engines=engines)
     assert oracle.compare(a, b)["bitwise_equal"]
+    # the numpy restatement of run_schedule (bench.py's reference arm) too
+    c = oracle.run_schedule_numpy(u, v, w, co["tcx"], co["tcy"], co["tzc1"], co["tzc2"], engines)
+    assert oracle.compare(a, c)["bitwise_equal"]
 
 
 def test_lcg_skip_ahead_and_naive_recurrence():
