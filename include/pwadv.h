@@ -55,6 +55,11 @@ enum {
 /* flags for pwadv_opts.flags */
 #define PWADV_FLAG_FMA 1u           /* contract into DFMA (not bit-exact; <=1e-12 normwise) */
 #define PWADV_FLAG_SIMPLE 2u        /* force the one-thread-per-point kernel */
+#define PWADV_FLAG_MARCH 4u         /* force the general march K1m (no shared-memory plane ring) */
+#define PWADV_FLAG_UNALIGNED 8u     /* X-march in its unaligned-run form (copies start up to one
+                                       element early, scalar shared loads/stores) even where the
+                                       aligned form applies; odd nz and 8-byte-aligned fields
+                                       always use it */
 #define PWADV_FLAG_RIM 16u          /* only the one-cell rim of the box (one launch; multi-GPU overlap) */
 #define PWADV_FLAG_GENERIC 32u      /* X-march with a run-time tile layout even for nz = 64 / 128 */
 #define PWADV_FLAG_L2_UNIT_HEAD 64u /* X-march: load each work unit's first two planes L2 evict_last */
@@ -117,8 +122,10 @@ int pwadv_advect_box_f64(const double *u, const double *v, const double *w,
 /* Launch plan the library would use for K1 on this box (for reports/benches). */
 typedef struct pwadv_plan_info {
     int32_t kernel;        /* 1 = X-march (bulk-copy plane ring), 2 = one-thread-per-point,
-                              3 = general march (register x-window, cached loads: odd nz,
-                              8-byte alignment, tall columns) */
+                              3 = general march (register x-window, cached loads: tall
+                              columns, fused halo push at odd nz / 8-byte alignment),
+                              4 = X-march with unaligned tile runs (odd nz, 8-byte-aligned
+                              fields) */
     int32_t tile_j, threads_per_column, stages, threads, grid;
     int64_t smem_bytes, strips;
     int32_t chunks;        /* X chunks of the strips after the full rounds */

@@ -35,6 +35,8 @@ PWADV_E_ALIGN = -6
 
 FLAG_FMA = 1
 FLAG_SIMPLE = 2
+FLAG_MARCH = 4
+FLAG_UNALIGNED = 8
 FLAG_RIM = 16
 FLAG_GENERIC = 32
 FLAG_L2_UNIT_HEAD = 64

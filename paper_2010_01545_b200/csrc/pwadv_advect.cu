@@ -120,6 +120,7 @@ struct TileCfg {
     int l2hint;       // 1: load each unit's first two planes with L2 evict_last
     int64_t nstrips;  // ceil((y1-y0)/tj)
     int64_t nlong;    // strips 0..nlong-1 are whole-X units (full rounds); the rest are chunked
+    int ua;           // planned UA (unaligned tile runs) — informational
 };
 
 // Work units (unit_at) are dealt round-robin to the CTAs: CTA b runs units
@@ -422,6 +423,39 @@ __device__ __forceinline__ void issue_plane(const RingState *rs, const BoxArgs &
     bulk_g2s(dst + 2 * CS, a.w + off, bytes, &full[st]);
 }
 
+// Unaligned tile runs (UA kernels: odd nz, 8-byte-aligned fields). A plane
+// tile of a field is still one contiguous run, but its start need not be
+// 16-byte aligned: the copy starts at the 16-byte boundary below it (d = 0 or
+// 1 element early; u, v and w share d, plan_xmarch checks) and is rounded up
+// to 16 bytes, so the tile sits at offset d of the stage slot and the compute
+// warps read it with scalar loads. Only a run that ends at the very end of a
+// field can have its rounded copy overrun the array by one element; then the
+// copy stops 16 bytes short and the producer moves the last element itself
+// (before arming the barrier, whose arrive releases the store).
+__device__ __forceinline__ void issue_plane_ua(const RingState *rs, const BoxArgs &a, int q, int st,
+                                               int CS, double *ring, uint64_t *full)
+{
+    int k = 0;
+    while (rs->first[k + 1] <= q) ++k;
+    const int64_t off = rs->src[k] + (int64_t)(q - rs->first[k]) * ((a.ny + 2) * a.nz);
+    const int64_t d = (int64_t)(((uintptr_t)(a.u + off) >> 3) & 1);
+    const int64_t run = rs->bytes[k] / sizeof(double);  // elements of the tile run
+    uint32_t n = (uint32_t)(((d + run) * 8 + 15) & ~(int64_t)15);
+    double *dst = ring + (size_t)st * 3 * CS;
+    const int64_t total = (a.nx + 2) * (a.ny + 2) * a.nz;  // elements per field
+    if (off - d + n / 8 > total) {  // overrun of one element at the end of the fields
+        n -= 16;
+        const int64_t last = off - d + n / 8;  // == total - 1, the run's last element
+        dst[n / 8] = a.u[last];
+        dst[CS + n / 8] = a.v[last];
+        dst[2 * CS + n / 8] = a.w[last];
+    }
+    mbar_arrive_expect_tx(&full[st], 3 * n);
+    bulk_g2s(dst, a.u + off - d, n, &full[st]);
+    bulk_g2s(dst + CS, a.v + off - d, n, &full[st]);
+    bulk_g2s(dst + 2 * CS, a.w + off - d, n, &full[st]);
+}
+
 // X-march kernel. Register slots U0[3], V0[3], ... hold plane p in slot p % 3
 // (relative to the unit start), so the x-1/x/x+1 window rotates by renaming —
 // the step body is instantiated for the three rotations and unrolled, with no
@@ -440,12 +474,16 @@ __host__ __device__ constexpr int ctas_per_sm(int maxt) { return maxt <= 128 ? 3
 // NZC > 0 (warp-specialised kernel only): nz, TJ and the tile layout are
 // compile-time constants, so every staged operand is one LDS at an immediate
 // offset from a per-plane base register (the BASELINE nz = 64 / 128 cases).
-template <bool FMA, bool STEP, int MAXT, bool FIX, int NZC = 0>
+// UA: unaligned tile runs (issue_plane_ua) — each staged plane sits at offset
+// d in its slot, scalar shared loads and output stores (odd nz or 8-byte-
+// aligned fields; warp-specialised kernel only, no fused halo push).
+template <bool FMA, bool STEP, int MAXT, bool FIX, int NZC = 0, bool UA = false>
 __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     k_advect_xmarch(const __grid_constant__ BoxArgs a, const __grid_constant__ TileCfg t)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     static_assert(NZC == 0 || (MAXT == 512 && 384 % (NZC / 2) == 0), "compile-time layout: WS only");
+    static_assert(!UA || (MAXT == 512 && NZC == 0), "unaligned runs: warp-specialised, run-time layout");
     // programmatic dependent launch (launch_box): wait until the previous grid
     // on the stream has completed and its writes are visible (they may be our
     // inputs) before any global access, and let the next grid be scheduled
@@ -456,7 +494,9 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     const int TJ = NZC ? 384 / (NZC / 2) : t.tj;
     const int KP = NZC ? NZC / 2 : t.kp;
     const int nz = NZC ? NZC : (int)a.nz;
-    const int CS = (TJ + 2) * nz;  // doubles per field per tile-plane
+    // doubles per field slot of a stage (UA: room for the offset d and the
+    // 16-byte rounding of the copy, kept even so every slot is 16-byte aligned)
+    const int CS = UA ? (((TJ + 2) * nz + 3) & ~1) : (TJ + 2) * nz;
     double *ring = reinterpret_cast<double *>(smem_raw);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + (size_t)S * 3 * CS * sizeof(double));
     uint64_t *empty = full + S;  // warp-specialised variant only
@@ -477,11 +517,13 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     const bool fixM = FIX && (lane == 0) && kp > 0;
     const bool fixQ = FIX && (lane == 31) && kp < KP - 1;
     const bool top_b = (k1 == nz - 1);
+    const bool top_a = UA && (k0 == nz - 1);  // odd nz: the top is a pair's first level
     const bool lvl0 = (k0 == 0);
+    const int k1c = UA ? (k1 < nz ? k1 : nz - 1) : k1;  // odd nz: k1 = nz is past the column
 
     const double tcx = a.tcx, tcy = a.tcy, dt = a.dt;
-    const double c1a = __ldg(a.tzc1 + k0), c1b = __ldg(a.tzc1 + k1);
-    const double c2a = __ldg(a.tzc2 + k0), c2b = __ldg(a.tzc2 + k1);
+    const double c1a = __ldg(a.tzc1 + k0), c1b = __ldg(a.tzc1 + k1c);
+    const double c2a = __ldg(a.tzc2 + k0), c2b = __ldg(a.tzc2 + k1c);
 
     const int64_t ny2 = a.ny + 2;
     const int64_t nunits = t.nlong + (t.nstrips - t.nlong) * t.nchunks;
@@ -510,14 +552,21 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
         }
         fence_mbar_init();
         const int n0 = q < S ? q : S;
-        for (int n = 0; n < n0; ++n) issue_plane<NZC == 0>(rs, a, n, n, CS, ring, full);
+        for (int n = 0; n < n0; ++n) {
+            if constexpr (UA) issue_plane_ua(rs, a, n, n, CS, ring, full);
+            else issue_plane<NZC == 0>(rs, a, n, n, CS, ring, full);
+        }
     }
     __syncthreads();
     const int total = rs->total;
     const int my_units = rs->nunits;
     if constexpr (WS) {
         if (tid >= 32 * kComputeWarps) {  // producer warpgroup
-            asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+            if constexpr (UA) {
+                asm volatile("setmaxnreg.dec.sync.aligned.u32 32;\n" ::: "memory");
+            } else {
+                asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+            }
             if (tid == 32 * kComputeWarps) {
                 for (int q = (total < S ? total : S); q < total; ++q) {
                     const int st = q % S;
@@ -527,7 +576,8 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
                     mbar_wait(&empty[st], (uint32_t)(((q / S) - 1) & 1));
 #endif
                     fence_proxy_async();
-                    issue_plane<NZC == 0>(rs, a, q, st, CS, ring, full);
+                    if constexpr (UA) issue_plane_ua(rs, a, q, st, CS, ring, full);
+                    else issue_plane<NZC == 0>(rs, a, q, st, CS, ring, full);
                 }
             }
             return;
@@ -575,11 +625,17 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
         }
     };
     auto P = [&](const double *pl, int f, int dy) -> double2 {
-        return *reinterpret_cast<const double2 *>(pl + f * CS + dy * nz + toff);
+        const double *x = pl + f * CS + dy * nz + toff;
+        if constexpr (UA) return make_double2(x[0], x[1]);  // 8-byte aligned only
+        return *reinterpret_cast<const double2 *>(x);
     };
     auto colp = [&](const double *pl, int f, int dy) -> const double * {
         return pl + f * CS + (c + 1 + dy) * nz;
     };
+    // UA: offset d of a staged plane in its slot (plane stride parity toggles
+    // it from plane to plane; the unit's first plane fixes it)
+    const int psodd = UA ? (int)(((a.ny + 2) * a.nz) & 1) : 0;
+    const int inpar = UA ? (int)(((uintptr_t)a.u >> 3) & 1) : 0;
 
     double2 U0[3], V0[3], W0[3], VM[3];
     double W0M[3];
@@ -614,9 +670,11 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
             }
         }
 
+        // UA: offset of the unit's first plane in its slot
+        int dC = UA ? (inpar ^ (int)((((ib - 1) * ny2 + (j0 - 1)) * (int64_t)nz) & 1)) : 0;
         // plane ib-1 -> slot 2 (the x-1 window of the first step)
         {
-            const double *pl = wait_next();
+            const double *pl = wait_next() + dC;
             U0[2] = P(pl, 0, 0);
             const double2 u1 = P(pl, 0, 1);
             V0[2] = P(pl, 1, 0);
@@ -631,8 +689,9 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
         }
         // plane ib -> slot 0 (items read from the leading plane)
         int pst = cst;  // stage of the current x plane, released one step later
+        dC ^= psodd;
         {
-            const double *pl = wait_next();
+            const double *pl = wait_next() + dC;
             U0[0] = P(pl, 0, 0);
             V0[0] = P(pl, 1, 0);
             W0[0] = P(pl, 2, 0);
@@ -653,8 +712,9 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
             constexpr int r = decltype(R)::value;
             constexpr int rm = (r + 2) % 3, rp = (r + 1) % 3;
             const int lst = cst;
-            const double *L = wait_next();                           // plane i+1
-            const double *C = ring + (size_t)pst * 3 * CS;           // plane i
+            const int dL = dC ^ psodd;
+            const double *L = wait_next() + dL;                      // plane i+1
+            const double *C = ring + (size_t)pst * 3 * CS + dC;      // plane i
             U0[rp] = P(L, 0, 0);
             V0[rp] = P(L, 1, 0);
             W0[rp] = P(L, 2, 0);
@@ -692,18 +752,18 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
                     (v0m.x + w0m.y) + (vmc.y + v0p.y) + (w0cM + w0pM) + (u0cQ + v0cQ) +
                     (w0cQ + vmcM) + (v0cM + w1cM) + (u0cM + w0p.x);
             } else {
-                // level k0 (never the top; level 0 is identically zero).
+                // level k0 (the top only for odd nz, UA; level 0 is identically zero).
                 // pw_sums(x1, x2+x3, x4, x5+x6, y1, .., z1, z2+z3, z4, z5+z6)
                 // with the operand wiring of kernel.py:117-128
                 su_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, u0m.x, sxu_a, u0p.x, nsxu_a,
                                     umc.x, __dadd_rn(vmc.x, vmp.x), u1c.x, __dadd_rn(v0c.x, v0p.x),
-                                    u0cM, __dadd_rn(w0cM, w0pM), u0c.y, szu, false);
+                                    u0cM, __dadd_rn(w0cM, w0pM), u0c.y, szu, top_a);
                 sv_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, v0m.x, txu_a, v0p.x, ntxu_a,
                                     vmc.x, __dadd_rn(v0c.x, vmc.x), v1c.x, __dadd_rn(v0c.x, v1c.x),
-                                    v0cM, __dadd_rn(w0cM, w1cM), v0c.y, szv, false);
+                                    v0cM, __dadd_rn(w0cM, w1cM), v0c.y, szv, top_a);
                 sw_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, w0m.x, rxu_a, w0p.x, nrxu_a,
                                     wmc.x, __dadd_rn(vmcM, vmc.x), w1c.x, __dadd_rn(v0cM, v0c.x),
-                                    w0cM, __dadd_rn(w0c.x, w0cM), w0c.y, szw, false);
+                                    w0cM, __dadd_rn(w0c.x, w0cM), w0c.y, szw, top_a);
                 // level k1 (the top when k1 == nz-1)
                 su_b = pw_sums<FMA>(tcx, tcy, c1b, c2b, u0m.y, sxu_b, u0p.y, nsxu_b,
                                     umc.y, __dadd_rn(vmc.y, vmp.y), u1c.y, __dadd_rn(v0c.y, v0p.y),
@@ -735,11 +795,22 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
                 sw_b = fwd_update(w0c.y, dt, sw_b);
             }
             if (active && !(NZC == 0 && (t.debug & 4))) {
-                store2(o0, su_a, su_b);
-                store2(o1, sv_a, sv_b);
-                store2(o2, sw_a, sw_b);
+                if constexpr (UA) {  // 8-byte-aligned pairs; odd nz: k1 may be past the column
+                    __stcs(o0, su_a);
+                    __stcs(o1, sv_a);
+                    __stcs(o2, sw_a);
+                    if (!top_a) {
+                        __stcs(o0 + 1, su_b);
+                        __stcs(o1 + 1, sv_b);
+                        __stcs(o2 + 1, sw_b);
+                    }
+                } else {
+                    store2(o0, su_a, su_b);
+                    store2(o1, sv_a, sv_b);
+                    store2(o2, sw_a, sw_b);
+                }
             }
-            if constexpr (STEP) {
+            if constexpr (STEP && !UA) {
                 if (a.push && active) {
                     if (ci == 1 || ci == a.nx || a.ny == 1) {
                         if (ci == 1 || ci == a.nx || j0 + c == 1 || j0 + c == a.ny)
@@ -757,6 +828,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
             o1 += ostep;
             o2 += ostep;
             pst = lst;
+            dC = dL;
             advance();
         };
 
@@ -867,10 +939,11 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         t.l2hint = (L.flags & PWADV_FLAG_L2_UNIT_HEAD) ? 1 : 0;
         t.nstrips = plan.nstrips;
         t.nlong = plan.nlong;
+        t.ua = plan.elem;
         void (*kern)(BoxArgs, TileCfg) = nullptr;
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
         // compile-time layout for the BASELINE depths at the default tile
-        const int nzc = (plan.maxt == 512 && plan.tj * plan.kp == 384 &&
+        const int nzc = (!plan.elem && plan.maxt == 512 && plan.tj * plan.kp == 384 &&
                          (L.nz == 64 || L.nz == 128) &&
                          !(L.flags & (PWADV_FLAG_GENERIC | PWADV_FLAG_DEBUG_NO_COMPUTE |
                                       PWADV_FLAG_DEBUG_NO_STORE)))
@@ -887,6 +960,18 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         PWADV_PICK_NZ(64, false)
         PWADV_PICK_NZ(128, true)
 #undef PWADV_PICK_NZ
+#define PWADV_PICK_ELEM(FX)                                                      \
+    if (plan.elem && fix == FX) {                                                \
+        if (L.step)                                                              \
+            kern = fma ? k_advect_xmarch<true, true, 512, FX, 0, true>           \
+                       : k_advect_xmarch<false, true, 512, FX, 0, true>;         \
+        else                                                                     \
+            kern = fma ? k_advect_xmarch<true, false, 512, FX, 0, true>          \
+                       : k_advect_xmarch<false, false, 512, FX, 0, true>;        \
+    }
+        PWADV_PICK_ELEM(false)
+        PWADV_PICK_ELEM(true)
+#undef PWADV_PICK_ELEM
 #define PWADV_PICK(MT, FX)                                                       \
     if (!kern && plan.maxt == MT && fix == FX) {                                 \
         if (L.step)                                                              \
@@ -972,16 +1057,32 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
     return PWADV_OK;
 }
 
+// doubles per field slot of a ring stage (k_advect_xmarch's CS)
+static size_t slot_doubles(int64_t tj, int64_t nz, bool ua)
+{
+    const int64_t run = (tj + 2) * nz;
+    return (size_t)(ua ? ((run + 3) & ~(int64_t)1) : run);
+}
+
 bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
 {
-    if (L.flags & (PWADV_FLAG_SIMPLE | PWADV_FLAG_RIM)) return false;
+    if (L.flags & (PWADV_FLAG_SIMPLE | PWADV_FLAG_RIM | PWADV_FLAG_MARCH)) return false;
     const int64_t nz = L.nz;
-    if (nz % 2 != 0 || nz > 1024) return false;
-    // 16-byte alignment for the bulk copies and the paired loads/stores
+    // 16-byte alignment and even nz for 16-byte-aligned tile runs and the
+    // paired loads/stores; otherwise UA (unaligned runs: the copies start up to
+    // one element early, scalar shared loads and stores) — warp-specialised
+    // only, u, v, w with the same 16-byte phase, and not for the fused halo
+    // push (it stores pairs into the peers' halos)
     const uintptr_t al = (uintptr_t)L.u | (uintptr_t)L.v | (uintptr_t)L.w | (uintptr_t)L.o0 |
                          (uintptr_t)L.o1 | (uintptr_t)L.o2;
-    if (al & 15) return false;
-    const int kp = (int)(nz / 2);
+    const bool ua = (nz % 2 != 0) || (al & 15) || (L.flags & PWADV_FLAG_UNALIGNED);
+    const uintptr_t inpar = ((uintptr_t)L.u ^ (uintptr_t)L.v) | ((uintptr_t)L.u ^ (uintptr_t)L.w);
+    if (ua && ((al & 7) || (inpar & 8) || L.peers || (L.max_threads > 0 && L.max_threads != 512) ||
+               (L.flags & (PWADV_FLAG_DEBUG_NO_COMPUTE | PWADV_FLAG_DEBUG_NO_STORE))))
+        return false;
+    if (nz > 1024) return false;
+    p->elem = ua ? 1 : 0;
+    const int kp = (int)((nz + 1) / 2);
     const int64_t nby = L.y1 - L.y0, nbx = L.x1 - L.x0;
     // thread budget per CTA (register file / CTA): 384 by default, which
     // leaves ~168 registers per thread for the rolled x-window
@@ -1003,7 +1104,7 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     if (per_sm > 1) smem_cap = (size_t)(228 * 1024) / per_sm - bar_bytes - 1024 - 1024;
     int stages = 0;
     for (;;) {
-        const size_t stage_bytes = (size_t)3 * (tj + 2) * nz * sizeof(double);
+        const size_t stage_bytes = (size_t)3 * slot_doubles(tj, nz, ua) * sizeof(double);
         int smax = (int)(smem_cap / stage_bytes);
         if (smax > 16) smax = 16;  // RingState::released
         // default ring depth 5 (tools/sweep.py); single-round plans deepen it
@@ -1018,7 +1119,7 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     p->kp = kp;
     p->stages = stages;
     p->threads = maxt == 512 ? 512 : round_up(tj * kp, 32);
-    p->smem = (size_t)stages * 3 * (tj + 2) * nz * sizeof(double) + 2 * stages * sizeof(uint64_t) +
+    p->smem = (size_t)stages * 3 * slot_doubles(tj, nz, ua) * sizeof(double) + 2 * stages * sizeof(uint64_t) +
               sizeof(RingState);
     p->nstrips = (nby + tj - 1) / tj;
     // Work units dealt round-robin to one wave of CTAs. Whole strips fill
@@ -1067,7 +1168,7 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     // sustained); multi-round plans keep 5 (C2 129 vs 125; a cold C4 launch
     // read 4% more DRAM with 6).
     if (L.stages <= 0 && maxt == 512 && p->rounds == 1) {
-        const size_t stage_bytes = (size_t)3 * (tj + 2) * nz * sizeof(double);
+        const size_t stage_bytes = (size_t)3 * slot_doubles(tj, nz, ua) * sizeof(double);
         if ((size_t)6 * stage_bytes <= smem_cap) {
             p->stages = 6;
             p->smem = (size_t)6 * stage_bytes + 2 * 6 * sizeof(uint64_t) + sizeof(RingState);

@@ -218,4 +218,19 @@ __device__ __forceinline__ void store2(double *p, double a, double b)
     __stcs(reinterpret_cast<double2 *>(p), make_double2(a, b));
 }
 
+// 8-byte global -> shared asynchronous copy (LDGSTS; any 8-byte alignment)
+__device__ __forceinline__ void cp_async8(void *dst_smem, const void *src_gmem)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem)
+                 : "memory");
+}
+
+// arrive on `bar` once this thread's earlier cp.async copies have landed; the
+// barrier's expected count includes this arrival (.noinc)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar)
+{
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
 }  // namespace pwadv

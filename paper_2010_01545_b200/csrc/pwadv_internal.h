@@ -36,6 +36,7 @@ struct XmarchPlan {
     int64_t nstrips;
     int64_t rounds;  // units per CTA (the kernel's unit table holds kMaxUnitsPerCta)
     int64_t nlong;   // strips run as whole-X units (full rounds)
+    int elem;        // 1: unaligned tile runs (UA kernels: odd nz, 8-byte alignment)
 };
 
 // cached attributes of the current device (lazily filled, thread-safe)

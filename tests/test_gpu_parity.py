@@ -419,7 +419,8 @@ def test_tall_and_odd_columns_bitwise(shape):
     got, dims = gpu_advect(u, v, w, *args)
     assert_bitwise(got, oracle.advect(u, v, w, *args), shape)
     plan = device.describe_plan(dims)
-    assert plan["kernel"] == ("xmarch" if nz in (300, 512) else "march")
+    assert plan["kernel"] == ("xmarch" if nz in (300, 512) else
+                              "xmarch_elem" if nz % 2 and nz < 1024 else "march")
     # and the one-thread-per-point kernel, forced, agrees
     got_s, _ = gpu_advect(u, v, w, *args, "simple")
     assert_bitwise(got_s, oracle.advect(u, v, w, *args), (shape, "simple"))
@@ -616,6 +617,56 @@ def test_random_medium_shapes_exercise_every_schedule():
                                       ref[1:-1, 1:-1].view(np.int64)), (nx, ny, nz)
 
 
+def test_element_ring_xmarch_random_shapes():
+    """The element-ring X-march (8-byte cp.async into padded columns): odd nz
+    with whole-X rounds, chunked tails, partial strips and columns that
+    straddle warps; 8-byte-aligned fields at even nz; the element ring forced
+    at nz = 64 with explicit tilings and ring depths — bit-exact against the
+    oracle (K1 and K4), the FMA build within 1e-12."""
+    rng = np.random.default_rng(77)
+    cases = [((300, 1800, 63), {}), ((257, 97, 33), {}), ((5, 1785, 127), {}),
+             ((64, 301, 99), {}), ((150, 150, 5), {}), ((31, 29, 3), {}),
+             ((96, 200, 64), {"tile_j": 7, "stages": 3}), ((96, 200, 64), {"chunks": 5})]
+    for n, ((nx, ny, nz), kw) in enumerate(cases):
+        seed = int(rng.integers(0, 2**31))
+        u, v, w = oracle.fill_random(nx, ny, nz, seed, baseline=True)
+        co = oracle.baseline_coefficients(seed, nz)
+        args = (co["tcx"], co["tcy"], co["tzc1"], co["tzc2"])
+        dims = pw.make_grid(nx, ny, nz)
+        want = oracle.advect(u, v, w, *args, engines=oracle.host_threads())
+        got, _ = gpu_advect(u, v, w, *args, "xmarch_elem", **kw)
+        assert device.describe_plan(dims, opts=device.make_opts("xmarch_elem", **kw))["kernel"] \
+            == "xmarch_elem"
+        assert_bitwise(got, want, (nx, ny, nz, kw))
+        dco = pw.AdvectionCoefficients(*args)
+        if n % 2 == 0:  # the fused step, default plan
+            du, dv, dw = to_dev(u, v, w)
+            nxt = device.alloc_fields(dims, "cuda")
+            device.step(du, dv, dw, dco, 0.1, nxt)
+            for g, f, s in zip(nxt, (u, v, w), want):
+                assert np.array_equal(g.cpu().numpy()[1:-1, 1:-1].view(np.int64),
+                                      (f + 0.1 * s)[1:-1, 1:-1].view(np.int64)), (nx, ny, nz)
+        if n == 1:  # FMA build
+            gf, _ = gpu_advect(u, v, w, *args, "xmarch_elem_fma")
+            assert oracle.compare(gf, want)["normwise_rel"] <= 1e-12
+        if nz % 2 == 0:  # 8-byte (not 16-byte) aligned device fields: default plan
+            nn = (nx + 2) * (ny + 2) * nz
+            bufs = [torch.empty(nn + 1, dtype=torch.float64, device="cuda") for _ in range(6)]
+            fin = [b[1:].view(dims.padded_shape) for b in bufs[:3]]
+            fout = [b[1:].view(dims.padded_shape) for b in bufs[3:]]
+            for t, a in zip(fin, (u, v, w)):
+                t.copy_(torch.from_numpy(a))
+            for t in fout:
+                t.zero_()
+            device.advect(*fin, dco, fout)
+            assert_bitwise([t.cpu().numpy() for t in fout], want, (nx, ny, nz, "8-byte aligned"))
+            # u 16-byte aligned, v and w not: different phases (the general march)
+            fin[0] = bufs[0][:nn].view(dims.padded_shape)
+            fin[0].copy_(torch.from_numpy(u))
+            device.advect(*fin, dco, fout)
+            assert_bitwise([t.cpu().numpy() for t in fout], want, (nx, ny, nz, "mixed phases"))
+
+
 def test_back_to_back_dependent_launches():
     """Programmatic dependent launch: K1 launches whose inputs are the previous
     launch's outputs, and K4 chained directly (no wrap in between), with no
@@ -714,8 +765,10 @@ def test_dropin_tour_example_runs():
 @pytest.mark.parametrize("shape", [(9, 7, 3), (20, 13, 33), (37, 29, 63), (12, 9, 65), (6, 5, 127),
                                    (3, 2, 1030), (40, 1, 2)])
 def test_general_march_kernel_bitwise(shape):
-    """K1m (odd nz, tall columns, 8-byte-aligned fields): whole grid, a sub-box,
-    the fused step and the FMA build against the oracle; its plan is 'march'."""
+    """The general shapes (odd nz, tall columns, 8-byte-aligned fields): whole
+    grid, a sub-box, the fused step and the FMA build against the oracle, on
+    the default plan ('xmarch_elem' for odd nz up to 1023, 'march' above) and
+    with K1m and the element ring each forced."""
     nx, ny, nz = shape
     u, v, w = oracle.fill_random(nx, ny, nz, 31, baseline=True)
     co = oracle.baseline_coefficients(31, nz)
@@ -724,8 +777,12 @@ def test_general_march_kernel_bitwise(shape):
     want = oracle.advect(u, v, w, *args)
     got, _ = gpu_advect(u, v, w, *args)
     if nz % 2:
-        assert device.describe_plan(dims)["kernel"] == "march"
+        assert device.describe_plan(dims)["kernel"] == ("xmarch_elem" if nz < 1024 else "march")
     assert_bitwise(got, want, shape)
+    # K1m and the element-ring X-march, each forced, agree too
+    for variant in ("march", "xmarch_elem"):
+        got_v, _ = gpu_advect(u, v, w, *args, variant)
+        assert_bitwise(got_v, want, (shape, variant))
     # 8-byte (not 16-byte) aligned device fields: views one double into a buffer
     n = (nx + 2) * (ny + 2) * nz
     bufs = [torch.empty(n + 1, dtype=torch.float64, device="cuda") for _ in range(6)]
