@@ -48,8 +48,9 @@ enum {
     PWADV_E_RANGE = -3,     /* sub-box outside the interior / bad slab */
     PWADV_E_CUDA = -4,      /* CUDA launch or runtime error */
     PWADV_E_ARG = -5,       /* other invalid argument (mode, tuning) */
-    PWADV_E_ALIGN = -6      /* pointer not 8-byte aligned (the X-march also wants 16 bytes;
-                               8-byte-aligned fields run on the one-thread-per-point kernel) */
+    PWADV_E_ALIGN = -6      /* pointer not 8-byte aligned (16-byte-aligned fields take the
+                               X-march's aligned form, 8-byte-aligned ones its unaligned-run
+                               form) */
 };
 
 /* flags for pwadv_opts.flags */
