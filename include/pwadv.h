@@ -124,7 +124,7 @@ int pwadv_advect_box_f64(const double *u, const double *v, const double *w,
 typedef struct pwadv_plan_info {
     int32_t kernel;        /* 1 = X-march (bulk-copy plane ring), 2 = one-thread-per-point,
                               3 = general march (register x-window, cached loads: tall
-                              columns, fused halo push at odd nz / 8-byte alignment),
+                              columns, inputs with different 16-byte phases),
                               4 = X-march with unaligned tile runs (odd nz, 8-byte-aligned
                               fields) */
     int32_t tile_j, threads_per_column, stages, threads, grid;

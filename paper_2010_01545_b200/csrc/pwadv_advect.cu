@@ -111,6 +111,16 @@ __device__ __noinline__ void push_pair(const BoxArgs *A, int64_t i, int64_t j, i
     push_boundary<2>(*A, i, j, k0, pa, pb, pc);
 }
 
+// As push_pair for the X-march's UA form: 8-byte stores, and for odd nz the
+// pair's second level may be past the column.
+__device__ __noinline__ void push_pair_ua(const BoxArgs *A, int64_t i, int64_t j, int64_t k0,
+                                          double a0, double a1, double b0, double b1, double c0,
+                                          double c1)
+{
+    push_boundary<1>(*A, i, j, k0, &a0, &b0, &c0);
+    if (k0 + 1 < A->nz) push_boundary<1>(*A, i, j, k0 + 1, &a1, &b1, &c1);
+}
+
 struct TileCfg {
     int tj;           // columns per strip
     int kp;           // threads per column (= nz/2)
@@ -476,7 +486,7 @@ __host__ __device__ constexpr int ctas_per_sm(int maxt) { return maxt <= 128 ? 3
 // offset from a per-plane base register (the BASELINE nz = 64 / 128 cases).
 // UA: unaligned tile runs (issue_plane_ua) — each staged plane sits at offset
 // d in its slot, scalar shared loads and output stores (odd nz or 8-byte-
-// aligned fields; warp-specialised kernel only, no fused halo push).
+// aligned fields; warp-specialised kernel only).
 template <bool FMA, bool STEP, int MAXT, bool FIX, int NZC = 0, bool UA = false>
 __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     k_advect_xmarch(const __grid_constant__ BoxArgs a, const __grid_constant__ TileCfg t)
@@ -810,16 +820,31 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
                     store2(o2, sw_a, sw_b);
                 }
             }
-            if constexpr (STEP && !UA) {
+            if constexpr (STEP) {
                 if (a.push && active) {
                     if (ci == 1 || ci == a.nx || a.ny == 1) {
-                        if (ci == 1 || ci == a.nx || j0 + c == 1 || j0 + c == a.ny)
-                            push_pair(&a, ci, j0 + c, k0, su_a, su_b, sv_a, sv_b, sw_a, sw_b);
+                        if (ci == 1 || ci == a.nx || j0 + c == 1 || j0 + c == a.ny) {
+                            if constexpr (UA)
+                                push_pair_ua(&a, ci, j0 + c, k0, su_a, su_b, sv_a, sv_b, sw_a, sw_b);
+                            else
+                                push_pair(&a, ci, j0 + c, k0, su_a, su_b, sv_a, sv_b, sw_a, sw_b);
+                        }
                     } else if (ydir >= 0) {
                         const int64_t off = (ci * ystr + ypj) * (int64_t)nz + k0;
-                        store2(a.peers.u[ydir] + off, su_a, su_b);
-                        store2(a.peers.v[ydir] + off, sv_a, sv_b);
-                        store2(a.peers.w[ydir] + off, sw_a, sw_b);
+                        if constexpr (UA) {
+                            a.peers.u[ydir][off] = su_a;
+                            a.peers.v[ydir][off] = sv_a;
+                            a.peers.w[ydir][off] = sw_a;
+                            if (!top_a) {
+                                a.peers.u[ydir][off + 1] = su_b;
+                                a.peers.v[ydir][off + 1] = sv_b;
+                                a.peers.w[ydir][off + 1] = sw_b;
+                            }
+                        } else {
+                            store2(a.peers.u[ydir] + off, su_a, su_b);
+                            store2(a.peers.v[ydir] + off, sv_a, sv_b);
+                            store2(a.peers.w[ydir] + off, sw_a, sw_b);
+                        }
                     }
                 }
             }
@@ -1070,14 +1095,13 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     const int64_t nz = L.nz;
     // 16-byte alignment and even nz for 16-byte-aligned tile runs and the
     // paired loads/stores; otherwise UA (unaligned runs: the copies start up to
-    // one element early, scalar shared loads and stores) — warp-specialised
-    // only, u, v, w with the same 16-byte phase, and not for the fused halo
-    // push (it stores pairs into the peers' halos)
+    // one element early, scalar shared loads and stores, also into the peers'
+    // halos) — warp-specialised only, u, v, w with the same 16-byte phase
     const uintptr_t al = (uintptr_t)L.u | (uintptr_t)L.v | (uintptr_t)L.w | (uintptr_t)L.o0 |
                          (uintptr_t)L.o1 | (uintptr_t)L.o2;
     const bool ua = (nz % 2 != 0) || (al & 15) || (L.flags & PWADV_FLAG_UNALIGNED);
     const uintptr_t inpar = ((uintptr_t)L.u ^ (uintptr_t)L.v) | ((uintptr_t)L.u ^ (uintptr_t)L.w);
-    if (ua && ((al & 7) || (inpar & 8) || L.peers || (L.max_threads > 0 && L.max_threads != 512) ||
+    if (ua && ((al & 7) || (inpar & 8) || (L.max_threads > 0 && L.max_threads != 512) ||
                (L.flags & (PWADV_FLAG_DEBUG_NO_COMPUTE | PWADV_FLAG_DEBUG_NO_STORE))))
         return false;
     if (nz > 1024) return false;

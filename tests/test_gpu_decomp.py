@@ -102,7 +102,8 @@ def test_emulated_decomposed_time_stepping(px, py):
 
 
 @pytest.mark.parametrize("px,py,shape", [(2, 4, (48, 40, 16)), (1, 2, (30, 26, 64)), (2, 2, (25, 23, 6)),
-                                         (1, 1, (20, 18, 64)), (3, 2, (36, 30, 128))])
+                                         (1, 1, (20, 18, 64)), (3, 2, (36, 30, 128)),
+                                         (2, 2, (25, 23, 7)), (2, 4, (48, 40, 33))])
 def test_emulated_fused_push_stepping(px, py, shape):
     """K4 with the exchange fused in (peer stores + one barrier per step) ==
     single-domain stepping, bitwise, halos included."""
