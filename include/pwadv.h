@@ -177,6 +177,39 @@ int pwadv_step_push_f64(const double *u, const double *v, const double *w,
                         const double *tzc1, const double *tzc2, double dt,
                         const pwadv_peers *peers, const pwadv_opts *opts, void *stream);
 
+/*
+ * K1 with the halo exchange fused in (pull): su, sv, sw of this block's whole
+ * interior, with every halo cell the stencil reads loaded from the
+ * neighbours' CURRENT u, v, w (src: the same peer table layout, extents as
+ * above) instead of this block's halos — x-halo planes from the x neighbours'
+ * last / first interior plane, y-halo columns from the y neighbours', the
+ * corners u(0, ny+1) and v(nx+1, 0) from the diagonal ones: the values a
+ * two-phase periodic exchange (wrap_halos, grid.py:203-208) would have put
+ * there, so the result is bit-identical to exchange-then-pwadv_advect_f64.
+ * This block's halos are neither read nor written. The neighbours' interiors
+ * must be final when the kernel runs (one cross-rank barrier before the call
+ * when they change). Peer buffers 16-byte aligned; needs the aligned X-march
+ * (even nz <= 768, 16-byte-aligned fields), else PWADV_E_ARG. An undivided
+ * axis passes this block's own buffers as its neighbours (periodic wrap with
+ * no halo copy).
+ */
+int pwadv_advect_pull_f64(const double *u, const double *v, const double *w,
+                          double *su, double *sv, double *sw,
+                          int64_t nx, int64_t ny, int64_t nz,
+                          double tcx, double tcy,
+                          const double *tzc1, const double *tzc2,
+                          const pwadv_peers *src, const pwadv_opts *opts, void *stream);
+
+/* K4 with the halo pull: as pwadv_step_f64 over the whole interior, halos
+ * loaded from src as in pwadv_advect_pull_f64; the new buffers' halos are not
+ * written (the next step pulls again). */
+int pwadv_step_pull_f64(const double *u, const double *v, const double *w,
+                        double *u_new, double *v_new, double *w_new,
+                        int64_t nx, int64_t ny, int64_t nz,
+                        double tcx, double tcy,
+                        const double *tzc1, const double *tzc2, double dt,
+                        const pwadv_peers *src, const pwadv_opts *opts, void *stream);
+
 /* CUDA IPC helpers for the peer buffers of pwadv_step_push_f64 (one process
  * per GPU): export a device allocation (handle: 64 opaque bytes, plus the
  * pointer's byte offset inside its allocation), open a peer's export, close. */

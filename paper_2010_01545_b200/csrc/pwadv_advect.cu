@@ -56,8 +56,10 @@ struct BoxArgs {
     int64_t x0, x1, y0, y1;  // interior box, 1-based, half-open
     unsigned long long *trace;  // profiling only: per-plane issue/arrival timestamps (CTA 0)
     int push;                   // fused step only: also store boundary values into peers' halos
+    int pull;                   // X-march: load halo cells from the peers' current buffers
     int rim;                    // simple kernel: only the one-cell rim of the box (x0/x1-1/y0/y1-1)
-    pwadv_peers peers;          // (include/pwadv.h) the neighbours' new buffers and extents
+    pwadv_peers peers;          // (include/pwadv.h) push: the neighbours' new buffers; pull:
+                                // their current u, v, w; and their extents
 };
 
 // Fused halo push (K4 + exchange in one kernel): an interior boundary value of
@@ -131,6 +133,8 @@ struct TileCfg {
     int64_t nstrips;  // ceil((y1-y0)/tj)
     int64_t nlong;    // strips 0..nlong-1 are whole-X units (full rounds); the rest are chunked
     int ua;           // planned UA (unaligned tile runs) — informational
+    int rot;          // strips are rotated by this much (halo pull: the two y-face strips,
+                      // whose tiles take six copies per plane, fall in the chunked tail)
 };
 
 // Work units (unit_at) are dealt round-robin to the CTAs: CTA b runs units
@@ -150,7 +154,7 @@ __device__ __forceinline__ Unit unit_at(const BoxArgs &a, const TileCfg &t, int6
     const int64_t nxr = a.x1 - a.x0;
     Unit w;
     if (u < t.nlong) {
-        w.strip = u;
+        w.strip = u + t.rot < t.nstrips ? u + t.rot : u + t.rot - t.nstrips;
         w.ib = a.x0;
         w.ie = a.x1;
         return w;
@@ -158,7 +162,8 @@ __device__ __forceinline__ Unit unit_at(const BoxArgs &a, const TileCfg &t, int6
     const int64_t tail = t.nstrips - t.nlong;
     const int64_t v = u - t.nlong;
     const int64_t chunk = v / tail;
-    w.strip = t.nlong + (v - chunk * tail);
+    w.strip = t.nlong + (v - chunk * tail) + t.rot;
+    if (w.strip >= t.nstrips) w.strip -= t.nstrips;
     w.ib = a.x0 + (nxr * chunk) / t.nchunks;
     w.ie = a.x0 + (nxr * (chunk + 1)) / t.nchunks;
     return w;
@@ -394,6 +399,12 @@ struct RingState {
     int first[kMaxUnitsPerCta + 1];   // first sequence number of each unit
     uint32_t bytes[kMaxUnitsPerCta];  // bytes per field per plane of each unit
     int64_t src[kMaxUnitsPerCta];     // element offset of the unit's first plane tile
+    int32_t ui0[kMaxUnitsPerCta];     // halo pull: plane index of the unit's first plane (ib - 1)
+    int32_t uj0[kMaxUnitsPerCta];     //   first interior column of its strip
+    int32_t utj[kMaxUnitsPerCta];     //   columns of its strip
+    int32_t dsto[kMaxUnitsPerCta];    //   where the local run lands in a slot (doubles)
+    int64_t clo[kMaxUnitsPerCta];     //   y-face units: YM / YP halo column of the unit's first
+    int64_t chi[kMaxUnitsPerCta];     //   plane in the neighbour's field (elements), or -1
     int l2hint;                       // TileCfg::l2hint
     int released[16];                 // per stage: warps done with its current plane
 };
@@ -405,20 +416,76 @@ __device__ __forceinline__ unsigned long long gtime()
     return t;
 }
 
+// Halo pull (K1 with the exchange fused in, pwadv_advect_pull_f64): the halo
+// cells of plane q's tile are copied from the neighbours' current buffers
+// instead of this block's halos — an x-halo plane (i = 0 / nx+1) from the x
+// neighbour's last / first interior plane, the y-halo columns (j = 0 / ny+1)
+// of an interior plane from the y neighbour's last / first interior column,
+// and the two corner columns the stencil reads, u(0, ny+1) and v(nx+1, 0),
+// from the diagonal neighbours (wrap_halos' semantics, grid.py:203-208: the
+// X pass then the Y pass over the X halos). Peer buffers are read over NVLink
+// by the same bulk copies; cells the stencil never reads (the other corner
+// cells) are left unfilled. At most three pieces per field and plane, and
+// only for halo planes and y-face strips: all other tiles are one local run.
+__device__ __forceinline__ void copy_cols(double *dst, const double *u, const double *v,
+                                          const double *w, int64_t off, int CS, uint32_t bytes,
+                                          uint64_t *bar)
+{
+    bulk_g2s(dst, u + off, bytes, bar);
+    bulk_g2s(dst + CS, v + off, bytes, bar);
+    bulk_g2s(dst + 2 * CS, w + off, bytes, bar);
+}
+
+// x-halo plane i (0 or nx+1) of unit k.
+__device__ __forceinline__ void issue_plane_pull(const RingState *rs, const BoxArgs &a, int k,
+                                                 int64_t i, int st, int CS, double *ring,
+                                                 uint64_t *full)
+{
+    const int64_t jlo = rs->uj0[k] - 1, jhi = rs->uj0[k] + rs->utj[k];  // tile columns [jlo, jhi]
+    const int64_t nz = a.nz, ny = a.ny, ny2 = a.ny + 2;
+    const uint32_t cb = (uint32_t)(nz * sizeof(double));  // bytes per column
+    const pwadv_peers &p = a.peers;
+    const int64_t c0 = jlo > 1 ? jlo : 1, c1 = jhi < ny ? jhi : ny;  // interior columns of the tile
+    const bool lo = jlo == 0, hi = jhi == ny + 1;
+    double *dst = ring + (size_t)st * 3 * CS;
+    uint64_t *bar = &full[st];
+    (void)c1;
+    if (i == 0) {  // x-lo halo plane: the XM neighbour's last plane; u(0, ny+1) from XMYP
+        const uint32_t b = (uint32_t)(c1 - jlo + 1) * cb;
+        mbar_arrive_expect_tx(bar, 3 * b + (hi ? cb : 0));
+        const int d = PWADV_NB_XM;
+        copy_cols(dst, p.u[d], p.v[d], p.w[d], (p.nx[d] * ny2 + jlo) * nz, CS, b, bar);
+        if (hi) {
+            const int e = PWADV_NB_XMYP;
+            bulk_g2s(dst + (jhi - jlo) * nz, p.u[e] + (p.nx[e] * (p.ny[e] + 2) + 1) * nz, cb, bar);
+        }
+    } else {  // x-hi halo plane: XP's first plane; v(nx+1, 0) from XPYM
+        const uint32_t b = (uint32_t)(jhi - c0 + 1) * cb;
+        mbar_arrive_expect_tx(bar, 3 * b + (lo ? cb : 0));
+        const int d = PWADV_NB_XP;
+        copy_cols(dst + (c0 - jlo) * nz, p.u[d], p.v[d], p.w[d], (ny2 + c0) * nz, CS, b, bar);
+        if (lo) {
+            const int e = PWADV_NB_XPYM;
+            bulk_g2s(dst + CS, p.v[e] + ((p.ny[e] + 2) + p.ny[e]) * nz, cb, bar);
+        }
+    }
+}
+
 // Issue the bulk copies of plane q (3 fields, one contiguous run each) into
 // stage st, completing on full[st]. A table lookup and one multiply-add: the
 // warp that issues must not fall behind the others (it gates the next refill).
-template <bool TRACE = true>
+template <bool TRACE = true, bool PULL = false>
 __device__ __forceinline__ void issue_plane(const RingState *rs, const BoxArgs &a, int q, int st,
                                             int CS, double *ring, uint64_t *full)
 {
     if (TRACE && a.trace && blockIdx.x == 0 && q < 4096) a.trace[2 * q] = gtime();
     int k = 0;
     while (rs->first[k + 1] <= q) ++k;
+    double *dst = ring + (size_t)st * 3 * CS;
+    if constexpr (PULL) dst += rs->dsto[k] > 0 ? rs->dsto[k] : 0;  // y-face unit: trimmed run
     const uint32_t bytes = rs->bytes[k];
     const int64_t off = rs->src[k] + (int64_t)(q - rs->first[k]) * ((a.ny + 2) * a.nz);
     mbar_arrive_expect_tx(&full[st], 3 * bytes);
-    double *dst = ring + (size_t)st * 3 * CS;
     // the first two planes of a unit are read again, much later, by the unit
     // of the previous X chunk (as its last two planes): keep them in L2
     if (rs->l2hint && q - rs->first[k] < 2) {
@@ -487,13 +554,14 @@ __host__ __device__ constexpr int ctas_per_sm(int maxt) { return maxt <= 128 ? 3
 // UA: unaligned tile runs (issue_plane_ua) — each staged plane sits at offset
 // d in its slot, scalar shared loads and output stores (odd nz or 8-byte-
 // aligned fields; warp-specialised kernel only).
-template <bool FMA, bool STEP, int MAXT, bool FIX, int NZC = 0, bool UA = false>
+template <bool FMA, bool STEP, int MAXT, bool FIX, int NZC = 0, bool UA = false, bool PULL = false>
 __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     k_advect_xmarch(const __grid_constant__ BoxArgs a, const __grid_constant__ TileCfg t)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     static_assert(NZC == 0 || (MAXT == 512 && 384 % (NZC / 2) == 0), "compile-time layout: WS only");
     static_assert(!UA || (MAXT == 512 && NZC == 0), "unaligned runs: warp-specialised, run-time layout");
+    static_assert(!PULL || (MAXT == 512 && !UA), "halo pull: warp-specialised, aligned runs");
     // programmatic dependent launch (launch_box): wait until the previous grid
     // on the stream has completed and its writes are visible (they may be our
     // inputs) before any global access, and let the next grid be scheduled
@@ -549,6 +617,21 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
             rs->first[k] = q;
             rs->bytes[k] = (uint32_t)((tjs + 2) * nz * sizeof(double));
             rs->src[k] = ((w.ib - 1) * ny2 + (j0 - 1)) * nz;
+            rs->ui0[k] = (int32_t)(w.ib - 1);
+            rs->uj0[k] = (int32_t)j0;
+            rs->utj[k] = (int32_t)tjs;
+            rs->dsto[k] = -1;  // not a y-face unit
+            if constexpr (PULL) {  // y-face unit: its local run skips the halo columns
+                const bool lo = j0 == 1, hi = j0 + tjs == a.ny + 1;
+                const pwadv_peers &pp = a.peers;
+                rs->clo[k] = lo ? ((w.ib - 1) * (pp.ny[PWADV_NB_YM] + 2) + pp.ny[PWADV_NB_YM]) * nz : -1;
+                rs->chi[k] = hi ? ((w.ib - 1) * (pp.ny[PWADV_NB_YP] + 2) + 1) * nz : -1;
+                if (lo || hi) {
+                    rs->src[k] += lo ? nz : 0;
+                    rs->bytes[k] -= (uint32_t)(((lo ? 1 : 0) + (hi ? 1 : 0)) * nz * sizeof(double));
+                    rs->dsto[k] = lo ? nz : 0;
+                }
+            }
             q += (int)(w.ie - w.ib + 2);
         }
         rs->first[k] = q;
@@ -561,7 +644,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
             rs->released[s] = 0;
         }
         fence_mbar_init();
-        const int n0 = q < S ? q : S;
+        const int n0 = PULL ? 0 : (q < S ? q : S);  // pull: the producer warp issues all
         for (int n = 0; n < n0; ++n) {
             if constexpr (UA) issue_plane_ua(rs, a, n, n, CS, ring, full);
             else issue_plane<NZC == 0>(rs, a, n, n, CS, ring, full);
@@ -572,10 +655,54 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     const int my_units = rs->nunits;
     if constexpr (WS) {
         if (tid >= 32 * kComputeWarps) {  // producer warpgroup
-            if constexpr (UA) {
+            if constexpr (UA || PULL) {  // 4 x 32 x 32 + 12 x 32 x 160 = 64 K registers
                 asm volatile("setmaxnreg.dec.sync.aligned.u32 32;\n" ::: "memory");
             } else {
                 asm volatile("setmaxnreg.dec.sync.aligned.u32 24;\n" ::: "memory");
+            }
+            if constexpr (PULL) {
+                // the producer thread: x-halo planes from the x / diagonal
+                // neighbours, else the local run (trimmed on y-face units) plus
+                // the y-halo columns from YM / YP, with per-unit offsets
+                // precomputed in the unit table (this loop must keep pace
+                // with the consumers).
+                if (tid == 32 * kComputeWarps) {
+                    const pwadv_peers &pp = a.peers;
+                    const int64_t slo = (pp.ny[PWADV_NB_YM] + 2) * a.nz, shi = (pp.ny[PWADV_NB_YP] + 2) * a.nz;
+                    const uint32_t cb = (uint32_t)(nz * sizeof(double));
+                    int k = 0;
+                    for (int q = 0; q < total; ++q) {
+                        while (rs->first[k + 1] <= q) ++k;
+                        const int st = q % S;
+                        if (q >= S) mbar_wait(&empty[st], (uint32_t)(((q / S) - 1) & 1));
+                        fence_proxy_async();
+                        const int rel = q - rs->first[k];
+                        const int64_t i = rs->ui0[k] + rel;
+                        if (i == 0 || i == a.nx + 1) {
+                            issue_plane_pull(rs, a, k, i, st, CS, ring, full);
+                            continue;
+                        }
+                        // the local run (trimmed on y-face units) and, on those,
+                        // the y-halo columns from YM / YP
+                        double *dst = ring + (size_t)st * 3 * CS;
+                        const int64_t lo = rs->clo[k], hi = rs->chi[k];
+                        const uint32_t bytes = rs->bytes[k];
+                        const int64_t off = rs->src[k] + (int64_t)rel * ((a.ny + 2) * a.nz);
+                        mbar_arrive_expect_tx(&full[st], 3 * (bytes + (lo >= 0 ? cb : 0) + (hi >= 0 ? cb : 0)));
+                        copy_cols(dst + (rs->dsto[k] > 0 ? rs->dsto[k] : 0), a.u, a.v, a.w, off, CS, bytes,
+                                  &full[st]);
+                        if (lo >= 0) {
+                            const int d = PWADV_NB_YM;
+                            copy_cols(dst, pp.u[d], pp.v[d], pp.w[d], lo + rel * slo, CS, cb, &full[st]);
+                        }
+                        if (hi >= 0) {
+                            const int d = PWADV_NB_YP;
+                            copy_cols(dst + (rs->utj[k] + 1) * nz, pp.u[d], pp.v[d], pp.w[d], hi + rel * shi,
+                                      CS, cb, &full[st]);
+                        }
+                    }
+                }
+                return;
             }
             if (tid == 32 * kComputeWarps) {
                 for (int q = (total < S ? total : S); q < total; ++q) {
@@ -587,7 +714,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
 #endif
                     fence_proxy_async();
                     if constexpr (UA) issue_plane_ua(rs, a, q, st, CS, ring, full);
-                    else issue_plane<NZC == 0>(rs, a, q, st, CS, ring, full);
+                    else issue_plane<NZC == 0, PULL>(rs, a, q, st, CS, ring, full);
                 }
             }
             return;
@@ -880,6 +1007,17 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
 
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
+// the warp-specialised X-march instantiation for (step, fma)
+template <int NZ, bool FX, bool UA, bool PULL>
+static void (*pick_ws(bool step, bool fma))(BoxArgs, TileCfg)
+{
+    if (step)
+        return fma ? k_advect_xmarch<true, true, 512, FX, NZ, UA, PULL>
+                   : k_advect_xmarch<false, true, 512, FX, NZ, UA, PULL>;
+    return fma ? k_advect_xmarch<true, false, 512, FX, NZ, UA, PULL>
+               : k_advect_xmarch<false, false, 512, FX, NZ, UA, PULL>;
+}
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
 // and size: it costs a driver call per launch otherwise (host overhead that
 // shows at small per-GPU blocks).
@@ -931,7 +1069,8 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
     a.y0 = L.y0;
     a.y1 = L.y1;
     a.trace = reinterpret_cast<unsigned long long *>(L.trace);
-    a.push = L.peers != nullptr ? 1 : 0;
+    a.push = (L.peers != nullptr && !L.pull) ? 1 : 0;
+    a.pull = L.pull ? 1 : 0;
     a.rim = (L.flags & PWADV_FLAG_RIM) && (L.x1 - L.x0) >= 3 && (L.y1 - L.y0) >= 3 ? 1 : 0;
     if (L.peers) a.peers = *L.peers;
     else a.peers = pwadv_peers{};
@@ -944,6 +1083,9 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
 
     XmarchPlan plan;
     const bool tiled = plan_xmarch(L, *dev, &plan);
+    if (L.pull && (!tiled || plan.elem || plan.maxt != 512))
+        return set_error(PWADV_E_ARG, "halo pull needs the aligned X-march (even nz <= 768, "
+                                      "16-byte-aligned fields, 512-thread plan)");
     if (tiled && plan.rounds > kMaxUnitsPerCta) {
         // more strips than one launch's unit tables hold (very long y): split
         // the box along y at a strip boundary and launch the halves in order
@@ -965,6 +1107,7 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         t.nstrips = plan.nstrips;
         t.nlong = plan.nlong;
         t.ua = plan.elem;
+        t.rot = (L.pull && plan.nlong > 0 && plan.nlong < plan.nstrips) ? 1 : 0;
         void (*kern)(BoxArgs, TileCfg) = nullptr;
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
         // compile-time layout for the BASELINE depths at the default tile
@@ -982,8 +1125,17 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
             kern = fma ? k_advect_xmarch<true, false, 512, FX, NZ>               \
                        : k_advect_xmarch<false, false, 512, FX, NZ>;             \
     }
-        PWADV_PICK_NZ(64, false)
-        PWADV_PICK_NZ(128, true)
+        if (L.pull) {  // K1 / K4 with the halo pull (own instantiations: the producer's extra
+                       // work stays out of the other kernels)
+            if (nzc == 64) kern = pick_ws<64, false, false, true>(L.step, fma);
+            else if (nzc == 128) kern = pick_ws<128, true, false, true>(L.step, fma);
+            else kern = fix ? pick_ws<0, true, false, true>(L.step, fma)
+                            : pick_ws<0, false, false, true>(L.step, fma);
+        }
+        if (!kern) {
+            PWADV_PICK_NZ(64, false)
+            PWADV_PICK_NZ(128, true)
+        }
 #undef PWADV_PICK_NZ
 #define PWADV_PICK_ELEM(FX)                                                      \
     if (plan.elem && fix == FX) {                                                \

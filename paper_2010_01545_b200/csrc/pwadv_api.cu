@@ -82,7 +82,7 @@ static int run_box(const double *u, const double *v, const double *w, double *o0
                    double *o2, int64_t nx, int64_t ny, int64_t nz, double tcx, double tcy,
                    const double *tzc1, const double *tzc2, double dt, bool step, int64_t x0,
                    int64_t x1, int64_t y0, int64_t y1, const pwadv_opts *opts, void *stream,
-                   const pwadv_peers *peers = nullptr)
+                   const pwadv_peers *peers = nullptr, bool pull = false)
 {
     int rc = check_dims(nx, ny, nz);
     if (rc) return rc;
@@ -120,6 +120,7 @@ static int run_box(const double *u, const double *v, const double *w, double *o0
     L.chunks = opts ? opts->chunks : 0;
     L.trace = opts ? opts->trace : nullptr;
     L.peers = peers;
+    L.pull = pull;
     if (L.tile_j < 0 || L.stages < 0 || L.grid < 0 || L.max_threads < 0 || L.chunks < 0)
         return set_error(PWADV_E_ARG, "negative tuning value");
     return launch_box(L, (cudaStream_t)stream);
@@ -181,17 +182,16 @@ int pwadv_step_box_f64(const double *u, const double *v, const double *w, double
                    x_begin, x_end, y_begin, y_end, opts, stream);
 }
 
-int pwadv_step_push_f64(const double *u, const double *v, const double *w, double *u_new,
-                        double *v_new, double *w_new, int64_t nx, int64_t ny, int64_t nz,
-                        double tcx, double tcy, const double *tzc1, const double *tzc2, double dt,
-                        const pwadv_peers *peers, const pwadv_opts *opts, void *stream)
+// peer table of the fused push / pull entry points: complete, aligned to
+// `align` bytes, extents consistent with an x-y decomposition
+static int check_peers(const pwadv_peers *peers, int64_t nx, int64_t ny, uintptr_t align)
 {
     if (!peers) return set_error(PWADV_E_NULL, "null peers");
     for (int d = 0; d < 8; ++d) {
         if (!peers->u[d] || !peers->v[d] || !peers->w[d])
             return set_error(PWADV_E_NULL, "peer %d buffers missing", d);
-        if (((uintptr_t)peers->u[d] | (uintptr_t)peers->v[d] | (uintptr_t)peers->w[d]) & 7)
-            return set_error(PWADV_E_ALIGN, "peer %d buffers misaligned", d);
+        if (((uintptr_t)peers->u[d] | (uintptr_t)peers->v[d] | (uintptr_t)peers->w[d]) & (align - 1))
+            return set_error(PWADV_E_ALIGN, "peer %d buffers not %d-byte aligned", d, (int)align);
         if (peers->nx[d] < 1 || peers->ny[d] < 1)
             return set_error(PWADV_E_DIMS, "peer %d extents invalid", d);
     }
@@ -199,10 +199,44 @@ int pwadv_step_push_f64(const double *u, const double *v, const double *w, doubl
     if (peers->ny[PWADV_NB_XM] != ny || peers->ny[PWADV_NB_XP] != ny ||
         peers->nx[PWADV_NB_YM] != nx || peers->nx[PWADV_NB_YP] != nx)
         return set_error(PWADV_E_RANGE, "peer extents inconsistent with an x-y decomposition");
+    return PWADV_OK;
+}
+
+int pwadv_step_push_f64(const double *u, const double *v, const double *w, double *u_new,
+                        double *v_new, double *w_new, int64_t nx, int64_t ny, int64_t nz,
+                        double tcx, double tcy, const double *tzc1, const double *tzc2, double dt,
+                        const pwadv_peers *peers, const pwadv_opts *opts, void *stream)
+{
+    int rc = check_peers(peers, nx, ny, 8);
+    if (rc) return rc;
     if (u == u_new || v == v_new || w == w_new)
         return set_error(PWADV_E_ARG, "fused step needs distinct (ping-pong) output buffers");
     return run_box(u, v, w, u_new, v_new, w_new, nx, ny, nz, tcx, tcy, tzc1, tzc2, dt, true, 1,
                    nx + 1, 1, ny + 1, opts, stream, peers);
+}
+
+int pwadv_advect_pull_f64(const double *u, const double *v, const double *w, double *su,
+                          double *sv, double *sw, int64_t nx, int64_t ny, int64_t nz, double tcx,
+                          double tcy, const double *tzc1, const double *tzc2,
+                          const pwadv_peers *src, const pwadv_opts *opts, void *stream)
+{
+    int rc = check_peers(src, nx, ny, 16);
+    if (rc) return rc;
+    return run_box(u, v, w, su, sv, sw, nx, ny, nz, tcx, tcy, tzc1, tzc2, 0.0, false, 1, nx + 1, 1,
+                   ny + 1, opts, stream, src, true);
+}
+
+int pwadv_step_pull_f64(const double *u, const double *v, const double *w, double *u_new,
+                        double *v_new, double *w_new, int64_t nx, int64_t ny, int64_t nz,
+                        double tcx, double tcy, const double *tzc1, const double *tzc2, double dt,
+                        const pwadv_peers *src, const pwadv_opts *opts, void *stream)
+{
+    int rc = check_peers(src, nx, ny, 16);
+    if (rc) return rc;
+    if (u == u_new || v == v_new || w == w_new)
+        return set_error(PWADV_E_ARG, "fused step needs distinct (ping-pong) output buffers");
+    return run_box(u, v, w, u_new, v_new, w_new, nx, ny, nz, tcx, tcy, tzc1, tzc2, dt, true, 1,
+                   nx + 1, 1, ny + 1, opts, stream, src, true);
 }
 
 // Base address of the allocation containing `ptr`, through the driver's

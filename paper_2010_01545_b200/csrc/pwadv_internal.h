@@ -27,7 +27,9 @@ struct BoxLaunch {
     uint32_t flags;
     int tile_j, stages, grid, max_threads, chunks;
     void *trace;
-    const pwadv_peers *peers;  // fused step: push boundary values into these halos
+    const pwadv_peers *peers;  // fused step: push boundary values into these halos; with
+                               // pull: the neighbours' current buffers to load halos from
+    bool pull = false;
 };
 
 struct XmarchPlan {

@@ -537,6 +537,55 @@ class IpcPeerRegistry:
         self._bases = {}
 
 
+class PullEvaluator:
+    """PW advection of one block with the halo exchange fused into K1 (pull):
+    the kernel's bulk copies load the halo cells straight from the
+    neighbours' current u, v, w — over NVLink for another GPU's block (CUDA IPC
+    through `registry`), from this block's own buffers along an undivided axis
+    — so an evaluation is one launch, with no pack/unpack, no separate
+    exchange and nothing to overlap by hand. `barrier(stream)` (all ranks)
+    orders each evaluation after every rank's previous writes to its fields;
+    the first evaluation always passes one (all blocks published and filled)."""
+
+    def __init__(self, dec: Decomposition, fields, coeffs, registry, barrier=None, *, opts=None):
+        from . import device as dv
+        self.dec = dec
+        self.fields = tuple(fields)
+        self.coeffs = dv._as_device_coeffs(coeffs, self.fields[0].device)
+        self.registry = registry
+        self.barrier = barrier
+        self.opts = opts
+        registry.publish(dec.rank, (self.fields,))
+        self.peers = None
+        self._launches: dict = {}
+
+    def _build_peers(self):
+        from . import _lib
+        p = _lib.Peers()
+        for d, r in enumerate(neighbour_ranks(self.dec)):
+            p.u[d], p.v[d], p.w[d] = self.registry.pointers(r, 0)
+            _, nxl, _, nyl = self.dec.block(r)
+            p.nx[d], p.ny[d] = nxl, nyl
+        return p
+
+    def evaluate(self, out, stream=None, *, sync: bool = True, dt: float | None = None) -> None:
+        """su, sv, sw (or, with dt, the forward-Euler update) of this block into `out`."""
+        from . import device as dv
+        first = self.peers is None
+        if (first or sync) and self.barrier is not None:
+            self.barrier(stream)
+        if first:
+            self.peers = self._build_peers()
+        key = (tuple(t.data_ptr() for t in out), dt)
+        launch = self._launches.get(key)
+        if launch is None:
+            if len(self._launches) > 8:
+                self._launches.clear()
+            launch = self._launches[key] = dv.BoundLaunch(self.fields, self.coeffs, out,
+                                                          opts=self.opts, dt=dt, pull=self.peers)
+        launch(stream)
+
+
 class NcclBarrier:
     """Stream-ordered barrier across ranks: a one-element all-reduce on the
     compute stream completes only after every rank's preceding kernels."""

@@ -176,9 +176,11 @@ class BoundLaunch:
     otherwise exceed the kernel time of a small per-GPU block."""
 
     def __init__(self, fields, coeffs, out, *, box=None, opts: _lib.Opts | None = None,
-                 dt: float | None = None):
+                 dt: float | None = None, pull: "_lib.Peers | None" = None):
         u, v, w = fields
         dims = dims_of(u)
+        if pull is not None and box is not None:
+            raise ValueError("a halo-pull launch covers the whole interior (no box)")
         for t, n in zip(tuple(fields) + tuple(out), ("u", "v", "w", "o0", "o1", "o2")):
             _check_field(t, dims, n)
         dc = _as_device_coeffs(coeffs, u.device)
@@ -190,7 +192,16 @@ class BoundLaunch:
         L = _lib.lib()
         head = [_p(u), _p(v), _p(w), _p(out[0]), _p(out[1]), _p(out[2]), dims.nx, dims.ny,
                 dims.nz, dc.tcx, dc.tcy, _p(dc.tz[0]), _p(dc.tz[1])]
-        if dt is None:
+        if pull is not None:
+            self._keep += (pull,)
+            pp = ctypes.byref(pull)
+            if dt is None:
+                self._fn = L.pwadv_advect_pull_f64
+                self._args = head + [pp, _lib.opts_ptr(opts)]
+            else:
+                self._fn = L.pwadv_step_pull_f64
+                self._args = head + [float(dt), pp, _lib.opts_ptr(opts)]
+        elif dt is None:
             self._fn = L.pwadv_advect_box_f64
             self._args = head + [x0, x1, y0, y1, _lib.opts_ptr(opts)]
         else:
@@ -199,6 +210,36 @@ class BoundLaunch:
 
     def __call__(self, stream=None) -> None:
         _lib.check(self._fn(*self._args, _stream_handle(stream, self.device)))
+
+
+def self_peers(fields) -> _lib.Peers:
+    """Peer table naming this block as all eight of its neighbours: a halo-pull
+    launch with it evaluates the periodic domain without a halo wrap."""
+    dims = dims_of(fields[0])
+    p = _lib.Peers()
+    for d in range(8):
+        p.u[d], p.v[d], p.w[d] = (_p(t) for t in fields)
+        p.nx[d], p.ny[d] = dims.nx, dims.ny
+    return p
+
+
+def advect_pull(u, v, w, coeffs, peers: _lib.Peers, out=None, *, opts: _lib.Opts | None = None,
+                stream=None):
+    """K1 with the halo exchange fused in: su, sv, sw of the whole interior
+    with halo cells loaded from the neighbours' current (u, v, w) in `peers`
+    (pwadv_advect_pull_f64); this block's halos are not read."""
+    if out is None:
+        out = alloc_fields(dims_of(u), u.device)
+    BoundLaunch((u, v, w), coeffs, out, opts=opts, pull=peers)(stream)
+    return out
+
+
+def step_pull(u, v, w, coeffs, dt: float, out, peers: _lib.Peers, *, opts: _lib.Opts | None = None,
+              stream=None):
+    """K4 with the halo pull (pwadv_step_pull_f64): out = (u, v, w) + dt*PW on
+    the whole interior; out's halos are not written."""
+    BoundLaunch((u, v, w), coeffs, out, opts=opts, dt=float(dt), pull=peers)(stream)
+    return out
 
 
 def wrap_halos(*fields, stream=None) -> None:

@@ -204,3 +204,109 @@ def test_ipc_export_map_and_write_across_processes():
     torch.cuda.synchronize()
     for f, w in zip(fields, want):
         assert torch.equal(f.view(torch.int64), w.view(torch.int64))
+
+
+# --- K1 / K4 with the halo exchange fused in (pull) ---------------------------
+
+def _poison_halos(fields):
+    for f in fields:
+        f[0].fill_(float("nan"))
+        f[-1].fill_(float("nan"))
+        f[:, 0].fill_(float("nan"))
+        f[:, -1].fill_(float("nan"))
+
+
+@pytest.mark.parametrize("shape", [(40, 36, 64), (7, 300, 64), (33, 5, 128), (1, 1, 2), (150, 13, 6)])
+def test_pull_single_block_self_peers(shape):
+    """An undivided domain pulling from itself: halos never read (NaN-poisoned),
+    results bit-identical to wrap + K1 (and wrap + K4)."""
+    gd = pw.make_grid(*shape)
+    spec = pw.GeneratorSpec.baseline(5)
+    co = pw.baseline_coefficients(5, gd.nz)
+    f = device.fill(gd, spec)
+    want = device.advect(*f, co)
+    want_step = device.step(*f, co, 0.1, device.alloc_fields(gd, "cuda"))
+    g = [t.clone() for t in f]
+    _poison_halos(g)
+    peers = device.self_peers(g)
+    got = device.advect_pull(*g, co, peers)
+    nxt = device.alloc_fields(gd, "cuda")
+    device.step_pull(*g, co, 0.1, nxt, peers)
+    torch.cuda.synchronize()
+    for a, b in zip(got, want):
+        assert torch.equal(a.view(torch.int64), b.view(torch.int64))
+    for a, b in zip(nxt, want_step):
+        assert torch.equal(a[1:-1, 1:-1].contiguous().view(torch.int64),
+                           b[1:-1, 1:-1].contiguous().view(torch.int64))
+    assert all(torch.equal(t[0], torch.zeros_like(t[0])) for t in nxt)  # new halos untouched
+
+
+@pytest.mark.parametrize("shape", [(40, 36, 64), (64, 48, 128), (25, 23, 6)])
+@pytest.mark.parametrize("px,py", [(1, 2), (2, 1), (2, 2), (2, 4), (3, 2)])
+def test_emulated_pull_decomposition_bitwise(shape, px, py):
+    """PullEvaluator on every block of a px x py decomposition (peer buffers on
+    this GPU, halos NaN-poisoned): bit-identical to the undivided evaluation;
+    and a pulled forward step too."""
+    from paper_2010_01545_b200.decomp import LocalPeerRegistry, PullEvaluator
+    gd = pw.make_grid(*shape)
+    spec = pw.GeneratorSpec.baseline(9)
+    co = pw.baseline_coefficients(9, gd.nz)
+    gfields = device.fill(gd, spec)
+    want = device.advect(*gfields, co)
+    want_step = device.step(*gfields, co, 0.1, device.alloc_fields(gd, "cuda"))
+    reg = LocalPeerRegistry()
+    evs = []
+    for r in range(px * py):
+        dec = Decomposition(gd, px, py, r)
+        fs = dec.fill_local(spec)
+        _poison_halos(fs)
+        evs.append((dec, PullEvaluator(dec, fs, co, reg)))
+    torch.cuda.synchronize()
+    for dec, ev in evs:  # every block published before any evaluation
+        out = device.alloc_fields(dec.local_dims, "cuda")
+        ev.evaluate(out)
+        nxt = device.alloc_fields(dec.local_dims, "cuda")
+        ev.evaluate(nxt, dt=0.1)
+        torch.cuda.synchronize()
+        xo, bx, yo, by = dec.block()
+        for o, w in zip(out, want):
+            assert torch.equal(o[1:-1, 1:-1].contiguous().view(torch.int64),
+                               w[1 + xo:1 + xo + bx, 1 + yo:1 + yo + by].contiguous().view(torch.int64)), dec.rank
+        for o, w in zip(nxt, want_step):
+            assert torch.equal(o[1:-1, 1:-1].contiguous().view(torch.int64),
+                               w[1 + xo:1 + xo + bx, 1 + yo:1 + yo + by].contiguous().view(torch.int64)), dec.rank
+
+
+def test_pull_rejects_shapes_off_the_aligned_xmarch():
+    from paper_2010_01545_b200 import _lib
+    gd = pw.make_grid(8, 8, 7)  # odd nz
+    f = device.fill(gd, pw.GeneratorSpec.baseline(1))
+    co = pw.baseline_coefficients(1, 7)
+    with pytest.raises(_lib.PwadvError):
+        device.advect_pull(*f, co, device.self_peers(f))
+    gd = pw.make_grid(8, 8, 8)
+    f = device.fill(gd, pw.GeneratorSpec.baseline(1))
+    p = device.self_peers(f)
+    p.ny[0] = 9  # an x neighbour with another y extent
+    with pytest.raises(_lib.PwadvError):
+        device.advect_pull(*f, pw.baseline_coefficients(1, 8), p)
+
+
+@pytest.mark.parametrize("kw", [dict(grid=3, chunks=4), dict(grid=5, chunks=2, tile_j=5), dict(grid=7),
+                                dict(grid=4), dict(grid=4, tile_j=7)])
+def test_pull_multi_unit_plans(kw):
+    """Halo pull with several work units per CTA (forced small grids / chunks):
+    y-face and interior units interleaved in one CTA's plane sequence; with
+    whole-X rounds plus a chunked tail (grid=4) the strips are rotated so the
+    y-face strips fall in the tail."""
+    gd = pw.make_grid(50, 70, 64)
+    spec = pw.GeneratorSpec.baseline(3)
+    co = pw.baseline_coefficients(3, gd.nz)
+    f = device.fill(gd, spec)
+    want = device.advect(*f, co)
+    g = [t.clone() for t in f]
+    _poison_halos(g)
+    got = device.advect_pull(*g, co, device.self_peers(g), opts=device.make_opts("xmarch", **kw))
+    torch.cuda.synchronize()
+    for a, b in zip(got, want):
+        assert torch.equal(a.view(torch.int64), b.view(torch.int64)), kw
