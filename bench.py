@@ -300,8 +300,25 @@ def run_ours(args):
                 def one_step():
                     st._one(stream)
         else:
-            def one_step():
-                exch.advect_overlapped(fields, co, out, opts=opts, stream=stream)
+            # K1 with the exchange fused in: halo cells pulled from the
+            # neighbours' buffers over NVLink (CUDA IPC), one NCCL barrier per
+            # evaluation (the neighbours' fields are final before it reads them)
+            try:
+                ev = decomp.PullEvaluator(dec, fields, co, decomp.IpcPeerRegistry(dec),
+                                          decomp.NcclBarrier(dev), opts=opts)
+                ev.evaluate(out, stream=stream)
+                step_path = "K1 with halo pull (peer loads over NVLink, CUDA IPC) + NCCL barrier"
+
+                def one_step():
+                    ev.evaluate(out, stream=stream)
+            except _lib.PwadvError as exc:
+                # no CUDA IPC for these allocations, or a shape off the aligned
+                # X-march: NCCL halo exchange overlapped with the interior
+                print(f"bench: halo pull unavailable ({exc}); NCCL exchange + overlap", file=sys.stderr)
+                step_path = "NCCL exchange overlapped with K1 (interior), then K1 rim"
+
+                def one_step():
+                    exch.advect_overlapped(fields, co, out, opts=opts, stream=stream)
 
     def barrier():
         if dist is not None:

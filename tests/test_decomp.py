@@ -134,3 +134,37 @@ def test_gloo_multiprocess_exchange(px, py):
     assert sorted(r for r, _, _ in results) == list(range(world))
     for r, ok, err in results:
         assert ok, (r, err)
+
+
+@pytest.mark.parametrize("px,py,shape", [(2, 4, (21, 30, 4)), (1, 2, (9, 11, 4)), (3, 1, (10, 5, 4))])
+def test_pull_evaluator_peer_table(px, py, shape):
+    """PullEvaluator's peer table (host side, no launch): entry d names the
+    neighbour in direction d (PWADV_NB_* order) — the buffers that rank
+    published and its block extents; an undivided axis names the block itself."""
+    from paper_2010_01545_b200 import _lib
+    from paper_2010_01545_b200.decomp import LocalPeerRegistry, PullEvaluator
+    gd = pw.make_grid(*shape)
+    co = pw.AdvectionCoefficients(0.005, 0.005, np.full(gd.nz, 2e-3), np.full(gd.nz, 3e-3))
+    reg = LocalPeerRegistry()
+    evs = []
+    for r in range(px * py):
+        dec = Decomposition(gd, px, py, r)
+        d = dec.local_dims
+        fs = tuple(torch.zeros(d.padded_shape, dtype=torch.float64) for _ in range(3))
+        evs.append((dec, fs, PullEvaluator(dec, fs, co, reg)))
+    ptrs = {dec.rank: tuple(t.data_ptr() for t in fs) for dec, fs, _ in evs}
+    dirs = {_lib.NB_XM: (-1, 0), _lib.NB_XP: (1, 0), _lib.NB_YM: (0, -1), _lib.NB_YP: (0, 1),
+            _lib.NB_XMYM: (-1, -1), _lib.NB_XMYP: (-1, 1), _lib.NB_XPYM: (1, -1), _lib.NB_XPYP: (1, 1)}
+    for dec, _, ev in evs:
+        p = ev._build_peers()
+        cx, cy = dec.coords
+        for d, (dx, dy) in dirs.items():
+            r = dec.rank_of(cx + dx, cy + dy)
+            assert (p.u[d], p.v[d], p.w[d]) == ptrs[r], (dec.rank, d)
+            _, nxl, _, nyl = dec.block(r)
+            assert (p.nx[d], p.ny[d]) == (nxl, nyl)
+        # x neighbours share this block's y extent, y neighbours its x extent
+        assert p.ny[_lib.NB_XM] == p.ny[_lib.NB_XP] == dec.local_dims.ny
+        assert p.nx[_lib.NB_YM] == p.nx[_lib.NB_YP] == dec.local_dims.nx
+        if px == 1:
+            assert (p.u[_lib.NB_XM], p.u[_lib.NB_XP]) == (ptrs[dec.rank][0],) * 2
