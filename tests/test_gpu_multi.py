@@ -4,7 +4,7 @@ Skipped when fewer than 2 GPUs are visible (this round's boxes have one; the
 thread-emulated versions in test_gpu_decomp.py run there). With >= 2 GPUs
 they run the production paths exactly as `bench.py --gpus N` does:
 HaloExchanger over DistTransport (NCCL batch_isend_irecv) with
-advect_overlapped, and the fused PushStepper with IpcPeerRegistry +
+advect_overlapped, the halo-pull PullEvaluator and the fused PushStepper with IpcPeerRegistry +
 NcclBarrier, each compared bitwise with the single-domain result computed in
 the same process.
 """
@@ -67,7 +67,21 @@ def _worker(rank, world, port, px, py, q):
         torch.cuda.synchronize()
         for f, w in zip(st.fields, want_step):
             ok &= torch.equal(f.view(torch.int64), dec.local_view(w).contiguous().view(torch.int64))
+        # K1 with the halo pull: neighbours' buffers over CUDA IPC, halos NaN
+        fs3 = dec.fill_local(spec, device=dev)
+        for f in fs3:
+            f[0].fill_(float("nan")); f[-1].fill_(float("nan"))  # noqa: E702
+            f[:, 0].fill_(float("nan")); f[:, -1].fill_(float("nan"))  # noqa: E702
+        reg3 = decomp.IpcPeerRegistry(dec)
+        ev = decomp.PullEvaluator(dec, fs3, co, reg3, decomp.NcclBarrier(dev))
+        out3 = device.alloc_fields(dec.local_dims, dev)
+        ev.evaluate(out3)
+        torch.cuda.synchronize()
+        for o, w in zip(out3, want_adv):
+            ok &= torch.equal(o[1:-1, 1:-1].contiguous().view(torch.int64),
+                              w[1 + xo:1 + xo + bx, 1 + yo:1 + yo + by].contiguous().view(torch.int64))
         dist.barrier()
+        reg3.close()
         reg.close()
         dist.destroy_process_group()
         q.put((rank, bool(ok), ""))
