@@ -480,6 +480,37 @@ def run_ours(args):
                "frac_of_pcie_bound": round(dims.cells * ke / (t1 - t0) / (pcie_gbs * 1e9 / (h2d / dims.cells)), 3),
                "bitwise_equal_to_device_run": bool(same)}
 
+    # config 4 (stepping, N=1) end to end through the public stepping API: the
+    # state is uploaded from pinned host memory once, stepped, one probe value
+    # of the new w is read back to the host after every step (the step's
+    # "result"; it also serialises the host with every step), and the final
+    # state is downloaded — all inside the timed region
+    if ws == 1 and stepping and not args.no_e2e:
+        hin = [torch.empty(dims.padded_shape, dtype=torch.float64, pin_memory=True) for _ in range(3)]
+        hout = [torch.empty(dims.padded_shape, dtype=torch.float64, pin_memory=True) for _ in range(3)]
+        for h, f in zip(hin, st.fields):
+            h.copy_(f)
+        probe = torch.empty(1, dtype=torch.float64, pin_memory=True)
+        ke = 100  # BASELINE config 4: 100 steps per run
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for f, h in zip(st.a, hin):
+            f.copy_(h, non_blocking=True)
+        for _ in range(ke):
+            st._one(stream)
+            probe.copy_(st.a[2][nx // 2, ny // 2, nz // 2:nz // 2 + 1], non_blocking=True)
+            stream.synchronize()
+        for h, f in zip(hout, st.fields):
+            h.copy_(f, non_blocking=True)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        fb = 3 * hin[0].numel() * 8
+        e2e = {"value": dims.cells * ke / (t1 - t0) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": fb / ke, "d2h_bytes_per_step": 8 + fb / ke, "steps": ke,
+               "api": "stepper.Stepper (wrap + K4 per step) on a state uploaded from pinned host "
+                      "memory; one probe value read back per step; final state downloaded",
+               "probe_finite": bool(torch.isfinite(probe).all())}
+
     # N>1: every rank streams its own padded block (host data distributed per
     # rank, halos included as the exchange left them) through its own PCIe
     # link; value = global points / max-over-ranks wall time
