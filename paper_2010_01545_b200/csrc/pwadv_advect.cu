@@ -125,14 +125,13 @@ __device__ __noinline__ void push_pair_ua(const BoxArgs *A, int64_t i, int64_t j
 
 struct TileCfg {
     int tj;           // columns per strip
-    int kp;           // threads per column (= nz/2)
+    int kp;           // threads per column (= (nz+1)/2)
     int stages;       // ring depth
     int nchunks;      // X chunks per strip; work unit = (chunk, strip)
     int debug;        // ablation bits (PWADV_FLAG_DEBUG_*): 1 = no PW arithmetic, 4 = no stores
     int l2hint;       // 1: load each unit's first two planes with L2 evict_last
     int64_t nstrips;  // ceil((y1-y0)/tj)
     int64_t nlong;    // strips 0..nlong-1 are whole-X units (full rounds); the rest are chunked
-    int ua;           // planned UA (unaligned tile runs) — informational
     int rot;          // strips are rotated by this much (halo pull: the two y-face strips,
                       // whose tiles take six copies per plane, fall in the chunked tail)
 };
@@ -1106,7 +1105,6 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         t.l2hint = (L.flags & PWADV_FLAG_L2_UNIT_HEAD) ? 1 : 0;
         t.nstrips = plan.nstrips;
         t.nlong = plan.nlong;
-        t.ua = plan.elem;
         t.rot = (L.pull && plan.nlong > 0 && plan.nlong < plan.nstrips) ? 1 : 0;
         void (*kern)(BoxArgs, TileCfg) = nullptr;
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
