@@ -1105,7 +1105,10 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         t.l2hint = (L.flags & PWADV_FLAG_L2_UNIT_HEAD) ? 1 : 0;
         t.nstrips = plan.nstrips;
         t.nlong = plan.nlong;
-        t.rot = (L.pull && plan.nlong > 0 && plan.nlong < plan.nstrips) ? 1 : 0;
+#ifndef PWADV_PULL_ROT
+#define PWADV_PULL_ROT 1
+#endif
+        t.rot = (PWADV_PULL_ROT && L.pull && plan.nlong > 0 && plan.nlong < plan.nstrips) ? 1 : 0;
         void (*kern)(BoxArgs, TileCfg) = nullptr;
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
         // compile-time layout for the BASELINE depths at the default tile

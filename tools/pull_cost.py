@@ -1,6 +1,6 @@
 """Cost of the fused halo pull in K1 on one GPU.
 
-    python tools/pull_cost.py [NXxNYxNZ] [reps]
+    python tools/pull_cost.py [NXxNYxNZ] [reps] [flags]
 
 (a) K1 on a block whose halos are already valid; (b) K2 wrap + K1 (the
 periodic evaluation without the pull); (c) K1-pull with the block as all
@@ -37,6 +37,8 @@ def rate(fn, cells, reps):
 def main():
     nx, ny, nz = (int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "2048x2048x64").split("x"))
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+    flags = int(sys.argv[3]) if len(sys.argv) > 3 else 0  # e.g. 128: ordinary launches (no PDL)
+    opts = device.make_opts("xmarch", flags=flags)
     gd = pw.make_grid(nx, ny, nz)
     spec = pw.GeneratorSpec.baseline(42)
     co = device.DeviceCoefficients.from_host(pw.baseline_coefficients(42, nz), "cuda")
@@ -44,8 +46,8 @@ def main():
     ref = device.advect(*f, co)
     out = device.alloc_fields(gd, "cuda")
     peers = device.self_peers(f)
-    pull = device.BoundLaunch(f, co, out, pull=peers)
-    plain = device.BoundLaunch(f, co, out)
+    pull = device.BoundLaunch(f, co, out, pull=peers, opts=opts)
+    plain = device.BoundLaunch(f, co, out, opts=opts)
     # 2x4 blocks of the same grid on this GPU
     reg = decomp.LocalPeerRegistry()
     blocks = []
