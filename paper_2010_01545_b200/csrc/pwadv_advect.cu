@@ -134,7 +134,15 @@ struct TileCfg {
     int64_t nlong;    // strips 0..nlong-1 are whole-X units (full rounds); the rest are chunked
     int rot;          // strips are rotated by this much (halo pull: the two y-face strips,
                       // whose tiles take six copies per plane, fall in the chunked tail)
+    int nface;        // halo pull: the last nface strips of the tail (the y-face strips)
+    int nchf;         //   are cut into nchf chunks instead of nchunks (shorter units)
 };
+
+// work units of a launch (unit_at's numbering)
+__host__ __device__ __forceinline__ int64_t units_of(const TileCfg &t)
+{
+    return t.nlong + (t.nstrips - t.nlong - t.nface) * t.nchunks + (int64_t)t.nface * t.nchf;
+}
 
 // Work units (unit_at) are dealt round-robin to the CTAs: CTA b runs units
 // b, b+G, b+2G, ... All CTAs start a round together and march at the same
@@ -158,13 +166,23 @@ __device__ __forceinline__ Unit unit_at(const BoxArgs &a, const TileCfg &t, int6
         w.ie = a.x1;
         return w;
     }
-    const int64_t tail = t.nstrips - t.nlong;
+    const int64_t treg = t.nstrips - t.nlong - t.nface;  // tail strips with nchunks chunks
     const int64_t v = u - t.nlong;
-    const int64_t chunk = v / tail;
-    w.strip = t.nlong + (v - chunk * tail) + t.rot;
+    int64_t chunk, idx, nch;
+    if (v < treg * t.nchunks) {
+        chunk = v / treg;
+        idx = v - chunk * treg;
+        nch = t.nchunks;
+    } else {  // the y-face strips of a pull plan, in shorter chunks
+        const int64_t r = v - treg * t.nchunks;
+        chunk = r / t.nface;
+        idx = treg + (r - chunk * t.nface);
+        nch = t.nchf;
+    }
+    w.strip = t.nlong + idx + t.rot;
     if (w.strip >= t.nstrips) w.strip -= t.nstrips;
-    w.ib = a.x0 + (nxr * chunk) / t.nchunks;
-    w.ie = a.x0 + (nxr * (chunk + 1)) / t.nchunks;
+    w.ib = a.x0 + (nxr * chunk) / nch;
+    w.ie = a.x0 + (nxr * (chunk + 1)) / nch;
     return w;
 }
 
@@ -603,7 +621,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     const double c2a = __ldg(a.tzc2 + k0), c2b = __ldg(a.tzc2 + k1c);
 
     const int64_t ny2 = a.ny + 2;
-    const int64_t nunits = t.nlong + (t.nstrips - t.nlong) * t.nchunks;
+    const int64_t nunits = units_of(t);
     const int64_t G = gridDim.x;
     if ((int64_t)blockIdx.x >= nunits) return;
 
@@ -1105,10 +1123,9 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         t.l2hint = (L.flags & PWADV_FLAG_L2_UNIT_HEAD) ? 1 : 0;
         t.nstrips = plan.nstrips;
         t.nlong = plan.nlong;
-#ifndef PWADV_PULL_ROT
-#define PWADV_PULL_ROT 1
-#endif
-        t.rot = (PWADV_PULL_ROT && L.pull && plan.nlong > 0 && plan.nlong < plan.nstrips) ? 1 : 0;
+        t.rot = plan.rot;
+        t.nface = plan.nface;
+        t.nchf = plan.nchf;
         void (*kern)(BoxArgs, TileCfg) = nullptr;
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
         // compile-time layout for the BASELINE depths at the default tile
@@ -1334,11 +1351,35 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
         if (L.chunks > 0) break;
     }
     p->nchunks = (int)best_nch;
-    const int64_t units = p->nlong + tail * best_nch;
+    int64_t units = p->nlong + tail * best_nch;
     int64_t grid = units < g0 ? units : g0;
     if (grid < 1) grid = 1;
     p->grid = (int)grid;
     p->rounds = (units + grid - 1) / grid;
+    // Halo pull: the two y-face strips copy six runs per plane instead of
+    // three and set the pace of whatever round they are in. Rotate the strips
+    // by one so they are the last two of the chunked tail, and cut them into
+    // shorter chunks using the tail round's free CTA slots (no extra round).
+    p->rot = 0;
+    p->nface = 0;
+    p->nchf = 0;
+#ifndef PWADV_PULL_ROT
+#define PWADV_PULL_ROT 1
+#endif
+    if (L.pull && PWADV_PULL_ROT && p->nstrips > 1 && tail > 0) {
+        p->rot = 1;
+        p->nface = (int)(tail < 2 ? tail : 2);
+        const int64_t spare = L.grid > 0 || L.chunks > 0 ? 0 : p->rounds * g0 - units;
+        int64_t nchf = best_nch + spare / p->nface;
+        if (nchf > nbx) nchf = nbx;
+        if (nchf < best_nch) nchf = best_nch;
+        p->nchf = (int)nchf;
+        units += (int64_t)p->nface * (nchf - best_nch);
+        grid = units < g0 ? units : g0;
+        if (grid < 1) grid = 1;
+        p->grid = (int)grid;
+        p->rounds = (units + grid - 1) / grid;
+    }
     // Ring depth measured with interleaved sweeps (tools/sweep.py --rounds,
     // profiles/README.md): a plan that is one round of long units (C1: 129
     // CTAs x 171 planes) streams better with 6 stages (124.7 vs 121.0 Gpts/s

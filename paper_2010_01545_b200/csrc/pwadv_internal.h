@@ -39,6 +39,7 @@ struct XmarchPlan {
     int64_t rounds;  // units per CTA (the kernel's unit table holds kMaxUnitsPerCta)
     int64_t nlong;   // strips run as whole-X units (full rounds)
     int elem;        // 1: unaligned tile runs (UA kernels: odd nz, 8-byte alignment)
+    int rot, nface, nchf;  // halo pull: strip rotation and the y-face strips' chunking
 };
 
 // cached attributes of the current device (lazily filled, thread-safe)
