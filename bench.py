@@ -307,6 +307,18 @@ def run_ours(args):
                 ev = decomp.PullEvaluator(dec, fields, co, decomp.IpcPeerRegistry(dec),
                                           decomp.NcclBarrier(dev), opts=opts)
                 ev.evaluate(out, stream=stream)
+                # self-check on this box: the pulled evaluation must equal the
+                # NCCL-exchange evaluation bit for bit on every rank
+                ref_out = device.alloc_fields(dims, dev)
+                exch.advect_overlapped(fields, co, ref_out, opts=opts, stream=stream)
+                torch.cuda.synchronize()
+                bad = torch.tensor([0 if all(torch.equal(a.view(torch.int64), b.view(torch.int64))
+                                             for a, b in zip(out, ref_out)) else 1], device=dev)
+                dist.all_reduce(bad)
+                del ref_out
+                if int(bad.item()):
+                    raise _lib.PwadvError(_lib.PWADV_E_ARG, "pulled evaluation differs from the "
+                                                            "NCCL-exchange evaluation")
                 step_path = "K1 with halo pull (peer loads over NVLink, CUDA IPC) + NCCL barrier"
 
                 def one_step():
