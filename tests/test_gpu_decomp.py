@@ -254,6 +254,11 @@ def test_emulated_pull_decomposition_bitwise(shape, px, py):
     gfields = device.fill(gd, spec)
     want = device.advect(*gfields, co)
     want_step = device.step(*gfields, co, 0.1, device.alloc_fields(gd, "cuda"))
+    # the undivided reference is itself the oracle's result (checker only)
+    from oracle import oracle
+    host = [f.cpu().numpy() for f in gfields]
+    ow = oracle.advect(*host, co.tcx, co.tcy, co.tzc1, co.tzc2, engines=oracle.host_threads())
+    assert oracle.compare([t.cpu().numpy() for t in want], ow)["bitwise_equal"]
     reg = LocalPeerRegistry()
     evs = []
     for r in range(px * py):
