@@ -2,7 +2,7 @@
 the same bits (a rare race in the mbarrier / refill protocol would show up as
 a changed digest or a hang). Prints one JSON line.
 
-    python tools/soak.py [--launches 100000] [--steps 3000]
+    python tools/soak.py [--launches 100000] [--steps 3000] [--only k1,k4,pull,ua]
 """
 import argparse
 import json
@@ -26,8 +26,51 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--launches", type=int, default=100000)
     ap.add_argument("--steps", type=int, default=3000)
+    ap.add_argument("--only", default="k1,k4,pull,ua")
     a = ap.parse_args()
+    which = set(a.only.split(","))
     res = {}
+    if "pull" in which:  # K1 with the halo pull (block as its own neighbours), 2048^2x64
+        dp = pw.make_grid(2048, 2048, 64)
+        fp = device.fill(dp, pw.GeneratorSpec.baseline(7))
+        cop = device.DeviceCoefficients.from_host(pw.baseline_coefficients(7, 64), "cuda")
+        want = device.advect(*fp, cop)
+        for t_ in fp:  # halos must not matter
+            t_[0].fill_(float("nan"))
+            t_[:, 0].fill_(float("nan"))
+        outp = device.alloc_fields(dp, "cuda")
+        launch = device.BoundLaunch(fp, cop, outp, pull=device.self_peers(fp))
+        ref = digest(want)
+        n_pull = max(1, a.launches // 20)
+        bad = 0
+        t = time.perf_counter()
+        for n in range(n_pull):
+            launch()
+            if n % 100 == 99:
+                bad += digest(outp) != ref
+        torch.cuda.synchronize()
+        res["k1_pull_2048sq"] = {"launches": n_pull, "mismatches": bad, "s": round(time.perf_counter() - t, 1)}
+        del fp, outp, want, launch
+        torch.cuda.empty_cache()
+    if "ua" in which:  # the UA form, odd nz
+        du = pw.make_grid(512, 512, 63)
+        fu = device.fill(du, pw.GeneratorSpec.baseline(5))
+        cou = device.DeviceCoefficients.from_host(pw.baseline_coefficients(5, 63), "cuda")
+        outu = device.alloc_fields(du, "cuda")
+        device.advect(*fu, cou, outu)
+        ref = digest(outu)
+        n_ua = max(1, a.launches // 4)
+        bad = 0
+        t = time.perf_counter()
+        for n in range(n_ua):
+            device.advect(*fu, cou, outu)
+            if n % 1000 == 999:
+                bad += digest(outu) != ref
+        torch.cuda.synchronize()
+        res["k1_ua_512x512x63"] = {"launches": n_ua, "mismatches": bad, "s": round(time.perf_counter() - t, 1)}
+    if not which & {"k1", "k4"}:
+        print(json.dumps(res))
+        return
     # K1, C1: same inputs, same outputs, every 1000 launches compared
     d = pw.make_grid(512, 512, 64)
     f = device.fill(d, pw.GeneratorSpec.baseline(42))
