@@ -200,7 +200,7 @@ template <bool FMA, bool STEP>
 __global__ void __launch_bounds__(128) k_advect_march(BoxArgs a, int64_t nchunks)
 {
     const int64_t nz = a.nz, ny2 = a.ny + 2;
-    const int64_t nbx = a.x1 - a.x0, nby = a.y1 - a.y0;
+    const int64_t nbx = a.x1 - a.x0;
     const int64_t ktiles = (nz + 31) / 32;
     const int64_t tile = blockIdx.x;
     const int64_t kt = tile % ktiles, jt = tile / ktiles;
