@@ -243,9 +243,18 @@ __global__ void __launch_bounds__(128) k_advect_march(BoxArgs a, int64_t nchunks
     double u_xm1_jp1 = at(a.u, ib - 1, jj + 1, kk);
     double u_xm1_km1 = up(u_m, a.u, ib - 1, jj);
     double u_c = at(a.u, ib, jj, kk), v_c = at(a.v, ib, jj, kk), w_c = at(a.w, ib, jj, kk);
+#ifndef PWADV_MARCH_L2_AHEAD
+#define PWADV_MARCH_L2_AHEAD 2
+#endif
     for (int64_t i = ib; i < ie; ++i) {
-        // leading plane i+1 (a one-plane-ahead prefetch measured slower: the
-        // extra registers cost occupancy)
+        // planes i+1+AHEAD into L2 ahead of their loads (no registers held;
+        // a one-plane-ahead register prefetch measured slower: occupancy)
+        if (PWADV_MARCH_L2_AHEAD > 0 && i + 1 + PWADV_MARCH_L2_AHEAD <= ie) {
+            const int64_t o = ((i + 1 + PWADV_MARCH_L2_AHEAD) * ny2 + jj) * nz + kk;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.u + o));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.v + o));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.w + o));
+        }
         const double u_p = at(a.u, i + 1, jj, kk), v_p = at(a.v, i + 1, jj, kk);
         const double w_p = at(a.w, i + 1, jj, kk);
         const double v_p_jm1 = at(a.v, i + 1, jj - 1, kk);
