@@ -216,7 +216,8 @@ def _poison_halos(fields):
         f[:, -1].fill_(float("nan"))
 
 
-@pytest.mark.parametrize("shape", [(40, 36, 64), (7, 300, 64), (33, 5, 128), (1, 1, 2), (150, 13, 6)])
+@pytest.mark.parametrize("shape", [(40, 36, 64), (7, 300, 64), (33, 5, 128), (1, 1, 2), (150, 13, 6),
+                                   (40, 24, 64), (40, 30, 64), (3, 2000, 64)])
 def test_pull_single_block_self_peers(shape):
     """An undivided domain pulling from itself: halos never read (NaN-poisoned),
     results bit-identical to wrap + K1 (and wrap + K4)."""
