@@ -186,6 +186,20 @@ def pcie_concurrent(hin, hout, dev):
     return best
 
 
+def host_info() -> dict:
+    """CPU model, logical CPUs and numpy version of this host."""
+    import numpy as np
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "numpy": np.__version__}
+
+
 def cpu_baseline_arm(nx, ny, nz, reps=400, max_seconds=10.0):
     """The oracle port (C restatement, oracle/) on all host threads: the same
     X-slab sample evaluated repeatedly for ~10 s of CPU work (at most `reps`
@@ -209,7 +223,7 @@ def cpu_baseline_arm(nx, ny, nz, reps=400, max_seconds=10.0):
     pts = sx * ny * nz
     med = sorted(times)[len(times) // 2]
     return {"value": pts / min(times) / 1e9, "value_median": pts / med / 1e9, "unit": UNIT,
-            "cores": threads, "kind": "port",
+            "cores": threads, "kind": "port", "host": host_info(),
             "sample": f"{sx}x{ny}x{nz} X-slab of the config grid ({pts} points) evaluated "
                       f"{len(times)} times over {time.perf_counter() - t_start:.1f} s (value = best, "
                       f"value_median = median), oracle/pwadv_oracle.c on {threads} threads "
@@ -652,7 +666,7 @@ def run_reference(args):
             "data": "synthetic (same generator as our arm)", "impl": "reference",
             "config": {"workload": desc, "nx": nx, "ny": ny, "nz": nz, "sample_nx": sx},
             "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": engines, "kind": "port",
-                             "sample": sample},
+                             "sample": sample, "host": host_info()},
             "engines_probe_s": {str(e): round(t, 4) for e, t in probe.items()},
             "c_port": c_port,
             "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
