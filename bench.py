@@ -650,6 +650,10 @@ def run_reference(args):
     dt = time.perf_counter() - t0
     pts = sx * ny * nz
     value = pts * steps / dt / 1e9
+    # the reference's single-thread run_reference on the same sample (min of 3)
+    t1 = min(timed(lambda: oracle.run_schedule_numpy(u, v, w, *cargs, 1, outs=outs)) for _ in range(3))
+    single = {"value": round(pts / t1 / 1e9, 5), "unit": UNIT, "cores": 1,
+              "sample": "same sample, engines=1 (run_reference), min of 3"}
     # the C port of the same algorithm, for context (~5 s)
     cts = []
     t_c = time.perf_counter()
@@ -668,6 +672,7 @@ def run_reference(args):
             "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": engines, "kind": "port",
                              "sample": sample, "host": host_info()},
             "engines_probe_s": {str(e): round(t, 4) for e, t in probe.items()},
+            "single_thread": single,
             "c_port": c_port,
             "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
