@@ -1,7 +1,7 @@
 // pwadv_advect.cu — K1 (PW advection) and K4 (fused forward step) for sm_100a.
 //
 // Replaces the reference hot path run_reference -> compute_block ->
-// su/sv/sw_formula (pkg/src/pwadvect/kernel.py:73-185). Two kernels:
+// su/sv/sw_formula (pkg/src/pwadvect/kernel.py:73-185). Three kernels:
 //
 //  * k_advect_xmarch — the production kernel. A CTA owns a strip of TJ
 //    y-columns (all nz levels) and marches through X (the GPU analogue of the
@@ -26,11 +26,20 @@
 //    Work distribution: whole strips for every full round of a persistent
 //    grid of one CTA per SM, the leftover strips in X chunks (see unit_at and
 //    plan_xmarch); a CTA moving to its next unit just continues its plane
-//    sequence (the ring never drains).
+//    sequence (the ring never drains). Variants: UA (odd nz, 8-byte-aligned
+//    fields: tile runs copied from the 16-byte boundary below them, scalar
+//    shared loads), PULL (the multi-GPU halo exchange fused in: halo cells
+//    copied from the neighbours' buffers), STEP (K4, the forward update
+//    fused into the epilogue, optionally pushing boundary values into the
+//    neighbours' halos).
 //
-//  * k_advect_simple — one thread per output point, direct global loads. Used
-//    for shapes the X-march does not cover (odd nz, misaligned pointers, very
-//    tall columns), for thin rim boxes, and as an independent check.
+//  * k_advect_march (K1m) — a register-window X-march without the plane
+//    ring, for what the X-march does not take (nz > 768, inputs whose
+//    16-byte phases differ).
+//
+//  * k_advect_simple — one thread per output point, direct global loads: the
+//    one-cell rims of the overlapped multi-GPU evaluation, and an
+//    independent cross-check.
 //
 // Both are bit-exact with the reference by construction (pwadv_device.cuh).
 #include "pwadv_device.cuh"
@@ -187,8 +196,8 @@ __device__ __forceinline__ Unit unit_at(const BoxArgs &a, const TileCfg &t, int6
 }
 
 // ---------------------------------------------------------------------------
-// march kernel (K1m): the general X-march for shapes the TMA ring does not
-// take (odd nz, 8-byte-aligned fields, tall columns). A 32 x 4 thread block
+// march kernel (K1m): the general X-march for shapes the plane ring does not
+// take (nz > 768, inputs with different 16-byte phases). A 32 x 4 thread block
 // owns a tile of 32 levels x 4 columns and marches through an X chunk with
 // the x-1/x/x+1 window of its own (j, k) in registers; j +- 1 operands are
 // read-only-cache loads (the neighbouring columns' own operands, mostly L1
@@ -1218,7 +1227,7 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
             if (e != cudaSuccess) return set_cuda_error("advect launch", e);
         }
     } else if (!a.rim && !a.push && !(L.flags & PWADV_FLAG_SIMPLE)) {
-        // K1m: the general march (odd nz, 8-byte alignment, tall columns)
+        // K1m: the general march (nz > 768, inputs with different 16-byte phases)
         const int64_t tiles = ((L.nz + 31) / 32) * ((nby + 3) / 4);
         int64_t nch = ((int64_t)dev->sms * 16 + tiles - 1) / tiles;
         const int64_t nch_max = nbx / 8 > 1 ? nbx / 8 : 1;
