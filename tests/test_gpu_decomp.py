@@ -206,6 +206,61 @@ def test_ipc_export_map_and_write_across_processes():
         assert torch.equal(f.view(torch.int64), w.view(torch.int64))
 
 
+def _ipc_puller(q_in, q_out):
+    """Second process: K1 with the halo pull whose eight neighbours are the
+    first process's buffers, mapped by CUDA IPC (the bulk copies read them
+    through the IPC mapping, as they read another GPU's buffers over NVLink)."""
+    try:
+        import paper_2010_01545_b200 as pw2
+        from paper_2010_01545_b200 import _lib, decomp as dc, device as dv
+        torch.cuda.set_device(0)
+        exported, dims = q_in.get(timeout=120)
+        reg = dc.IpcPeerRegistry.__new__(dc.IpcPeerRegistry)
+        reg._opened, reg._bases = [], {}
+        (ptrs,) = reg.map_remote([exported])
+        g = pw2.make_grid(*dims)
+        mine = dv.fill(g, pw2.GeneratorSpec.baseline(13))  # the same values as the owner's
+        for f in mine:
+            f[0].fill_(float("nan")); f[-1].fill_(float("nan"))  # noqa: E702
+            f[:, 0].fill_(float("nan")); f[:, -1].fill_(float("nan"))  # noqa: E702
+        peers = _lib.Peers()
+        for d_ in range(8):
+            peers.u[d_], peers.v[d_], peers.w[d_] = ptrs
+            peers.nx[d_], peers.ny[d_] = g.nx, g.ny
+        out = dv.advect_pull(*mine, pw2.baseline_coefficients(13, g.nz), peers)
+        torch.cuda.synchronize()
+        q_out.put(("ok", [o.cpu().numpy() for o in out]))
+        reg.close()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q_out.put(("error", repr(e)))
+
+
+def test_ipc_pull_reads_mapped_peer_buffers():
+    """The halo pull's bulk copies reading CUDA-IPC-mapped buffers of another
+    process (on this one GPU; the owner is idle while they are read): the
+    result equals K1 on valid halos, bit for bit."""
+    import torch.multiprocessing as mp
+    from paper_2010_01545_b200.decomp import IpcPeerRegistry
+    d = pw.make_grid(40, 36, 64)
+    n = d.padded_len
+    block = torch.zeros(3 * n + 64, dtype=torch.float64, device="cuda")
+    fields = [block[8 + m * n: 8 + (m + 1) * n].view(d.padded_shape) for m in range(3)]
+    for f, w in zip(fields, device.fill(d, pw.GeneratorSpec.baseline(13))):
+        f.copy_(w)
+    want = device.advect(*fields, pw.baseline_coefficients(13, d.nz))
+    torch.cuda.synchronize()
+    ctx = mp.get_context("spawn")
+    q_in, q_out = ctx.Queue(), ctx.Queue()
+    p = ctx.Process(target=_ipc_puller, args=(q_in, q_out))
+    p.start()
+    q_in.put((IpcPeerRegistry.export(fields), (d.nx, d.ny, d.nz)))
+    status, got = q_out.get(timeout=180)
+    p.join(timeout=60)
+    assert status == "ok", got
+    for g, w in zip(got, want):
+        assert np.array_equal(g.view(np.int64), w.cpu().numpy().view(np.int64))
+
+
 # --- K1 / K4 with the halo exchange fused in (pull) ---------------------------
 
 def _poison_halos(fields):
