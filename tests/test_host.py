@@ -69,6 +69,36 @@ def test_validation_before_compute():
         _lib.check(_lib.PWADV_E_DIMS)
 
 
+def test_fused_exchange_entry_points_validate_their_peer_tables():
+    """pwadv_advect_pull_f64 / pwadv_step_pull_f64 / pwadv_step_push_f64
+    reject bad peer tables before touching the device (no GPU needed)."""
+    L = _lib.lib()
+    p, q = ctypes.c_void_p(256), ctypes.c_void_p(4096)
+
+    def table(ptr=256, nx=4, ny=4):
+        t = _lib.Peers()
+        for d in range(8):
+            t.u[d] = t.v[d] = t.w[d] = ptr
+            t.nx[d], t.ny[d] = nx, ny
+        return t
+
+    head = (p, p, p, q, q, q, 4, 4, 4, 0.1, 0.1, p, p)
+    assert L.pwadv_advect_pull_f64(*head, None, None, None) == _lib.PWADV_E_NULL
+    assert L.pwadv_advect_pull_f64(*head, ctypes.byref(table(264)), None, None) == _lib.PWADV_E_ALIGN
+    assert b"16-byte" in L.pwadv_last_error()  # the pull's bulk copies want 16 bytes
+    bad = table()
+    bad.ny[_lib.NB_XM] = 5  # an x neighbour with another y extent
+    assert L.pwadv_advect_pull_f64(*head, ctypes.byref(bad), None, None) == _lib.PWADV_E_RANGE
+    bad = table()
+    bad.u[_lib.NB_YP] = None
+    assert L.pwadv_advect_pull_f64(*head, ctypes.byref(bad), None, None) == _lib.PWADV_E_NULL
+    assert L.pwadv_advect_pull_f64(*head, ctypes.byref(table(nx=0)), None, None) == _lib.PWADV_E_DIMS
+    same = (p, p, p, p, p, p, 4, 4, 4, 0.1, 0.1, p, p, 0.1)
+    assert L.pwadv_step_pull_f64(*same, ctypes.byref(table()), None, None) == _lib.PWADV_E_ARG
+    assert L.pwadv_step_push_f64(*same, ctypes.byref(table(264)), None, None) == _lib.PWADV_E_ARG
+    assert L.pwadv_step_push_f64(*same, None, None, None) == _lib.PWADV_E_NULL
+
+
 # --- layout (reference test_grid.py) ------------------------------------------
 
 def test_make_grid_and_rejects():
