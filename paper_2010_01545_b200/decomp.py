@@ -568,8 +568,10 @@ class PullEvaluator:
             p.nx[d], p.ny[d] = nxl, nyl
         return p
 
-    def evaluate(self, out, stream=None, *, sync: bool = True, dt: float | None = None) -> None:
-        """su, sv, sw (or, with dt, the forward-Euler update) of this block into `out`."""
+    def evaluate(self, out, stream=None, *, sync: bool = True, dt: float | None = None,
+                 events=None) -> None:
+        """su, sv, sw (or, with dt, the forward-Euler update) of this block into
+        `out`; with `events` (a list) an event pair around the launch is appended."""
         from . import device as dv
         first = self.peers is None
         if (first or sync) and self.barrier is not None:
@@ -583,7 +585,9 @@ class PullEvaluator:
                 self._launches.clear()
             launch = self._launches[key] = dv.BoundLaunch(self.fields, self.coeffs, out,
                                                           opts=self.opts, dt=dt, pull=self.peers)
+        ev = dv.event_pair(events, stream)
         launch(stream)
+        dv.close_event_pair(ev, stream)
 
 
 class NcclBarrier:
@@ -666,7 +670,7 @@ class PushStepper:
             P.append(p)
         return P
 
-    def step(self, n: int = 1, stream=None) -> None:
+    def step(self, n: int = 1, stream=None, events=None) -> None:
         from . import _lib, device as dv
         if self._peers is None:  # all ranks have published by the first step
             if self._initial is not None:
@@ -679,10 +683,12 @@ class PushStepper:
         for _ in range(n):
             src, dst = self.sets[self.cur], self.sets[1 - self.cur]
             h = dv._stream_handle(stream, src[0].device)
+            ev = dv.event_pair(events, stream)
             _lib.check(L.pwadv_step_push_f64(
                 dv._p(src[0]), dv._p(src[1]), dv._p(src[2]), dv._p(dst[0]), dv._p(dst[1]),
                 dv._p(dst[2]), d.nx, d.ny, d.nz, dc.tcx, dc.tcy, dv._p(dc.tz[0]), dv._p(dc.tz[1]),
                 self.dt, ctypes.byref(self._peers[1 - self.cur]), _lib.opts_ptr(self.opts), h))
+            dv.close_event_pair(ev, stream)
             self.barrier(stream)
             self.cur = 1 - self.cur
             self.steps_done += 1

@@ -212,6 +212,22 @@ class BoundLaunch:
         _lib.check(self._fn(*self._args, _stream_handle(stream, self.device)))
 
 
+def event_pair(events, stream=None):
+    """Start a timing event pair on `stream` if `events` is a list (else None)."""
+    if events is None:
+        return None
+    s = stream or torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    events.append((a, b))
+    return b
+
+
+def close_event_pair(end, stream=None) -> None:
+    if end is not None:
+        end.record(stream or torch.cuda.current_stream())
+
+
 def self_peers(fields) -> _lib.Peers:
     """Peer table naming this block as all eight of its neighbours: a halo-pull
     launch with it evaluates the periodic domain without a halo wrap."""

@@ -46,12 +46,16 @@ class Stepper:
         else:
             device.wrap_halos(*fields, stream=stream)
 
-    def _one(self, stream=None):
+    def _one(self, stream=None, events=None):
+        """One step; with `events` (a list), a CUDA event pair recorded around
+        the K4 launch is appended (the benchmark's live kernel timing)."""
         if self.exchanger is not None:
             self.exchanger.step_overlapped(self.a, self.coeffs, self.dt, self.b, self.opts, stream)
         else:
             device.wrap_halos(*self.a, stream=stream)
+            ev = device.event_pair(events, stream)
             device.step(*self.a, self.coeffs, self.dt, self.b, opts=self.opts, stream=stream)
+            device.close_event_pair(ev, stream)
         self.a, self.b = self.b, self.a
         self._halos_fresh = False
 
