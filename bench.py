@@ -259,7 +259,7 @@ def run_ours(args):
         gx, gy = nx, ny               # the config grid is the global grid
     else:
         gx, gy = px * nx, py * ny     # the config grid is each GPU's block
-    opts = device.make_opts(args.variant)
+    opts = device.make_opts(args.variant, tile_j=args.tile_j, stages=args.stages)
     stream = torch.cuda.current_stream(dev)
 
     # inputs generated on the device (K5, reference LCG stream + BASELINE map)
@@ -719,6 +719,8 @@ def main(argv=None):
                     choices=("xmarch", "simple", "xmarch_fma", "simple_fma"))
     ap.add_argument("--chunks", type=int, default=0,
                     help="X-slab chunks of the e2e pipeline (0 = the library's automatic choice)")
+    ap.add_argument("--tile-j", type=int, default=0, help="X-march strip width (0 = the planner's)")
+    ap.add_argument("--stages", type=int, default=0, help="X-march ring depth (0 = the planner's)")
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
