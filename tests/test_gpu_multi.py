@@ -108,3 +108,27 @@ def test_nccl_exchange_and_fused_ipc_step(px, py):
     assert sorted(r for r, _, _ in results) == list(range(world))
     for r, ok, err in results:
         assert ok, (r, err)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs (one process per GPU)")
+@pytest.mark.parametrize("config", ["c1", "c4"])
+def test_bench_under_torchrun(config):
+    """bench.py as the driver launches it for N=2 (torchrun, one rank per GPU):
+    one JSON line from rank 0, the fused multi-GPU path in use (halo pull for
+    evaluations, peer-store push for steps), bit-exact spot check."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(root / "bench.py"),
+           "--gpus", "2", "--config", config, "--steps", "10", "--warmup", "3", "--no-cpu", "--no-e2e"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    step = d["config"].get("multi_gpu_step", "")
+    assert ("halo pull" in step) if config == "c1" else ("peer stores" in step), step
