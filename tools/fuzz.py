@@ -1,0 +1,83 @@
+"""Randomised parity fuzz of K1 / K4 plans against the C oracle: random grid
+shapes (odd and even nz, thin and wide), random plan options (tile width,
+ring depth, chunks, grid), every kernel form (aligned X-march, UA forced,
+K1m, one-thread), the halo pull with the block as its own neighbours (NaN
+halos), and the fused step. Prints one JSON line; exit 1 on any mismatch.
+
+    python tools/fuzz.py [--cases 200] [--seed 1]
+"""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2010_01545_b200 as pw  # noqa: E402
+from paper_2010_01545_b200 import device  # noqa: E402
+from oracle import oracle  # noqa: E402  (checker)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", type=int, default=200)
+    ap.add_argument("--seed", type=int, default=1)
+    a = ap.parse_args()
+    rng = np.random.default_rng(a.seed)
+    bad, done = [], 0
+    for n in range(a.cases):
+        nz = int(rng.choice([2, 3, 5, 8, 16, 31, 33, 63, 64, 65, 96, 99, 127, 128, 200, 257]))
+        nx = int(rng.integers(1, 90))
+        ny = int(rng.integers(1, 400 if nz <= 64 else 120))
+        seed = int(rng.integers(0, 2**31))
+        u, v, w = oracle.fill_random(nx, ny, nz, seed, baseline=True)
+        co = oracle.baseline_coefficients(seed, nz)
+        args = (co["tcx"], co["tcy"], co["tzc1"], co["tzc2"])
+        want = oracle.advect(u, v, w, *args, engines=oracle.host_threads())
+        dims = pw.make_grid(nx, ny, nz)
+        f = [torch.from_numpy(x).cuda() for x in (u, v, w)]
+        dco = pw.AdvectionCoefficients(*args)
+        kw = {}
+        if rng.random() < 0.5:
+            kw["tile_j"] = int(rng.integers(1, 13))
+        if rng.random() < 0.3:
+            kw["stages"] = int(rng.integers(3, 8))
+        if rng.random() < 0.3:
+            kw["chunks"] = int(rng.integers(1, 9))
+        if rng.random() < 0.3:
+            kw["grid"] = int(rng.integers(1, 160))
+        variant = str(rng.choice(["xmarch", "xmarch_elem", "march", "simple"]))
+        case = {"shape": [nx, ny, nz], "variant": variant, **kw}
+        try:
+            out = device.advect(*f, dco, opts=device.make_opts(variant, **kw))
+            torch.cuda.synchronize()
+            if not oracle.compare([o.cpu().numpy() for o in out], want)["bitwise_equal"]:
+                bad.append({**case, "what": "advect"})
+            if nz % 2 == 0 and nz <= 768 and variant == "xmarch":
+                g = [t.clone() for t in f]
+                for t in g:
+                    t[0].fill_(float("nan")); t[-1].fill_(float("nan"))  # noqa: E702
+                    t[:, 0].fill_(float("nan")); t[:, -1].fill_(float("nan"))  # noqa: E702
+                outp = device.advect_pull(*g, dco, device.self_peers(g), opts=device.make_opts(variant, **kw))
+                torch.cuda.synchronize()
+                if not oracle.compare([o.cpu().numpy() for o in outp], want)["bitwise_equal"]:
+                    bad.append({**case, "what": "pull"})
+            nxt = device.alloc_fields(dims, "cuda")
+            device.step(*f, dco, 0.1, nxt, opts=device.make_opts(variant, **kw))
+            torch.cuda.synchronize()
+            for gtn, fh, s in zip(nxt, (u, v, w), want):
+                if not np.array_equal(gtn.cpu().numpy()[1:-1, 1:-1].view(np.int64),
+                                      (fh + 0.1 * s)[1:-1, 1:-1].view(np.int64)):
+                    bad.append({**case, "what": "step"})
+                    break
+        except Exception as e:  # noqa: BLE001
+            bad.append({**case, "what": f"error {type(e).__name__}: {e}"[:200]})
+        done += 1
+    print(json.dumps({"cases": done, "mismatches": len(bad), "first": bad[:5]}))
+    return 1 if bad else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
