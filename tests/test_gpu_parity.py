@@ -813,3 +813,15 @@ def test_general_march_kernel_bitwise(shape):
     gf, _ = gpu_advect(u, v, w, *args, "xmarch_fma")
     r = oracle.compare(gf, want)
     assert r["normwise_rel"] <= 1e-12, r
+
+
+def test_randomised_plan_fuzz():
+    """tools/fuzz.py on a fixed seed: random shapes x plan options x kernel
+    forms (K1, K4, halo pull) bit-exact against the oracle."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, str(root / "tools" / "fuzz.py"), "--cases", "120", "--seed", "11"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-2000:])
