@@ -2,7 +2,7 @@
 shapes (odd and even nz, thin and wide), random plan options (tile width,
 ring depth, chunks, grid), every kernel form (aligned X-march, UA forced,
 K1m, one-thread), the halo pull with the block as its own neighbours (NaN
-halos), and the fused step. Prints one JSON line; exit 1 on any mismatch.
+halos), the fused step, and the halo pull over random x-y decompositions. Prints one JSON line; exit 1 on any mismatch.
 
     python tools/fuzz.py [--cases 200] [--seed 1]
 """
@@ -72,6 +72,42 @@ def main():
                                       (fh + 0.1 * s)[1:-1, 1:-1].view(np.int64)):
                     bad.append({**case, "what": "step"})
                     break
+        except Exception as e:  # noqa: BLE001
+            bad.append({**case, "what": f"error {type(e).__name__}: {e}"[:200]})
+        done += 1
+    # the halo pull over random x-y decompositions (every block's neighbours
+    # are the other blocks' buffers on this GPU; blocks evaluated in turn)
+    from paper_2010_01545_b200.decomp import Decomposition, LocalPeerRegistry, PullEvaluator
+    for n in range(max(1, a.cases // 10)):
+        nz = int(rng.choice([2, 6, 16, 64, 96, 128]))
+        px, py = int(rng.integers(1, 4)), int(rng.integers(1, 5))
+        nx, ny = int(rng.integers(px, 70)), int(rng.integers(py, 150))
+        seed = int(rng.integers(0, 2**31))
+        gd = pw.make_grid(nx, ny, nz)
+        spec = pw.GeneratorSpec.baseline(seed)
+        co = pw.baseline_coefficients(seed, nz)
+        host = oracle.fill_random(nx, ny, nz, seed, baseline=True)
+        want = oracle.advect(*host, co.tcx, co.tcy, co.tzc1, co.tzc2, engines=oracle.host_threads())
+        case = {"pull_decomposition": [nx, ny, nz, px, py]}
+        try:
+            reg, evs = LocalPeerRegistry(), []
+            for r in range(px * py):
+                dec = Decomposition(gd, px, py, r)
+                fs = dec.fill_local(spec)
+                for t in fs:
+                    t[0].fill_(float("nan")); t[-1].fill_(float("nan"))  # noqa: E702
+                    t[:, 0].fill_(float("nan")); t[:, -1].fill_(float("nan"))  # noqa: E702
+                evs.append((dec, PullEvaluator(dec, fs, co, reg)))
+            for dec, ev in evs:
+                o = device.alloc_fields(dec.local_dims, "cuda")
+                ev.evaluate(o)
+                torch.cuda.synchronize()
+                xo, bx, yo, by = dec.block()
+                for got, wnt in zip(o, want):
+                    if not np.array_equal(got.cpu().numpy()[1:-1, 1:-1].view(np.int64),
+                                          wnt[1 + xo:1 + xo + bx, 1 + yo:1 + yo + by].view(np.int64)):
+                        bad.append({**case, "rank": dec.rank})
+                        break
         except Exception as e:  # noqa: BLE001
             bad.append({**case, "what": f"error {type(e).__name__}: {e}"[:200]})
         done += 1
