@@ -2,7 +2,8 @@
 shapes (odd and even nz, thin and wide), random plan options (tile width,
 ring depth, chunks, grid), every kernel form (aligned X-march, UA forced,
 K1m, one-thread), the halo pull with the block as its own neighbours (NaN
-halos), the fused step, and the halo pull over random x-y decompositions. Prints one JSON line; exit 1 on any mismatch.
+halos), the fused step, and the halo pull and the fused push step over
+random x-y decompositions. Prints one JSON line; exit 1 on any mismatch.
 
     python tools/fuzz.py [--cases 200] [--seed 1]
 """
@@ -106,6 +107,42 @@ def main():
                 for got, wnt in zip(o, want):
                     if not np.array_equal(got.cpu().numpy()[1:-1, 1:-1].view(np.int64),
                                           wnt[1 + xo:1 + xo + bx, 1 + yo:1 + yo + by].view(np.int64)):
+                        bad.append({**case, "rank": dec.rank})
+                        break
+        except Exception as e:  # noqa: BLE001
+            bad.append({**case, "what": f"error {type(e).__name__}: {e}"[:200]})
+        done += 1
+    # the fused push step over random decompositions, a few steps, ranks
+    # stepped in turn on one stream (no kernel waits on another)
+    from paper_2010_01545_b200.decomp import PushStepper
+    from paper_2010_01545_b200.stepper import Stepper
+    for n in range(max(1, a.cases // 20)):
+        nz = int(rng.choice([2, 5, 16, 33, 64, 128]))
+        px, py = int(rng.integers(1, 4)), int(rng.integers(1, 5))
+        nx, ny = int(rng.integers(px, 60)), int(rng.integers(py, 120))
+        steps = int(rng.integers(1, 5))
+        seed = int(rng.integers(0, 2**31))
+        gd = pw.make_grid(nx, ny, nz)
+        spec = pw.GeneratorSpec.baseline(seed)
+        co = pw.baseline_coefficients(seed, nz)
+        case = {"push_decomposition": [nx, ny, nz, px, py, steps]}
+        try:
+            g = device.fill(gd, spec)
+            single = Stepper([t.clone() for t in g], co, 0.1)
+            single.step(steps)
+            want = single.fields
+            reg, sts = LocalPeerRegistry(), []
+            for r in range(px * py):
+                dec = Decomposition(gd, px, py, r)
+                fs = tuple(dec.local_view(t).contiguous() for t in g)
+                sts.append((dec, PushStepper(dec, fs, co, 0.1, reg, lambda stream=None: None)))
+            for _ in range(steps):
+                for _, st in sts:
+                    st.step(1)
+            torch.cuda.synchronize()
+            for dec, st in sts:
+                for got, wnt in zip(st.fields, want):
+                    if not torch.equal(got.view(torch.int64), dec.local_view(wnt).contiguous().view(torch.int64)):
                         bad.append({**case, "rank": dec.rank})
                         break
         except Exception as e:  # noqa: BLE001
