@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define PWADV_ABI_VERSION 1
+#define PWADV_ABI_VERSION 2
 
 enum {
     PWADV_OK = 0,
@@ -70,6 +70,11 @@ enum {
  * (they select the run-time-layout X-march, as PWADV_FLAG_GENERIC) */
 #define PWADV_FLAG_DEBUG_NO_COMPUTE 0x100u
 #define PWADV_FLAG_DEBUG_NO_STORE 0x400u
+/* X-march work plan: never / always (where it applies) use the spare-tail
+ * plan (main chunks + tail chunks run by the spare CTAs; default: when it
+ * shortens the longest CTA by >= 5%) */
+#define PWADV_FLAG_NO_SPARE_TAIL 0x1000u
+#define PWADV_FLAG_SPARE_TAIL 0x2000u
 
 /* Optional tuning / variant selection; pass NULL for defaults. */
 typedef struct pwadv_opts {
@@ -131,6 +136,9 @@ typedef struct pwadv_plan_info {
     int64_t smem_bytes, strips;
     int32_t chunks;        /* X chunks of the strips after the full rounds */
     int32_t long_strips;   /* strips run as whole-X units (full rounds of the grid) */
+    int32_t spare_ctas;    /* spare-tail plan: CTAs running the strips' tail chunks (0 = off);
+                              then `chunks` main chunks of main_chunk_planes per strip */
+    int32_t main_chunk_planes;
 } pwadv_plan_info;
 int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz,
                         int64_t x_begin, int64_t x_end, int64_t y_begin, int64_t y_end,

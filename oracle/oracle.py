@@ -384,3 +384,56 @@ def compare(a, b) -> dict:
     mu = max(max_ulp(x, y) for x, y in pairs)
     return {"bitwise_equal": False, "max_abs_diff": max_abs, "max_ulp_diff": max(mu, 1),
             "normwise_rel": max_abs / ref_max}
+
+
+def _host(a) -> np.ndarray:
+    """numpy view/copy of a host array or a torch tensor (device or host)."""
+    if hasattr(a, "detach"):
+        return a.detach().cpu().numpy()
+    return np.asarray(a)
+
+
+def compare_streamed(fields, outs, tcx, tcy, tzc1, tzc2, *, dt=None, slab: int = 64,
+                     engines: int = 0) -> dict:
+    """Every plane of a result against the C oracle, X-slab by X-slab.
+
+    `fields` (u, v, w) and `outs` (su, sv, sw — or, with `dt`, the stepped
+    u', v', w') are padded (nx+2, ny+2, nz) arrays or torch tensors on any
+    device. Output planes [x0, x1) need input planes [x0-1, x1+1] only, so
+    each slab of `slab` planes is copied to the host with one halo plane on
+    each side and evaluated by the C restatement of run_reference
+    (kernel.py:175-185), threaded over all host cores; memory stays bounded
+    at full config sizes. Evaluations compare the whole padded output planes
+    (halo columns and level 0 must be +0.0, as in zeros_sources); steps
+    compare the interior columns against f + dt*s (mul then add), the
+    composed oracle of SURVEY.md §8f1. Returns compare()'s record plus the
+    planes checked and the first mismatching plane."""
+    nx = int(fields[0].shape[0]) - 2
+    engines = engines or host_threads()
+    tz1 = np.ascontiguousarray(_host(tzc1), dtype=np.float64)
+    tz2 = np.ascontiguousarray(_host(tzc2), dtype=np.float64)
+    res = {"bitwise_equal": True, "max_abs_diff": 0.0, "max_ulp_diff": 0, "normwise_rel": 0.0}
+    first_bad = None
+    planes = 0
+    for x0 in range(1, nx + 1, slab):
+        x1 = min(x0 + slab, nx + 1)
+        ins = [np.ascontiguousarray(_host(f[x0 - 1:x1 + 1]), dtype=np.float64) for f in fields]
+        want = advect(*ins, tcx, tcy, tz1, tz2, engines=max(1, min(engines, x1 - x0)))
+        got = [_host(o[x0:x1]) for o in outs]
+        if dt is None:
+            want = [wv[1:-1] for wv in want]
+        else:
+            want = [(f[1:-1] + float(dt) * s)[:, 1:-1] for f, s in zip(ins, (wv[1:-1] for wv in want))]
+            got = [g[:, 1:-1] for g in got]
+        c = compare(got, want)
+        planes += x1 - x0
+        if not c["bitwise_equal"]:
+            if first_bad is None:
+                first_bad = x0
+            res["bitwise_equal"] = False
+            res["max_abs_diff"] = max(res["max_abs_diff"], c["max_abs_diff"])
+            res["max_ulp_diff"] = max(res["max_ulp_diff"], c["max_ulp_diff"])
+            res["normwise_rel"] = max(res["normwise_rel"], c["normwise_rel"])
+    res["planes_checked"] = planes
+    res["first_bad_slab"] = first_bad
+    return res

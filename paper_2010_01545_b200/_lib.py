@@ -41,6 +41,9 @@ FLAG_RIM = 16
 FLAG_GENERIC = 32
 FLAG_L2_UNIT_HEAD = 64
 FLAG_NO_PDL = 128
+FLAG_NO_SPARE_TAIL = 0x1000
+FLAG_SPARE_TAIL = 0x2000
+ABI_VERSION = 2
 
 
 class Opts(ctypes.Structure):
@@ -59,7 +62,8 @@ class PlanInfo(ctypes.Structure):
                 ("threads_per_column", ctypes.c_int32), ("stages", ctypes.c_int32),
                 ("threads", ctypes.c_int32), ("grid", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_int64), ("strips", ctypes.c_int64),
-                ("chunks", ctypes.c_int32), ("long_strips", ctypes.c_int32)]
+                ("chunks", ctypes.c_int32), ("long_strips", ctypes.c_int32),
+                ("spare_ctas", ctypes.c_int32), ("main_chunk_planes", ctypes.c_int32)]
 
 
 class Peers(ctypes.Structure):
@@ -142,8 +146,8 @@ def lib():
                 fn.restype = res
                 fn.argtypes = args
             abi = L.pwadv_abi_version()
-            if abi != 1:
-                raise ImportError(f"libpwadv ABI {abi} != 1")
+            if abi != ABI_VERSION:
+                raise ImportError(f"libpwadv ABI {abi} != {ABI_VERSION}")
             _lib = L
     return _lib
 

@@ -45,6 +45,7 @@
 #include "pwadv_device.cuh"
 #include "pwadv_internal.h"
 
+#include <algorithm>
 #include <mutex>
 #include <type_traits>
 #include <vector>
@@ -145,11 +146,19 @@ struct TileCfg {
                       // whose tiles take six copies per plane, fall in the chunked tail)
     int nface;        // halo pull: the last nface strips of the tail (the y-face strips)
     int nchf;         //   are cut into nchf chunks instead of nchunks (shorter units)
+    // spare-tail plan (spare > 0; plan_xmarch): every strip is cut into nchunks
+    // main chunks of mlen planes, run by CTAs 0 .. nstrips*nchunks-1 in one
+    // round, and one tail chunk (the rest of X), run by the `spare` remaining
+    // CTAs, several in sequence — so a grid whose strips do not divide the SM
+    // count still keeps every SM busy for about the same time
+    int spare;
+    int64_t mlen;
 };
 
 // work units of a launch (unit_at's numbering)
-__host__ __device__ __forceinline__ int64_t units_of(const TileCfg &t)
+__host__ __device__ __forceinline__ int64_t units_of(const TileCfg &t, int64_t G)
 {
+    if (t.spare > 0) return G * ((t.nstrips + t.spare - 1) / t.spare);  // rounds x grid, with holes
     return t.nlong + (t.nstrips - t.nlong - t.nface) * t.nchunks + (int64_t)t.nface * t.nchf;
 }
 
@@ -169,6 +178,34 @@ __device__ __forceinline__ Unit unit_at(const BoxArgs &a, const TileCfg &t, int6
 {
     const int64_t nxr = a.x1 - a.x0;
     Unit w;
+    if (t.spare > 0) {
+        // spare-tail plan: unit u = round r of CTA b. Round 0 of CTAs
+        // 0 .. M-1 are the main chunks (CTA b: strip b % nstrips, chunk
+        // b / nstrips — all concurrent, so neighbouring strips stand on the
+        // same planes and share their halo columns through L2); the tail
+        // chunks go to the spare CTAs M .. G-1, strip r*spare + (b-M) in
+        // round r (adjacent strips' tails again run concurrently). Units
+        // outside these are empty (ib == ie) and skipped.
+        const int64_t G = gridDim.x, M = t.nstrips * t.nchunks;
+        const int64_t r = u / G, b = u - r * G;
+        w.ib = w.ie = a.x0;
+        w.strip = 0;
+        if (b < M) {
+            if (r == 0) {
+                w.strip = b % t.nstrips;
+                w.ib = a.x0 + (b / t.nstrips) * t.mlen;
+                w.ie = w.ib + t.mlen;
+            }
+        } else {
+            const int64_t s = r * t.spare + (b - M);
+            if (s < t.nstrips) {
+                w.strip = s;
+                w.ib = a.x0 + t.nchunks * t.mlen;
+                w.ie = a.x1;
+            }
+        }
+        return w;
+    }
     if (u < t.nlong) {
         w.strip = u + t.rot < t.nstrips ? u + t.rot : u + t.rot - t.nstrips;
         w.ib = a.x0;
@@ -639,14 +676,15 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     const double c2a = __ldg(a.tzc2 + k0), c2b = __ldg(a.tzc2 + k1c);
 
     const int64_t ny2 = a.ny + 2;
-    const int64_t nunits = units_of(t);
     const int64_t G = gridDim.x;
+    const int64_t nunits = units_of(t, G);
     if ((int64_t)blockIdx.x >= nunits) return;
 
     if (tid == 0) {
         int q = 0, k = 0;
-        for (int64_t u = blockIdx.x; u < nunits && k < kMaxUnitsPerCta; u += G, ++k) {
+        for (int64_t u = blockIdx.x; u < nunits && k < kMaxUnitsPerCta; u += G) {
             const Unit w = unit_at(a, t, u);
+            if (w.ie <= w.ib) continue;  // a hole of the spare-tail plan
             const int64_t j0 = a.y0 + w.strip * TJ;
             const int64_t tjs = (a.y1 - j0) < TJ ? (a.y1 - j0) : TJ;
             rs->first[k] = q;
@@ -668,6 +706,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
                 }
             }
             q += (int)(w.ie - w.ib + 2);
+            ++k;
         }
         rs->first[k] = q;
         rs->total = q;
@@ -819,10 +858,11 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     double sxu_a, sxu_b, txu_a, txu_b, rxu_a, rxu_b;
 
     for (int k = 0; k < my_units; ++k) {
-        const Unit wu = unit_at(a, t, (int64_t)blockIdx.x + (int64_t)k * G);
-        const int64_t ib = wu.ib, ie = wu.ie;
-        const int64_t j0 = a.y0 + wu.strip * TJ;
-        const int64_t tjs = (a.y1 - j0) < TJ ? (a.y1 - j0) : TJ;
+        // the unit's geometry from the table tid 0 built (planes ib-1 .. ie)
+        const int64_t ib = (int64_t)rs->ui0[k] + 1;
+        const int64_t ie = ib + (rs->first[k + 1] - rs->first[k]) - 2;
+        const int64_t j0 = rs->uj0[k];
+        const int64_t tjs = rs->utj[k];
         const bool active = in_tile && c < tjs;
         // fused step with the halo push: a thread on the y = 1 or y = ny face
         // stores its pair into one neighbour's halo column every plane — a
@@ -1144,6 +1184,8 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         t.rot = plan.rot;
         t.nface = plan.nface;
         t.nchf = plan.nchf;
+        t.spare = plan.spare;
+        t.mlen = plan.mlen;
         void (*kern)(BoxArgs, TileCfg) = nullptr;
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
         // compile-time layout for the BASELINE depths at the default tile
@@ -1319,8 +1361,7 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
         const size_t stage_bytes = (size_t)3 * slot_doubles(tj, nz, ua) * sizeof(double);
         int smax = (int)(smem_cap / stage_bytes);
         if (smax > 16) smax = 16;  // RingState::released
-        // default ring depth 5 (tools/sweep.py); single-round plans deepen it
-        // to 6 below
+        // default ring depth 5 (tools/sweep.py; see the note at the end)
         stages = L.stages > 0 ? (L.stages < smax ? L.stages : smax) : (smax < 5 ? smax : 5);
         if (stages >= 3) break;
         if (tj == 1) return false;
@@ -1398,18 +1439,52 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
         p->grid = (int)grid;
         p->rounds = (units + grid - 1) / grid;
     }
-    // Ring depth measured with interleaved sweeps (tools/sweep.py --rounds,
-    // profiles/README.md): a plan that is one round of long units (C1: 129
-    // CTAs x 171 planes) streams better with 6 stages (124.7 vs 121.0 Gpts/s
-    // sustained); multi-round plans keep 5 (C2 129 vs 125; a cold C4 launch
-    // read 4% more DRAM with 6).
-    if (L.stages <= 0 && maxt == 512 && p->rounds == 1) {
-        const size_t stage_bytes = (size_t)3 * slot_doubles(tj, nz, ua) * sizeof(double);
-        if ((size_t)6 * stage_bytes <= smem_cap) {
-            p->stages = 6;
-            p->smem = (size_t)6 * stage_bytes + 2 * 6 * sizeof(uint64_t) + sizeof(RingState);
+    // Spare-tail plan. A single-round plan whose units do not fill the SMs
+    // (C1 512x512x64: 43 strips x 3 chunks = 129 CTAs of 171 planes, 19 SMs
+    // idle) is rebalanced: each strip gets m main chunks of L planes (one per
+    // CTA, all concurrent) and one tail chunk of nbx - m*L planes; the G - n*m
+    // spare CTAs run the n tail chunks, ceil(n / spare) each in sequence. L
+    // balances a main CTA's L + 2 planes against a spare CTA's tail planes
+    // (C1: m = 3, L = 154, tails of 50, 3 per spare CTA: 156 planes per CTA
+    // instead of 173, on all 148 SMs).
+    p->spare = 0;
+    p->mlen = 0;
+    if (!L.pull && L.chunks <= 0 && L.grid <= 0 && full_rounds == 0 && per_sm == 1 &&
+        !(L.flags & PWADV_FLAG_NO_SPARE_TAIL) && p->rounds == 1 && !p->nface) {
+        const int64_t n = p->nstrips;
+        int64_t best_m = 0, best_l = 0, best_sp = 0, best_planes = 0;
+        for (int64_t m = 1; n * m < g0; ++m) {
+            const int64_t sp = std::min<int64_t>(g0 - n * m, n);
+            const int64_t rt = (n + sp - 1) / sp;
+            if (rt > kMaxUnitsPerCta) continue;
+            // L + 2 = rt * (nbx - m*L + 2)  ->  L = (rt*(nbx+2) - 2) / (1 + m*rt)
+            const int64_t l0 = (rt * (nbx + 2) - 2) / (1 + m * rt);
+            for (int64_t l = l0; l <= l0 + 1; ++l) {
+                if (l < 1 || m * l >= nbx) continue;
+                const int64_t planes = std::max<int64_t>(l + 2, rt * (nbx - m * l + 2));
+                if (best_m == 0 || planes < best_planes) {
+                    best_m = m;
+                    best_l = l;
+                    best_sp = sp;
+                    best_planes = planes;
+                }
+            }
+        }
+        const int64_t cur = (nbx + p->nchunks - 1) / p->nchunks + 2;  // planes per CTA now
+        if (best_m > 0 && ((L.flags & PWADV_FLAG_SPARE_TAIL) || best_planes * 100 <= cur * 95)) {
+            p->spare = (int)best_sp;
+            p->mlen = best_l;
+            p->nchunks = (int)best_m;
+            p->grid = (int)(n * best_m + best_sp);
+            p->rounds = (n + best_sp - 1) / best_sp;
         }
     }
+    // Ring depth: 5 stages (the default above) for every plan. Measured as
+    // the bench runs it — bursts of back-to-back launches at full clocks
+    // (tools/sweep.py --burst-sleep 0.3 --prewarm-ms 30, profiles/README.md):
+    // C1 131 / C2 131.8 / C3 133.8 / C4 block 134.8 Gpts/s with 5 stages
+    // against 118-126 with 6 and 128 with 4. (Round 1 chose 6 for single-
+    // round plans from sustained, power-capped runs.)
     return true;
 }
 

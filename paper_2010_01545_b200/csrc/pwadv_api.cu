@@ -337,6 +337,8 @@ int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz, int64_t x0, int64_t 
         out->strips = p.nstrips;
         out->chunks = p.nchunks;
         out->long_strips = (int32_t)p.nlong;
+        out->spare_ctas = p.spare;
+        out->main_chunk_planes = (int32_t)p.mlen;
     } else if (!(L.flags & (PWADV_FLAG_SIMPLE | PWADV_FLAG_RIM))) {
         out->kernel = 3;  // the general march (launch_box)
         out->threads = 128;

@@ -40,6 +40,8 @@ struct XmarchPlan {
     int64_t nlong;   // strips run as whole-X units (full rounds)
     int elem;        // 1: unaligned tile runs (UA kernels: odd nz, 8-byte alignment)
     int rot, nface, nchf;  // halo pull: strip rotation and the y-face strips' chunking
+    int spare;             // spare-tail plan: CTAs running the strips' tail chunks (0 = off)
+    int64_t mlen;          //   planes per main chunk (nchunks main chunks per strip)
 };
 
 // cached attributes of the current device (lazily filled, thread-safe)

@@ -299,7 +299,8 @@ def describe_plan(dims: GridDims, box=None, opts: _lib.Opts | None = None, devic
     return {"kernel": {1: "xmarch", 2: "simple", 3: "march", 4: "xmarch_elem"}[info.kernel], "tile_j": info.tile_j,
             "threads_per_column": info.threads_per_column, "stages": info.stages,
             "threads": info.threads, "grid": info.grid, "smem_bytes": info.smem_bytes,
-            "strips": info.strips, "chunks": info.chunks, "long_strips": info.long_strips}
+            "strips": info.strips, "chunks": info.chunks, "long_strips": info.long_strips,
+            "spare_ctas": info.spare_ctas, "main_chunk_planes": info.main_chunk_planes}
 
 
 # ---------------------------------------------------------------------------

@@ -120,6 +120,15 @@ def plan_traffic(dims: GridDims, box, plan: dict) -> TrafficReport:
     tj, nch = plan["tile_j"], plan.get("chunks", 1)
     nstrips, nlong = plan["strips"], plan.get("long_strips", 0)
     widths = [min(tj, nby - s * tj) for s in range(nstrips)]
+    if plan.get("spare_ctas", 0) > 0:
+        # spare-tail plan: nch main chunks of mlen planes + one tail chunk per strip
+        mlen = plan["main_chunk_planes"]
+        per_col = nch * (mlen + 2) + (nbx - nch * mlen + 2)
+        tr.external_reads = 3 * nz * per_col * sum(w + 2 for w in widths)
+        tr.local_writes = tr.external_reads
+        tr.local_reads = 9 * nbx * nby * nz
+        tr.scratch_bytes_peak = int(plan["smem_bytes"])
+        return tr
     # work units (pwadv_advect.cu unit_at): strips 0..nlong-1 whole, the rest
     # in nch X chunks; each unit streams its planes + one on each side
     planes = sum((nbx + 2) * (widths[s] + 2) for s in range(nlong))

@@ -296,6 +296,50 @@ def test_large_configs_slabwise_and_properties(shape):
     del again
 
 
+@pytest.mark.parametrize("shape", [(1024, 1024, 64), (2048, 2048, 64)])
+def test_large_configs_every_plane_streamed(shape):
+    """C2 / C3 at full size, every plane of su, sv, sw against the C oracle,
+    bitwise: X slabs of 64 planes (+1 halo plane each side) streamed to the
+    host and evaluated on all host cores — every chunk and unit edge of the
+    plan is covered, not a sample."""
+    dims, fields, co = baseline_case(*shape)
+    plan = device.describe_plan(dims)
+    outs = device.advect(*fields, co)
+    torch.cuda.synchronize()
+    r = oracle.compare_streamed(fields, outs, co.tcx, co.tcy, co.tzc1, co.tzc2, slab=64)
+    assert r["planes_checked"] == dims.nx
+    assert r["bitwise_equal"], (shape, plan, r)
+
+
+def test_config1_spare_tail_and_classic_plans_every_plane():
+    """C1 under both work plans (spare-tail: 148 CTAs; classic: 129), and the
+    fused step K4 under the default plan, every plane against the oracle."""
+    dims, fields, co = baseline_case(512, 512, 64)
+    for flags in (_lib.FLAG_SPARE_TAIL, _lib.FLAG_NO_SPARE_TAIL):
+        opts = device.make_opts("xmarch", flags=flags)
+        plan = device.describe_plan(dims, None, opts)
+        assert (plan["spare_ctas"] > 0) == (flags == _lib.FLAG_SPARE_TAIL), plan
+        outs = device.advect(*fields, co, opts=opts)
+        r = oracle.compare_streamed(fields, outs, co.tcx, co.tcy, co.tzc1, co.tzc2)
+        assert r["bitwise_equal"], (plan, r)
+    nxt = device.alloc_fields(dims, "cuda")
+    device.step(*fields, co, 0.1, nxt)
+    r = oracle.compare_streamed(fields, nxt, co.tcx, co.tcy, co.tzc1, co.tzc2, dt=0.1)
+    assert r["bitwise_equal"], r
+
+
+@pytest.mark.parametrize("shape", [(2048, 1024, 128)])
+def test_config4_block_step_every_plane_streamed(shape):
+    """One fused forward step K4 of BASELINE config 4's per-GPU block
+    (2048x1024x128), every plane of u', v', w' against the composed oracle."""
+    dims, fields, co = baseline_case(*shape, seed=42)
+    nxt = device.alloc_fields(dims, "cuda")
+    device.step(*fields, co, 0.1, nxt)
+    torch.cuda.synchronize()
+    r = oracle.compare_streamed(fields, nxt, co.tcx, co.tcy, co.tzc1, co.tzc2, dt=0.1, slab=32)
+    assert r["planes_checked"] == dims.nx and r["bitwise_equal"], r
+
+
 def test_config4_nz128_bitwise():
     dims, fields, co = baseline_case(96, 80, 128, seed=7)
     outs = device.advect(*fields, co)

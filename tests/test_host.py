@@ -35,7 +35,7 @@ def test_library_exports_every_header_symbol():
         assert hasattr(L, n), n
         assert n in _lib.SIGNATURES, f"{n} missing from the ctypes binding"
     assert set(_lib.SIGNATURES) == set(names)
-    assert L.pwadv_abi_version() == 1
+    assert L.pwadv_abi_version() == _lib.ABI_VERSION
 
 
 def test_library_is_sm100a_cubin():

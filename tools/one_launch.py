@@ -3,6 +3,7 @@ the given options — a small target for ncu metric runs.
 
     python tools/one_launch.py 4096x4096x128 --chunks 8 [--step] [--n 3]
         [--variant xmarch_elem] [--pull]   (--pull: the block as its own neighbours)
+        [--stages S] [--flags 0x1000]
 """
 import argparse
 import sys
@@ -23,13 +24,15 @@ def main():
     ap.add_argument("--n", type=int, default=3)
     ap.add_argument("--variant", default="xmarch")
     ap.add_argument("--pull", action="store_true")
+    ap.add_argument("--stages", type=int, default=0)
+    ap.add_argument("--flags", type=lambda x: int(x, 0), default=0)
     a = ap.parse_args()
     nx, ny, nz = (int(x) for x in a.grid.split("x"))
     dims = pw.make_grid(nx, ny, nz)
     f = device.fill(dims, pw.GeneratorSpec.baseline(42))
     co = device.DeviceCoefficients.from_host(pw.baseline_coefficients(42, nz), f[0].device)
     out = device.alloc_fields(dims, f[0].device)
-    opts = device.make_opts(a.variant, chunks=a.chunks)
+    opts = device.make_opts(a.variant, chunks=a.chunks, stages=a.stages, flags=a.flags)
     print(device.describe_plan(dims, None, opts))
     peers = device.self_peers(f) if a.pull else None
     for _ in range(a.n):

@@ -20,9 +20,24 @@ SHAPES = {"c1": (512, 512, 64), "c2": (1024, 1024, 64), "c3": (2048, 2048, 64),
           "c2blk8": (512, 256, 64), "c2blk4": (512, 512, 64)}
 
 
+BURST_SLEEP = 0.0
+PREWARM_MS = 0.0
+
+
 def time_it(fn, reps):
-    for _ in range(5):
-        fn()
+    import time
+    if BURST_SLEEP:
+        # the driver's bench shape: a short burst after an idle gap (no power
+        # cap), with the clocks ramped by PREWARM_MS of the same launches
+        torch.cuda.synchronize()
+        time.sleep(BURST_SLEEP)
+    t_end = time.perf_counter() + PREWARM_MS / 1e3
+    while True:
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize()
+        if time.perf_counter() >= t_end:
+            break
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
@@ -41,7 +56,14 @@ def main():
     ap.add_argument("--rounds", type=int, default=1)
     ap.add_argument("--step", action="store_true", help="time the fused step K4 (ping-pong) instead of K1")
     ap.add_argument("--variants", default="", help="JSON list of variant dicts (overrides)")
+    ap.add_argument("--burst-sleep", type=float, default=0.0,
+                    help="idle seconds before each timed burst (mimics bench.py --steps 20)")
+    ap.add_argument("--prewarm-ms", type=float, default=0.0,
+                    help="untimed launches for this long before each timed burst")
     args = ap.parse_args()
+    global BURST_SLEEP, PREWARM_MS
+    BURST_SLEEP = args.burst_sleep
+    PREWARM_MS = args.prewarm_ms
     nx, ny, nz = SHAPES[args.config]
     dims = pw.make_grid(nx, ny, nz)
     fields = device.fill(dims, pw.GeneratorSpec.baseline(42))
