@@ -23,11 +23,11 @@ MEASURED_PEAKS.json, the CPU oracle port timed on this host's cores
 path with H2D/D2H copies inside the timed region (`e2e`), our kernel launch
 count, and SM clocks sampled during the timed region.
 
-`--impl reference` times the reference's own CPU path as written (numpy
-run_schedule with X-slab engine threads, restated in oracle/ because the
-reference package is not on the GPU box) on a bounded sample of the same
-config, the C port of the algorithm beside it, and prints the same JSON line
-with "impl": "reference".
+`--impl reference` times the stock reference package (baseline/_ref, pip-
+installed from /root/reference/pkg, unmodified): its numpy run_schedule with
+X-slab engine threads on the full config grid, its single-thread
+run_reference beside it, and the C port of the algorithm for context, and
+prints the same JSON line with "impl": "reference".
 """
 
 from __future__ import annotations
@@ -228,6 +228,26 @@ def cpu_baseline_arm(nx, ny, nz, reps=400, max_seconds=10.0):
                       f"{len(times)} times over {time.perf_counter() - t_start:.1f} s (value = best, "
                       f"value_median = median), oracle/pwadv_oracle.c on {threads} threads "
                       f"(X-slab engines as run_schedule), host {os.cpu_count()} cpus"}
+
+
+def measure_live_traffic(args, dims, fields, co, out, opts, stepping, ws, dev):
+    """DRAM bytes of one launch of K1 (or K4) on this rank's block, from the
+    hardware counters; None if the counters are unavailable on this box."""
+    from paper_2010_01545_b200 import device, traffic
+    if args.no_traffic:
+        return None
+    if stepping:
+        nxt = device.alloc_fields(dims, dev)
+        fn = lambda: device.step(*fields, co, 0.1, nxt, opts=opts)  # noqa: E731
+    else:
+        fn = lambda: device.advect(*fields, co, out, opts=opts)  # noqa: E731
+    try:
+        r = traffic.measure(fn, plan_bytes=BYTES_PER_POINT * dims.cells, device=dev.index)
+    except traffic.TrafficUnavailable as exc:
+        return {"error": str(exc)[:300]}
+    r["what"] = ("one launch of the dominant kernel on this rank's block; plan_bytes = "
+                 "the algorithmic 48 B/point")
+    return r
 
 
 def agree_all(ok: bool, dev) -> bool:
@@ -500,14 +520,26 @@ def run_ours(args):
         kern_ms = k0.elapsed_time(k1) / nk
     peak, peak_src = measured_peak()
     achieved = BYTES_PER_POINT * pts_rank / (kern_ms / 1e3) / 1e9
+    # DRAM traffic of one launch of the dominant kernel, read live from the
+    # hardware counters (CUPTI range profiler, libpwadv_traffic.so) after
+    # the timed region, L2 flushed first (ncu's cold-cache convention)
+    live = measure_live_traffic(args, dims, fields, co, out, opts, stepping, ws, dev)
+    # the committed ncu --set full summary for this workload, only when it was
+    # captured with the very libpwadv.so loaded here (build hash)
     key = f"{args.config}:{args.variant}:{nx}x{ny}x{nz}"
     tr = ncu_traffic(key) or {}
+    if tr and tr.get("lib_sha16") != _lib.build_id():
+        tr = {}
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": tr.get("bytes"),
-                "traffic_source": tr.get("source"),
+                "frac": round(achieved / peak, 4),
+                "traffic": live.get("dram_bytes") if live else None,
+                "traffic_source": live.get("source") if live else None,
+                "traffic_live": live,
+                "lib_sha16": _lib.build_id(),
                 "ncu": ({k: tr.get(k) for k in ("duration_us", "dram_read", "dram_write",
                                                 "dram_throughput_pct", "fp64_pipe_pct",
-                                                "issue_active_pct", "registers")} if tr else None),
+                                                "issue_active_pct", "registers", "lib_sha16",
+                                                "source")} if tr else None),
                 "peak_source": peak_src, "kernel_ms": round(kern_ms, 5),
                 "algorithmic_bytes_per_launch": BYTES_PER_POINT * pts_rank,
                 "bytes_per_point": BYTES_PER_POINT,
@@ -707,79 +739,124 @@ def run_ours(args):
 # ---------------------------------------------------------------------------
 # reference arm
 
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def _import_stock_reference():
+    """The unmodified reference package (pwadvect 0.1.0), pip-installed into
+    baseline/_ref from /root/reference/pkg; None if absent."""
+    if not (REF_DIR / "pwadvect" / "__init__.py").exists():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import pwadvect
+    if Path(pwadvect.__file__).resolve().parent != (REF_DIR / "pwadvect").resolve():
+        raise ImportError(f"pwadvect resolved to {pwadvect.__file__}, not baseline/_ref")
+    return pwadvect
+
+
 def run_reference(args):
-    """The reference arm: the reference's own CPU path as written —
-    run_schedule(fields, coeffs, ScheduleSpec("reference", engines=E))
+    """The reference arm: the stock reference's own CPU path, unmodified —
+    `run_schedule(fields, coeffs, ScheduleSpec("reference", engines=E))`
     (schedules.py:207-232: X-slab engine threads, each evaluating
-    compute_block on grid_roles views with numpy ufuncs, kernel.py:139-185) —
-    restated in oracle/ (oracle.run_schedule_numpy, the same arithmetic form
-    and speed; the reference package itself is not on the GPU box). Each step
-    is one evaluation of a bounded X-slab sample of the config, E = the
-    faster of all host threads and half of them. The C port of the same
-    algorithm (oracle/pwadv_oracle.c, 20-30x faster than the reference's
-    numpy code) is timed beside it and reported as `c_port`."""
+    compute_block on grid_roles views with numpy ufuncs, kernel.py:139-185)
+    imported from baseline/_ref, on the FULL config grid, E = the host's
+    schedulable cores, W warm-up + K timed steps as asked
+    (K capped to ~3 minutes of CPU time, reported), wall time by
+    time.perf_counter around each call as the reference itself reports it
+    (`wall`, schedules.py:220-228). Beside it: the single-thread
+    `run_reference` (kernel.py:175-185, min of 3) and the C port of the same
+    algorithm (oracle/, all threads). Inputs: the same seeded BASELINE fields
+    as our arm (built by the checker's generator, bit-identical to the device
+    K5 fill), wrapped in the reference's own FieldSet / AdvectionCoefficients.
+    Falls back to the oracle's numpy restatement only when baseline/_ref is
+    missing (reported as kind "port")."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     nx, ny, nz, desc = CONFIGS[args.config]
-    from oracle import oracle  # the reference algorithm's CPU implementation (port)
+    if args.config == "c4":
+        nx, ny = 2048, 1024  # the per-GPU block our arm steps (evaluation timed here)
+    from oracle import oracle  # input generator + C port (checker / CPU baseline only)
     import numpy as np
     threads = oracle.host_threads()
-    sx = max(1, min(nx, (2 * 1024 * 1024) // (ny * nz)))  # bounded X-slab sample (~2M points)
-    u, v, w = oracle.fill_random(sx, ny, nz, SEED, baseline=True)
+    engines = max(1, min(nx, len(os.sched_getaffinity(0))))
     co = oracle.baseline_coefficients(SEED, nz)
     cargs = (co["tcx"], co["tcy"], co["tzc1"], co["tzc2"])
-    outs = [np.zeros_like(u) for _ in range(3)]
+    u, v, w = oracle.fill_random(nx, ny, nz, SEED, baseline=True)
+    pts = nx * ny * nz
 
     def timed(fn):
         t0 = time.perf_counter()
         fn()
         return time.perf_counter() - t0
 
-    # engine count: all host threads or half of them, whichever is faster here
-    cands = sorted({max(1, min(sx, threads)), max(1, min(sx, threads // 2))}, reverse=True)
-    probe = {e: min(timed(lambda e=e: oracle.run_schedule_numpy(u, v, w, *cargs, e, outs=outs))
-                    for _ in range(2)) for e in cands}
-    engines = min(probe, key=probe.get)
-    run = lambda: oracle.run_schedule_numpy(u, v, w, *cargs, engines, outs=outs)  # noqa: E731
-    warm = max(1, min(args.warmup, 3))
-    for _ in range(warm):
+    ref = _import_stock_reference()
+    if ref is not None:
+        from pwadvect.grid import Field3D, FieldSet, make_grid
+        from pwadvect.kernel import AdvectionCoefficients, run_reference as ref_run_reference
+        from pwadvect.schedules import ScheduleSpec, run_schedule
+        dims = make_grid(nx, ny, nz)
+        fields = FieldSet(Field3D(dims, u), Field3D(dims, v), Field3D(dims, w))
+        coeffs = AdvectionCoefficients(*cargs)
+        spec = ScheduleSpec("reference", engines=engines)
+        walls = []
+
+        def run():
+            _, _, wall = run_schedule(fields, coeffs, spec)
+            walls.append(wall)
+        kind = "reference"
+        impl_desc = (f"stock pwadvect {getattr(ref, '__version__', '0.1.0')} from baseline/_ref: "
+                     f"run_schedule(fields, coeffs, ScheduleSpec('reference', engines={engines}))")
+        single_fn = lambda: ref_run_reference(fields, coeffs)  # noqa: E731
+    else:
+        outs = [np.zeros_like(u) for _ in range(3)]
+        walls = []
+
+        def run():
+            walls.append(timed(lambda: oracle.run_schedule_numpy(u, v, w, *cargs, engines, outs=outs)))
+        kind = "port"
+        impl_desc = (f"baseline/_ref missing: the reference's run_schedule('reference', "
+                     f"engines={engines}) restated with numpy (oracle.run_schedule_numpy)")
+        single_fn = lambda: oracle.run_schedule_numpy(u, v, w, *cargs, 1, outs=outs)  # noqa: E731
+
+    warm = max(1, args.warmup)
+    per = timed(run)  # first call (also the steps-cap estimate)
+    for _ in range(warm - 1):
         run()
-    # K steps as asked, each one evaluation of the bounded sample, unless that
-    # would exceed ~2 minutes of CPU time (then as many as fit, reported)
-    per = timed(run)
-    steps = max(1, min(args.steps, int(120.0 / max(per, 1e-6))))
+    steps = max(1, min(args.steps, int(180.0 / max(per, 1e-6))))
+    walls.clear()
     t0 = time.perf_counter()
     for _ in range(steps):
         run()
     dt = time.perf_counter() - t0
-    pts = sx * ny * nz
     value = pts * steps / dt / 1e9
-    # the reference's single-thread run_reference on the same sample (min of 3)
-    t1 = min(timed(lambda: oracle.run_schedule_numpy(u, v, w, *cargs, 1, outs=outs)) for _ in range(3))
-    single = {"value": round(pts / t1 / 1e9, 5), "unit": UNIT, "cores": 1,
-              "sample": "same sample, engines=1 (run_reference), min of 3"}
+    # the reference's single-thread drop-in on the same grid (min of 3)
+    t1 = min(timed(single_fn) for _ in range(3))
+    single = {"value": round(pts / t1 / 1e9, 6), "unit": UNIT, "cores": 1,
+              "sample": "full config grid, run_reference (kernel.py:175-185), min of 3"}
     # the C port of the same algorithm, for context (~5 s)
+    outs_c = [np.zeros_like(u) for _ in range(3)]
     cts = []
     t_c = time.perf_counter()
     while time.perf_counter() - t_c < 5.0 and len(cts) < 400:
-        cts.append(timed(lambda: oracle.advect_into(u, v, w, *outs, *cargs, threads)))
+        cts.append(timed(lambda: oracle.advect_into(u, v, w, *outs_c, *cargs, threads)))
     c_port = {"value": round(pts / sorted(cts)[len(cts) // 2] / 1e9, 4), "unit": UNIT, "cores": threads,
-              "sample": f"same sample, oracle/pwadv_oracle.c on {threads} threads, median of {len(cts)}"}
-    sample = (f"{sx}x{ny}x{nz} X-slab of the config grid per step ({pts} points): the reference's "
-              f"run_schedule('reference', engines={engines}) restated with numpy "
-              f"(oracle.run_schedule_numpy), host {os.cpu_count()} cpus")
-    line = {"metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": ws, "steps": steps,
+              "sample": f"full config grid, oracle/pwadv_oracle.c on {threads} threads, median of {len(cts)}"}
+    sample = (f"full {nx}x{ny}x{nz} config grid ({pts} points) per step: {impl_desc}; "
+              f"host {os.cpu_count()} cpus")
+    line = {"metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": ws, "steps": steps,
             "warmup": warm, "ms_per_step": round(dt / steps * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (same generator as our arm)", "impl": "reference",
-            "config": {"workload": desc, "nx": nx, "ny": ny, "nz": nz, "sample_nx": sx},
-            "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": engines, "kind": "port",
+            "data": "synthetic (same generator and seed as our arm)", "impl": "reference",
+            "config": {"workload": desc, "nx": nx, "ny": ny, "nz": nz, "full_grid": True},
+            "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": engines, "kind": kind,
                              "sample": sample, "host": host_info()},
-            "engines_probe_s": {str(e): round(t, 4) for e, t in probe.items()},
+            "reference_wall_s": {"min": round(min(walls), 4), "median": round(statistics.median(walls), 4),
+                                 "what": "run_schedule's own wall (perf_counter around its engines)"},
             "single_thread": single,
             "c_port": c_port,
-            "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0,
+            "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -798,10 +875,12 @@ def main(argv=None):
     ap.add_argument("--tile-j", type=int, default=0, help="X-march strip width (0 = the planner's)")
     ap.add_argument("--stages", type=int, default=0, help="X-march ring depth (0 = the planner's)")
     ap.add_argument("--e2e-steps", type=int, default=50)
-    ap.add_argument("--ramp-ms", type=float, default=150.0,
-                    help="untimed steps for about this long before the warm-up (SM clock ramp)")
+    ap.add_argument("--ramp-ms", type=float, default=0.0,
+                    help="untimed steps for about this long before the warm-up (SM clock ramp; "
+                         "default off: 150 ms of load already trips sw_power_cap on B200)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the live DRAM counter read")
     ap.add_argument("--full-c4", action="store_true", help="c4 on one GPU at the full 4096x4096x128")
     ap.add_argument("--scaling", choices=("weak", "strong"), default=None,
                     help="N>1: weak = the config grid per GPU (default), strong = the config grid "

@@ -152,6 +152,19 @@ def lib():
     return _lib
 
 
+_build_id = None
+
+
+def build_id() -> str:
+    """sha256 (first 16 hex) of the libpwadv.so this process loads: stamps
+    profiles (profiles/ncu_traffic.json) to the build they were taken with."""
+    global _build_id
+    if _build_id is None:
+        import hashlib
+        _build_id = hashlib.sha256(LIB_PATH.read_bytes()).hexdigest()[:16]
+    return _build_id
+
+
 def check(rc: int) -> None:
     if rc != PWADV_OK:
         msg = lib().pwadv_last_error().decode(errors="replace")

@@ -11,6 +11,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpwadv.so"
+TRAFFIC_LIB = PKG / "libpwadv_traffic.so"  # optional: live DRAM counters (CUPTI)
+TRAFFIC_SRC = "pwadv_traffic.cpp"
 SOURCES = ["pwadv_advect.cu", "pwadv_aux.cu", "pwadv_roles.cu", "pwadv_api.cu"]
 HEADERS = ["pwadv_device.cuh", "pwadv_internal.h"]
 
@@ -43,6 +45,47 @@ def stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
+def cuda_home() -> Path:
+    return Path(nvcc_path()).resolve().parent.parent
+
+
+def build_traffic(force: bool = False) -> Path | None:
+    """libpwadv_traffic.so (CUPTI range profiler, host code only): g++ against
+    the toolkit's cupti headers; None where the toolkit has no CUPTI."""
+    # CUPTI must be the copy the host process loads: torch imports its bundled
+    # libcupti.so.12 (nvidia-cuda-cupti wheel) first, and a second copy with
+    # the same soname would bind to it with mismatched structs. Prefer the
+    # bundled headers + library; the toolkit's otherwise.
+    cu = cuda_home()
+    inc, lib = cu / "include", cu / "lib64"
+    try:
+        import nvidia.cuda_cupti as bundled
+        b = Path(list(bundled.__path__)[0])
+        if (b / "include" / "cupti_range_profiler.h").exists() and (b / "lib" / "libcupti.so.12").exists():
+            inc, lib = b / "include", b / "lib"
+    except ImportError:
+        pass
+    if not (inc / "cupti_range_profiler.h").exists():
+        return None
+    src = CSRC / TRAFFIC_SRC
+    hdr = PKG.parent / "include" / "pwadv_traffic.h"
+    if (not force and TRAFFIC_LIB.exists()
+            and TRAFFIC_LIB.stat().st_mtime > max(src.stat().st_mtime, hdr.stat().st_mtime)):
+        return TRAFFIC_LIB
+    tmp = TRAFFIC_LIB.with_suffix(".so.tmp")
+    cupti = lib / "libcupti.so"
+    if not cupti.exists():
+        cupti = lib / "libcupti.so.12"
+    cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", f"-I{inc}",
+           f"-I{cu / 'include'}", str(src), "-o", str(tmp), str(cupti),
+           f"-L{cu / 'lib64' / 'stubs'}", f"-Wl,-rpath,{lib}", "-lcuda"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"g++ failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stderr}")
+    os.replace(tmp, TRAFFIC_LIB)
+    return TRAFFIC_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not stale():
         return LIB
@@ -60,4 +103,5 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    build_traffic(force="--force" in sys.argv)
     print(LIB)

@@ -2,31 +2,43 @@
 reference schedules.py:27-272), executed on the B200.
 
 `run_schedule(fields, coeffs, spec) -> (SourceSet, TrafficReport, wall)` keeps
-the reference's signature and errors. Variants:
+the reference's signature, defaults and errors. Variants:
 
-* "xmarch" (default) — K1, the bulk-copy plane-ring X-march kernel;
-* "simple" — K1, one thread per point (independent second implementation);
-* "xmarch_fma" / "simple_fma" — DFMA-contracted builds (not bit-exact;
-  normwise error <= 1e-12, reported by compare_outputs);
-* the reference's FPGA data-movement variants ("reference",
-  "column_buffered", "y_batched", "x_reordered", schedules.py:27) are
-  accepted for drop-in compatibility and all run as "xmarch": the reference
-  guarantees they are bitwise identical (schedules.py:1-8), and the X-march
-  is the GPU form of "x_reordered" (schedules.py:160-191).
+* the reference's four ("reference" — the default, as in
+  schedules.py:80 —, "column_buffered", "y_batched", "x_reordered",
+  schedules.py:27) all run as K1, the bulk-copy plane-ring X-march kernel:
+  the reference guarantees they are bitwise identical (schedules.py:1-8),
+  and the X-march is the GPU form of "x_reordered" (schedules.py:160-191).
+  Their TrafficReport keeps the reference's contract: the element traffic
+  of that variant's data movement, in closed form from dims and spec
+  (schedules.py:117-191; docs/model-notes.md §3), identical to what the
+  reference counts;
+* the GPU's own: "xmarch" (K1), "simple" (one thread per point, an
+  independent second implementation), "xmarch_fma" / "simple_fma" (DFMA-
+  contracted builds: not bit-exact; normwise error <= 1e-12, reported by
+  compare_outputs). Their TrafficReport counts the chosen GPU plan's element
+  traffic: HBM reads (staged plane tiles, halo columns and segment-boundary
+  planes included), HBM writes, shared-memory reads/fills, shared memory
+  per CTA.
+
+Every report also carries `device` — the GPU plan's counts — and, with
+`ScheduleSpec(measure_traffic=True)`, `measured`: the DRAM bytes the launches
+actually moved, read from the hardware counters (CUPTI range profiler,
+libpwadv_traffic.so), beside the plan's bytes and their ratio. Neither takes
+part in equality, so the reference's determinism checks hold.
 
 `engines` splits the interior into balanced X slabs exactly like
 partition_domain (schedules.py:65-75); each slab is one box launch, outputs
-are bitwise independent of the engine count. `wall` is device time measured
-with CUDA events around the launches (inputs already resident), the analogue
-of the reference's perf_counter around its compute (schedules.py:220-228).
-`TrafficReport` counts element traffic of the chosen GPU plan: HBM reads
-(staged plane tiles, halo columns and segment-boundary planes included),
-HBM writes, shared-memory reads/fills, and shared memory per CTA.
+are bitwise independent of the engine count. `wall` is perf_counter time of
+the whole call after the output allocation, as the reference measures it
+(schedules.py:218-228): the upload of u, v, w, the launches and the download
+of su, sv, sw.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import time
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -34,7 +46,29 @@ from .layout import Field3D, GridDims, SourceSet
 
 GPU_VARIANTS = ("xmarch", "simple", "xmarch_fma", "simple_fma")
 REFERENCE_VARIANTS = ("reference", "column_buffered", "y_batched", "x_reordered")
-VARIANTS = GPU_VARIANTS + REFERENCE_VARIANTS
+VARIANTS = REFERENCE_VARIANTS + GPU_VARIANTS  # the reference's four first (schedules.py:27)
+
+
+def _xshift_roles(roles) -> tuple:
+    """Scratch blocks of the X-reordered schedule: the compute roles, closed
+    under "a role with dx <= 0 has its dx+1 parent" (the plane shift feeds
+    dx from dx+1), as schedules.py:30-50 defines them: 22 for COMPUTE_ROLES."""
+    have = set(roles)
+    todo = list(have)
+    while todo:
+        f, dx, dy = todo.pop()
+        if dx <= 0 and (f, dx + 1, dy) not in have:
+            have.add((f, dx + 1, dy))
+            todo.append((f, dx + 1, dy))
+    return tuple(sorted(have))
+
+
+def _compute_roles():
+    from .stencil import COMPUTE_ROLES
+    return COMPUTE_ROLES
+
+
+XSHIFT_ROLES = _xshift_roles(_compute_roles())
 
 
 @dataclass(frozen=True)
@@ -64,9 +98,10 @@ def partition_domain(dims, engines: int) -> list[Slab]:
 
 @dataclass(frozen=True)
 class ScheduleSpec:
-    variant: str = "xmarch"
+    variant: str = "reference"
     y_batch: int = 64
     engines: int = 1
+    measure_traffic: bool = False  # GPU extension: DRAM bytes from the hardware counters
 
     def __post_init__(self):
         if self.variant not in VARIANTS:
@@ -89,13 +124,17 @@ class ScheduleSpec:
 
 @dataclass
 class TrafficReport:
-    """Element traffic of one run (units: float64 elements; scratch in bytes)."""
+    """Element traffic of one run (units: float64 elements; scratch in bytes).
+    `device` (GPU plan counts) and `measured` (DRAM bytes from the counters)
+    are extensions that do not take part in equality."""
 
     external_reads: int = 0
     external_writes: int = 0
     local_reads: int = 0
     local_writes: int = 0
     scratch_bytes_peak: int = 0
+    device: "TrafficReport | None" = field(default=None, compare=False, repr=False)
+    measured: "dict | None" = field(default=None, compare=False)
 
     def merge(self, other: "TrafficReport") -> None:
         self.external_reads += other.external_reads
@@ -103,6 +142,43 @@ class TrafficReport:
         self.local_reads += other.local_reads
         self.local_writes += other.local_writes
         self.scratch_bytes_peak = max(self.scratch_bytes_peak, other.scratch_bytes_peak)
+
+
+def reference_traffic(dims, spec: "ScheduleSpec", slabs) -> TrafficReport:
+    """The element traffic the reference counts for its variant `spec.variant`
+    over `slabs` (schedules.py:117-191), in closed form — it depends only on
+    dims and spec (docs/model-notes.md §3): per output column 54 operand
+    touches per mid level and 45 at the top; column_buffered / y_batched
+    copy the 17 role columns of every output column into scratch;
+    x_reordered prefetches all XSHIFT_ROLES blocks once per slab and Y batch,
+    then per X step shifts the dx <= 0 blocks down and fetches the dx = +1
+    ones."""
+    from .stencil import COMPUTE_ROLES, reads_per_point
+    nx, ny, nz = dims.nx, dims.ny, dims.nz
+    col = reads_per_point(False) * (nz - 2) + reads_per_point(True)
+    nrole = len(COMPUTE_ROLES)
+    tr = TrafficReport(external_writes=3 * nx * ny * (nz - 1))
+    v = spec.variant
+    if v == "reference":
+        tr.external_reads = nx * ny * col
+    elif v in ("column_buffered", "y_batched"):
+        batch = 1 if v == "column_buffered" else spec.y_batch
+        tr.external_reads = nrole * nx * ny * nz
+        tr.local_writes = tr.external_reads
+        tr.local_reads = nx * ny * col
+        tr.scratch_bytes_peak = nrole * min(batch, ny) * nz * 8
+    else:  # x_reordered
+        nshift = sum(1 for r in XSHIFT_ROLES if r[1] <= 0)
+        nfetch = len(XSHIFT_ROLES) - nshift
+        for s in slabs:
+            steps = s.width - 1
+            fetched = ny * nz * (len(XSHIFT_ROLES) + nfetch * steps)
+            shifted = nshift * steps * ny * nz
+            tr.external_reads += fetched
+            tr.local_writes += fetched + shifted
+            tr.local_reads += shifted + s.width * ny * col
+        tr.scratch_bytes_peak = len(XSHIFT_ROLES) * min(spec.y_batch, ny) * nz * 8
+    return tr
 
 
 def plan_traffic(dims: GridDims, box, plan: dict) -> TrafficReport:
@@ -145,7 +221,8 @@ def plan_traffic(dims: GridDims, box, plan: dict) -> TrafficReport:
 
 
 def run_schedule(fields, coeffs, spec: ScheduleSpec):
-    """Execute one schedule on the GPU; returns (sources, traffic, wall seconds)."""
+    """Execute one schedule on the GPU; returns (sources, traffic, wall seconds)
+    (reference schedules.py:207-232)."""
     import torch
     from . import device
 
@@ -155,25 +232,41 @@ def run_schedule(fields, coeffs, spec: ScheduleSpec):
     spec.validate(dims)
     slabs = partition_domain(dims, spec.engines)
     gd = GridDims(dims.nx, dims.ny, dims.nz)
-    dev = torch.device("cuda")
-    u, v, w = (torch.from_numpy(np.ascontiguousarray(f.data, dtype=np.float64)).to(dev)
-               for f in (fields.u, fields.v, fields.w))
-    dc = device.DeviceCoefficients.from_host(coeffs, dev)
-    out = device.alloc_fields(gd, dev)
+    dev = torch.device("cuda", torch.cuda.current_device())
     opts = device.make_opts(spec.kernel_variant)
-    traffic = TrafficReport()
-    for s in slabs:
-        box = (s.x_begin, s.x_end, 1, gd.ny + 1)
-        traffic.merge(plan_traffic(gd, box, device.describe_plan(gd, box, opts, dev.index or 0)))
-    torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record()
-    for s in slabs:
-        device.advect(u, v, w, dc, out, box=(s.x_begin, s.x_end, 1, gd.ny + 1), opts=opts)
-    t1.record()
-    t1.synchronize()
-    wall = t0.elapsed_time(t1) / 1e3
-    res = SourceSet(*(Field3D(gd, t.cpu().numpy()) for t in out))
+    boxes = [(s.x_begin, s.x_end, 1, gd.ny + 1) for s in slabs]
+    plan = TrafficReport()
+    for box in boxes:
+        plan.merge(plan_traffic(gd, box, device.describe_plan(gd, box, opts, dev.index)))
+    if spec.variant in REFERENCE_VARIANTS:
+        traffic = reference_traffic(gd, spec, slabs)
+    else:
+        traffic = TrafficReport(plan.external_reads, plan.external_writes, plan.local_reads,
+                                plan.local_writes, plan.scratch_bytes_peak)
+    traffic.device = plan
+    hosts = [np.ascontiguousarray(f.data, dtype=np.float64) for f in (fields.u, fields.v, fields.w)]
+    res = SourceSet(*(Field3D(gd, np.zeros(gd.padded_shape)) for _ in range(3)))
+    dc = device.DeviceCoefficients.from_host(coeffs, dev)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    u, v, w = (torch.from_numpy(h).to(dev) for h in hosts)
+    out = device.alloc_fields(gd, dev)
+    for box in boxes:
+        device.advect(u, v, w, dc, out, box=box, opts=opts)
+    for r, o in zip((res.su, res.sv, res.sw), out):
+        r.data[...] = o.cpu().numpy()
+    wall = time.perf_counter() - t0
+    if spec.measure_traffic:  # one more pass of the same launches under the counters
+        from . import traffic as tmod
+
+        def launches():
+            for box in boxes:
+                device.advect(u, v, w, dc, out, box=box, opts=opts)
+        try:
+            traffic.measured = tmod.measure(launches, device=dev.index,
+                                            plan_bytes=8 * (plan.external_reads + plan.external_writes))
+        except tmod.TrafficUnavailable as exc:
+            traffic.measured = {"error": str(exc)}
     return res, traffic, wall
 
 

@@ -269,3 +269,63 @@ def test_cli_parser_and_schedule_names():
     with pytest.raises(SystemExit):
         p.parse_args(["bench", "--grid", "8x6x4", "--schedule", "nonsense"])
     assert cli.BENCH_COLUMNS[:3] == ("schedule", "engines", "y_batch")
+
+
+# --- the reference's traffic counters (schedules.py:117-191) in closed form ---
+
+def _stock_schedules():
+    ref = Path(__file__).resolve().parent.parent / "baseline" / "_ref"
+    if not (ref / "pwadvect" / "schedules.py").exists():
+        pytest.skip("stock reference not installed in baseline/_ref")
+    import importlib.util
+    import sys as _sys
+    # import the stock package under its own name in a private module table
+    saved = {k: v for k, v in _sys.modules.items() if k == "pwadvect" or k.startswith("pwadvect.")}
+    for k in saved:
+        del _sys.modules[k]
+    _sys.path.insert(0, str(ref))
+    try:
+        import pwadvect.grid as g
+        import pwadvect.kernel as k
+        import pwadvect.schedules as s
+        assert Path(s.__file__).resolve().parent == (ref / "pwadvect").resolve()
+        return g, k, s
+    finally:
+        _sys.path.remove(str(ref))
+        for key in [k for k in _sys.modules if k == "pwadvect" or k.startswith("pwadvect.")]:
+            del _sys.modules[key]
+        _sys.modules.update(saved)
+        del importlib
+
+
+def test_reference_traffic_matches_stock_counters():
+    """reference_traffic() equals what the stock reference counts while it
+    moves the data, for every variant, random dims, y_batch and engines."""
+    from paper_2010_01545_b200.engines import ScheduleSpec, partition_domain, reference_traffic
+    g, k, s = _stock_schedules()
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        nx, ny, nz = int(rng.integers(1, 9)), int(rng.integers(1, 8)), int(rng.integers(2, 7))
+        dims = g.make_grid(nx, ny, nz)
+        fields = g.fill_fields(dims, g.GeneratorSpec.random(int(rng.integers(0, 99))))
+        co = k.default_coefficients(nz)
+        yb = int(rng.integers(1, ny + 1))
+        eng = int(rng.integers(1, nx + 1))
+        for variant in s.VARIANTS:
+            _, want, _ = s.run_schedule(fields, co, s.ScheduleSpec(variant, yb, eng))
+            spec = ScheduleSpec(variant, yb, eng)
+            got = reference_traffic(pw.make_grid(nx, ny, nz), spec,
+                                    partition_domain(pw.make_grid(nx, ny, nz), eng))
+            assert (got.external_reads, got.external_writes, got.local_reads, got.local_writes,
+                    got.scratch_bytes_peak) == (want.external_reads, want.external_writes,
+                                                want.local_reads, want.local_writes,
+                                                want.scratch_bytes_peak), (variant, nx, ny, nz, yb, eng)
+
+
+def test_schedule_spec_and_variants_mirror_reference():
+    from paper_2010_01545_b200.engines import REFERENCE_VARIANTS, VARIANTS, XSHIFT_ROLES, ScheduleSpec
+    assert ScheduleSpec().variant == "reference"
+    assert VARIANTS[:4] == REFERENCE_VARIANTS == ("reference", "column_buffered", "y_batched",
+                                                  "x_reordered")
+    assert len(XSHIFT_ROLES) == 22
+    assert sum(1 for r in XSHIFT_ROLES if r[1] <= 0) == 13  # shifted blocks per X step

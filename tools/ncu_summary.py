@@ -1,6 +1,6 @@
 """Summarise ncu --set full captures of K1/K4 into profiles/ (raw CSV + ncu_traffic.json entry).
 
-    python tools/ncu_summary.py KEY REPORT.ncu-rep [KEY REPORT ...]
+    python tools/ncu_summary.py [--round=r02] KEY REPORT.ncu-rep|RAW.csv [KEY REPORT ...]
 """
 import csv
 import io
@@ -22,8 +22,13 @@ METRICS = {
 }
 
 
-def summarise(key, rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def summarise(key, rep, rnd="r02"):
+    """rep: an .ncu-rep, or the raw CSV of one (`ncu -i X --page raw --csv`)."""
+    if rep.endswith(".csv"):
+        raw = Path(rep).read_text()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     out = {"kernel": vals[hdr.index("Kernel Name")][:80]}
@@ -32,8 +37,14 @@ def summarise(key, rep):
         out[name] = round(float(vals[i].replace(",", "")) * scale.get(units[i], 1), 4)
     out["bytes"] = int(out["dram_read"] + out["dram_write"])
     tag = key.replace(":", "_")
-    out["source"] = f"profiles/r01_ncu_full_{tag}_raw.csv (ncu --set full, 1 launch, cold)"
-    (ROOT / "profiles" / f"r01_ncu_full_{tag}_raw.csv").write_text(raw)
+    dst = ROOT / "profiles" / f"{rnd}_ncu_full_{tag}_raw.csv"
+    out["source"] = f"profiles/{dst.name} (ncu --set full, 1 launch, cold)"
+    # the libpwadv.so the capture ran (shipped from this tree): bench.py uses
+    # the entry only while the loaded library has the same hash
+    sys.path.insert(0, str(ROOT))
+    from paper_2010_01545_b200 import _lib
+    out["lib_sha16"] = _lib.build_id()
+    dst.write_text(raw)
     return out
 
 
@@ -41,7 +52,10 @@ if __name__ == "__main__":
     p = ROOT / "profiles" / "ncu_traffic.json"
     table = json.loads(p.read_text()) if p.exists() else {}
     args = sys.argv[1:]
+    rnd = "r02"
+    if args and args[0].startswith("--round="):
+        rnd = args.pop(0).split("=", 1)[1]
     for key, rep in zip(args[::2], args[1::2]):
-        table[key] = summarise(key, rep)
+        table[key] = summarise(key, rep, rnd)
         print(key, table[key])
     p.write_text(json.dumps(table, indent=1) + "\n")
