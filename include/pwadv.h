@@ -168,7 +168,10 @@ int pwadv_step_box_f64(const double *u, const double *v, const double *w,
  * the global fields — no separate exchange. Peer buffers are device memory
  * this GPU can store to: the same device, or another GPU's allocation opened
  * with pwadv_ipc_open (CUDA IPC, NVLink P2P). A neighbour that is this block
- * itself (an undivided axis) is given as its own buffers.
+ * itself (an undivided axis) is given as its own buffers. Peer buffers must be
+ * 8-byte aligned (PWADV_E_ALIGN otherwise); when any of them is not 16-byte
+ * aligned the kernel takes its unaligned-run form, whose boundary stores are
+ * 8 bytes wide. The pull entry points (below) need 16-byte-aligned peers.
  */
 enum {
     PWADV_NB_XM = 0, PWADV_NB_XP = 1, PWADV_NB_YM = 2, PWADV_NB_YP = 3,

@@ -1327,8 +1327,14 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     // paired loads/stores; otherwise UA (unaligned runs: the copies start up to
     // one element early, scalar shared loads and stores, also into the peers'
     // halos) — warp-specialised only, u, v, w with the same 16-byte phase
-    const uintptr_t al = (uintptr_t)L.u | (uintptr_t)L.v | (uintptr_t)L.w | (uintptr_t)L.o0 |
-                         (uintptr_t)L.o1 | (uintptr_t)L.o2;
+    uintptr_t al = (uintptr_t)L.u | (uintptr_t)L.v | (uintptr_t)L.w | (uintptr_t)L.o0 |
+                   (uintptr_t)L.o1 | (uintptr_t)L.o2;
+    // fused push: the aligned form stores boundary pairs into the peers'
+    // halos with 16-byte stores too — 8-byte-aligned peers take the UA form
+    // (scalar stores); pwadv_step_push_f64 requires 8-byte-aligned peers
+    if (L.peers && !L.pull)
+        for (int d = 0; d < 8; ++d)
+            al |= (uintptr_t)L.peers->u[d] | (uintptr_t)L.peers->v[d] | (uintptr_t)L.peers->w[d];
     const bool ua = (nz % 2 != 0) || (al & 15) || (L.flags & PWADV_FLAG_UNALIGNED);
     const uintptr_t inpar = ((uintptr_t)L.u ^ (uintptr_t)L.v) | ((uintptr_t)L.u ^ (uintptr_t)L.w);
     if (ua && ((al & 7) || (inpar & 8) || (L.max_threads > 0 && L.max_threads != 512) ||

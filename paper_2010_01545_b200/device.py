@@ -334,6 +334,10 @@ def load_field(path, device=None) -> torch.Tensor:
     return host.to(device or "cuda")
 
 
+class ContextClosed(RuntimeError):
+    """A HostContext was closed (e.g. evicted) before or while it was fetched."""
+
+
 class HostContext:
     """pwadv_ctx: device buffers + 3 streams for host-buffer (end-to-end) calls."""
 
@@ -350,9 +354,20 @@ class HostContext:
         self._h = h
 
     def close(self) -> None:
-        if getattr(self, "_h", None) is not None and self._h.value:
-            _lib.lib().pwadv_ctx_destroy(self._h)
+        """Free the context. Waits for a call in progress on another thread
+        (it holds self.lock); later calls raise ContextClosed."""
+        lock = getattr(self, "lock", None)
+        if lock is None:
+            return
+        with lock:
+            if getattr(self, "_h", None) is not None and self._h.value:
+                _lib.lib().pwadv_ctx_destroy(self._h)
             self._h = None
+
+    def _handle(self) -> ctypes.c_void_p:
+        if self._h is None:  # caller holds self.lock
+            raise ContextClosed("pwadv_ctx was closed (evicted from the drop-in's cache)")
+        return self._h
 
     def __del__(self):  # pragma: no cover - best effort
         try:
@@ -384,11 +399,11 @@ class HostContext:
             raise ValueError(f"coefficient length {tz1.shape} != nz {d.nz}")
         with self.lock:
             _lib.check(_lib.lib().pwadv_ctx_advect_host(
-                self._h, self._hp(u), self._hp(v), self._hp(w), self._hp(su), self._hp(sv),
+                self._handle(), self._hp(u), self._hp(v), self._hp(w), self._hp(su), self._hp(sv),
                 self._hp(sw), float(tcx), float(tcy), ctypes.c_void_p(tz1.ctypes.data),
                 ctypes.c_void_p(tz2.ctypes.data), int(chunks), _lib.opts_ptr(opts)))
             a, b = ctypes.c_uint64(), ctypes.c_uint64()
-            _lib.check(_lib.lib().pwadv_ctx_last_bytes(self._h, ctypes.byref(a), ctypes.byref(b)))
+            _lib.check(_lib.lib().pwadv_ctx_last_bytes(self._handle(), ctypes.byref(a), ctypes.byref(b)))
         return int(a.value), int(b.value)
 
     def submit_host(self, u, v, w, su, sv, sw, tcx, tcy, tzc1, tzc2, chunks: int = 0,
@@ -404,13 +419,13 @@ class HostContext:
         with self.lock:
             self._keep = (tz1, tz2)  # the coefficient upload is asynchronous
             _lib.check(_lib.lib().pwadv_ctx_submit_host(
-                self._h, self._hp(u), self._hp(v), self._hp(w), self._hp(su), self._hp(sv),
+                self._handle(), self._hp(u), self._hp(v), self._hp(w), self._hp(su), self._hp(sv),
                 self._hp(sw), float(tcx), float(tcy), ctypes.c_void_p(tz1.ctypes.data),
                 ctypes.c_void_p(tz2.ctypes.data), int(chunks), _lib.opts_ptr(opts)))
             a, b = ctypes.c_uint64(), ctypes.c_uint64()
-            _lib.check(_lib.lib().pwadv_ctx_last_bytes(self._h, ctypes.byref(a), ctypes.byref(b)))
+            _lib.check(_lib.lib().pwadv_ctx_last_bytes(self._handle(), ctypes.byref(a), ctypes.byref(b)))
         return int(a.value), int(b.value)
 
     def sync(self) -> None:
         with self.lock:
-            _lib.check(_lib.lib().pwadv_ctx_sync(self._h))
+            _lib.check(_lib.lib().pwadv_ctx_sync(self._handle()))

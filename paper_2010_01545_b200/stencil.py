@@ -244,29 +244,35 @@ _CTX_MAX = 4
 
 
 def _context(dims: GridDims):
+    """The cached HostContext for this shape on the current device (created on
+    first use). At most _CTX_MAX shapes are kept, and their device buffers (6
+    padded fields each) within a quarter of the device memory; evicted
+    contexts are closed outside the cache lock — close() waits for a call in
+    progress on another thread, and that caller's next call re-fetches
+    (ContextClosed)."""
     import torch
     from .device import HostContext
     if not torch.cuda.is_available():
         raise RuntimeError("run_reference needs a CUDA device: the B200 path has no CPU fallback")
     dev = torch.cuda.current_device()
     key = (dev, dims.nx, dims.ny, dims.nz)
+    evicted = []
     with _CTX_LOCK:
         ctx = _CTX_CACHE.get(key)
         if ctx is None:
             ctx = HostContext(GridDims(dims.nx, dims.ny, dims.nz), dev)
             _CTX_CACHE[key] = ctx
-            # at most _CTX_MAX shapes, and their device buffers (6 padded
-            # fields each) within a quarter of the device memory
             budget = torch.cuda.get_device_properties(dev).total_memory // 4
 
             def held():
                 return sum(6 * 8 * (k[1] + 2) * (k[2] + 2) * k[3] for k in _CTX_CACHE)
             while len(_CTX_CACHE) > 1 and (len(_CTX_CACHE) > _CTX_MAX or held() > budget):
-                _, old = _CTX_CACHE.popitem(last=False)
-                old.close()
+                evicted.append(_CTX_CACHE.popitem(last=False)[1])
         else:
             _CTX_CACHE.move_to_end(key)
-        return ctx
+    for old in evicted:
+        old.close()
+    return ctx
 
 
 def _host_array(f, dims):
@@ -276,22 +282,31 @@ def _host_array(f, dims):
     return a
 
 
+# Outputs up to this size come from torch's caching page-locked allocator
+# (released results are reused; the D2H lands in them directly). Larger ones
+# are plain numpy memory, filled through the context's staging buffers: the
+# caching allocator rounds every block up to a power of two and never returns
+# it to the OS (three C3 outputs would pin ~3 x 4 GiB for the process's life).
+_PINNED_OUTPUT_MAX = 512 << 20
+
+
 def _output_array(shape) -> np.ndarray:
-    """A new float64 output array in page-locked memory (torch's caching host
-    allocator: blocks of released results are reused, and the D2H copies
-    land in it directly instead of through staging and first-touch page
-    faults); plain numpy memory if pinning is unavailable."""
+    """A new float64 output array (page-locked below _PINNED_OUTPUT_MAX)."""
     import torch
-    try:
-        return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
-    except RuntimeError:
-        return np.empty(shape)
+    nbytes = 8 * int(np.prod(shape, dtype=np.int64))
+    if nbytes <= _PINNED_OUTPUT_MAX:
+        try:
+            return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+        except RuntimeError:
+            pass
+    return np.empty(shape)
 
 
 def run_reference(fields, coeffs) -> SourceSet:
     """Whole-grid PW advection; pure function of its inputs (reference kernel.py:175-185).
     Like the reference (zeros_sources, grid.py:129-130) the callee allocates the
-    outputs; here they are page-locked numpy arrays."""
+    outputs: numpy arrays, page-locked up to _PINNED_OUTPUT_MAX bytes each. Safe
+    to call from several threads (each shape's context serialises its calls)."""
     dims = fields.dims
     nz_c = len(coeffs.tzc1)
     if nz_c != dims.nz:
@@ -299,7 +314,15 @@ def run_reference(fields, coeffs) -> SourceSet:
     gd = GridDims(dims.nx, dims.ny, dims.nz)
     u, v, w = (_host_array(f, dims) for f in (fields.u, fields.v, fields.w))
     outs = [_output_array(gd.padded_shape) for _ in range(3)]
-    _context(gd).advect_host(u, v, w, *outs, coeffs.tcx, coeffs.tcy, coeffs.tzc1, coeffs.tzc2)
+    from .device import ContextClosed
+    for attempt in range(3):
+        try:
+            _context(gd).advect_host(u, v, w, *outs, coeffs.tcx, coeffs.tcy, coeffs.tzc1,
+                                     coeffs.tzc2)
+            break
+        except ContextClosed:  # evicted by another thread between fetch and call
+            if attempt == 2:
+                raise
     return SourceSet(*(Field3D(gd, o) for o in outs))
 
 

@@ -134,6 +134,54 @@ def test_emulated_fused_push_stepping(px, py, shape):
             assert torch.equal(f.view(torch.int64), dec.local_view(w).contiguous().view(torch.int64)), dec.rank
 
 
+def _misaligned_fields(dims):
+    """Zeroed padded fields that are 8- but not 16-byte aligned."""
+    n = dims.padded_len
+    out = []
+    for _ in range(3):
+        base = torch.zeros(n + 1, dtype=torch.float64, device="cuda")
+        out.append(base[1:].view(dims.padded_shape))
+    assert all(t.data_ptr() % 16 == 8 for t in out)
+    return tuple(out)
+
+
+@pytest.mark.parametrize("px,py", [(1, 2), (2, 1), (2, 2)])
+def test_emulated_fused_push_8byte_aligned_peers(px, py):
+    """Blocks whose NEW buffers are only 8-byte aligned, next to blocks with
+    16-byte-aligned buffers: the aligned blocks' boundary stores into those
+    peers must take the 8-byte form (no misaligned 16-byte store), bitwise
+    equal to single-domain stepping."""
+    from paper_2010_01545_b200.decomp import LocalPeerRegistry, PushStepper, ThreadStreamBarrier
+    gd = pw.make_grid(30, 26, 16)
+    spec = pw.GeneratorSpec.baseline(5)
+    co = pw.baseline_coefficients(5, gd.nz)
+    single = Stepper(device.fill(gd, spec), co, 0.1)
+    single.step(3)
+    want = single.fields
+    torch.cuda.synchronize()
+    n = px * py
+    hub = ThreadHubTransport(n)
+    reg = LocalPeerRegistry()
+    bar = ThreadStreamBarrier(n)
+
+    def rank(r):
+        dec = Decomposition(gd, px, py, r)
+        fs = dec.fill_local(spec)
+        ex = HaloExchanger(dec, device="cuda", transport=hub.bind(r))
+        st = PushStepper(dec, fs, co, 0.1, reg, bar.bind(r), initial_exchange=ex.exchange)
+        if r % 2 == 1:  # odd ranks: 8-byte-aligned new buffers
+            st.sets = (st.sets[0], _misaligned_fields(dec.local_dims))
+            reg.publish(r, st.sets)
+        st.step(3)
+        torch.cuda.current_stream().synchronize()
+        return dec, st.fields
+
+    for dec, final in run_ranks(n, rank):
+        for f, w in zip(final, want):
+            assert torch.equal(f.contiguous().view(torch.int64),
+                               dec.local_view(w).contiguous().view(torch.int64)), dec.rank
+
+
 @pytest.mark.parametrize("axis", [0, 1])
 def test_cuda_face_ops_match_tensor_slicing(axis):
     """pwadv_pack/unpack_faces3_f64 (both faces of an axis in one launch) ==

@@ -259,18 +259,6 @@ def test_plan_traffic_accounting():
     assert t3.external_reads == 3 * 64 * want
 
 
-def test_cli_parser_and_schedule_names():
-    from paper_2010_01545_b200 import cli
-    p = cli.build_parser()
-    a = p.parse_args(["bench", "--grid", "8x6x4", "--schedule", "x-reordered", "--schedule", "simple_fma"])
-    assert a.grid.cells == 192 and a.schedule == ["x_reordered", "simple_fma"]
-    with pytest.raises(SystemExit):
-        p.parse_args(["bench", "--grid", "8x6"])
-    with pytest.raises(SystemExit):
-        p.parse_args(["bench", "--grid", "8x6x4", "--schedule", "nonsense"])
-    assert cli.BENCH_COLUMNS[:3] == ("schedule", "engines", "y_batch")
-
-
 # --- the reference's traffic counters (schedules.py:117-191) in closed form ---
 
 def _stock_schedules():
@@ -323,9 +311,13 @@ def test_reference_traffic_matches_stock_counters():
 
 
 def test_schedule_spec_and_variants_mirror_reference():
-    from paper_2010_01545_b200.engines import REFERENCE_VARIANTS, VARIANTS, XSHIFT_ROLES, ScheduleSpec
+    from paper_2010_01545_b200.engines import (ALL_VARIANTS, REFERENCE_VARIANTS, VARIANTS,
+                                               XSHIFT_ROLES, ScheduleSpec)
     assert ScheduleSpec().variant == "reference"
-    assert VARIANTS[:4] == REFERENCE_VARIANTS == ("reference", "column_buffered", "y_batched",
-                                                  "x_reordered")
+    assert VARIANTS == REFERENCE_VARIANTS == ("reference", "column_buffered", "y_batched",
+                                              "x_reordered")
+    assert set(ALL_VARIANTS) >= set(VARIANTS) | {"xmarch", "xmarch_fma"}
+    with pytest.raises(ValueError):
+        ScheduleSpec("nonsense")
     assert len(XSHIFT_ROLES) == 22
     assert sum(1 for r in XSHIFT_ROLES if r[1] <= 0) == 13  # shifted blocks per X step
