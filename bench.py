@@ -250,6 +250,39 @@ def measure_live_traffic(args, dims, fields, co, out, opts, stepping, ws, dev):
     return r
 
 
+def step_barrier(dec, dev, stream):
+    """The per-step ordering of the fused multi-GPU paths: the neighbour flag
+    handshake (decomp.FlagHandshake, stream-ordered flag writes/waits over
+    NVLink) when a probe round completes on every rank within 5 s, else the
+    round-1 global NCCL all-reduce barrier. A failed probe's pending wait is
+    released locally before falling back, so nothing is left blocked."""
+    import torch
+    from paper_2010_01545_b200 import _lib, decomp
+    hs, ok, err = None, False, None
+    try:
+        hs = decomp.FlagHandshake(dec, decomp.IpcPeerRegistry(dec), dev)
+        probe = torch.cuda.Stream(dev)
+        hs(probe)
+        ev = torch.cuda.Event()
+        ev.record(probe)
+        t0 = time.perf_counter()
+        while not ev.query() and time.perf_counter() - t0 < 5.0:
+            time.sleep(1e-3)
+        ok = ev.query()
+        if not ok:
+            err = "probe handshake did not complete within 5 s"
+    except _lib.PwadvError as exc:
+        err = str(exc)
+    if agree_all(ok, dev):
+        return hs, "neighbour flag handshake (stream memory ops, NVLink)"
+    if hs is not None:
+        hs.release()
+        torch.cuda.synchronize(dev)
+    print(f"bench: flag handshake unavailable ({err or 'on another rank'}); NCCL barrier",
+          file=sys.stderr)
+    return decomp.NcclBarrier(dev), "NCCL all-reduce barrier"
+
+
 def agree_all(ok: bool, dev) -> bool:
     """True on every rank iff `ok` on every rank (all ranks choose one path)."""
     import torch
@@ -335,6 +368,7 @@ def run_ours(args):
     else:
         from paper_2010_01545_b200 import decomp
         exch = decomp.HaloExchanger(dec, dev)
+        barrier, barrier_kind = step_barrier(dec, dev, stream)
         if stepping:
             # K4 with the exchange fused in: boundary values stored into the
             # neighbours' halos over NVLink (CUDA IPC), one NCCL barrier per step.
@@ -345,7 +379,7 @@ def run_ours(args):
             err = None
             try:
                 st = decomp.PushStepper(dec, fields, co, 0.1, decomp.IpcPeerRegistry(dec),
-                                        decomp.NcclBarrier(dev), opts=opts,
+                                        barrier, opts=opts,
                                         initial_exchange=lambda f: exch.exchange(f, stream=stream))
                 st.step(1, stream=stream)
                 ref_out = device.alloc_fields(dims, dev)
@@ -363,7 +397,7 @@ def run_ours(args):
             except _lib.PwadvError as exc:
                 err = str(exc)
             if agree_all(err is None, dev):
-                step_path = "K4 + peer stores (CUDA IPC) + NCCL barrier"
+                step_path = f"K4 + peer stores (CUDA IPC) + {barrier_kind}"
 
                 def one_step(events=None):
                     st.step(1, stream=stream, events=events)
@@ -389,7 +423,7 @@ def run_ours(args):
             err = None
             try:
                 ev = decomp.PullEvaluator(dec, fields, co, decomp.IpcPeerRegistry(dec),
-                                          decomp.NcclBarrier(dev), opts=opts)
+                                          barrier, opts=opts)
                 ev.evaluate(out, stream=stream)
                 ref_out = device.alloc_fields(dims, dev)
                 exch.advect_overlapped(fields, co, ref_out, opts=opts, stream=stream)
@@ -407,7 +441,7 @@ def run_ours(args):
             except _lib.PwadvError as exc:
                 err = str(exc)
             if agree_all(err is None, dev):
-                step_path = "K1 with halo pull (peer loads over NVLink, CUDA IPC) + NCCL barrier"
+                step_path = f"K1 with halo pull (peer loads over NVLink, CUDA IPC) + {barrier_kind}"
 
                 def one_step(events=None):
                     ev.evaluate(out, stream=stream, events=events)

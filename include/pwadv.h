@@ -229,6 +229,36 @@ int pwadv_ipc_open(const unsigned char handle[64], uint64_t offset, void **dev_p
 int pwadv_ipc_close(void *dev_ptr, uint64_t offset);
 
 /*
+ * Neighbour handshake for the fused multi-GPU steps (pwadv_sync.cu): before
+ * step k+1 every neighbour must have finished step k (its stores into my
+ * halos landed; it is done reading what I overwrite). Replaces a global
+ * barrier per step with stream-ordered flag writes and waits carried by the
+ * GPU front end (no kernel, no host round trip). Each rank owns a zeroed
+ * device array of one uint64 slot per rank, mapped into its neighbours with
+ * pwadv_ipc_open.
+ *   pwadv_signal_peers: after the preceding work on `stream` (fenced), write
+ *     `value` to each of slots[0..n) — my slot in each neighbour's array.
+ *   pwadv_wait_peers: later work on `stream` waits until each of slots[0..n)
+ *     — the neighbours' slots in my own array — holds >= value.
+ * pwadv_handshake_caps reports 64-bit stream memory-op and remote-write
+ * flush support (both are required / used when present). n <= 64.
+ */
+int pwadv_handshake_caps(int device, int *mem64, int *flush);
+int pwadv_signal_peers(uint64_t *const *slots, int n, uint64_t value, void *stream);
+int pwadv_wait_peers(uint64_t *const *slots, int n, uint64_t value, void *stream);
+/* signal then wait, one batch of stream memory operations */
+int pwadv_handshake(uint64_t *const *signal_slots, int nsignal, uint64_t *const *wait_slots,
+                    int nwait, uint64_t value, void *stream);
+/* the same handshake as one 32-thread kernel chained to the step kernels by
+ * programmatic dependent launch (the per-step call of decomp.FlagHandshake):
+ * release stores of `value` to the signal slots, acquire polls of the wait
+ * slots; a poll that exceeds timeout_ns (0 = 10 s) sets *err (device int) to 1
+ * and gives up, so a lost signal never hangs the stream. <= 32 slots each. */
+int pwadv_handshake_kernel(uint64_t *const *signal_slots, int nsignal,
+                           uint64_t *const *wait_slots, int nwait, uint64_t value, int *err,
+                           uint64_t timeout_ns, void *stream);
+
+/*
  * K6 — the reference's array-level entry points (device pointers):
  * compute_block (kernel.py:139-162): roles[17] are the COMPUTE_ROLES arrays
  * (kernel.py:134-136, sorted (field, dx, dy) order: u(-1,0) u(-1,1) u(0,-1)

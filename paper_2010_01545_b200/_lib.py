@@ -94,6 +94,14 @@ SIGNATURES = {
     "pwadv_ipc_export": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_uint64)]),
     "pwadv_ipc_open": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.POINTER(_P)]),
     "pwadv_ipc_close": (ctypes.c_int, [_P, ctypes.c_uint64]),
+    "pwadv_handshake_caps": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                            ctypes.POINTER(ctypes.c_int)]),
+    "pwadv_signal_peers": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_uint64, _P]),
+    "pwadv_wait_peers": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_uint64, _P]),
+    "pwadv_handshake": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.POINTER(_P),
+                                       ctypes.c_int, ctypes.c_uint64, _P]),
+    "pwadv_handshake_kernel": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.POINTER(_P),
+                                              ctypes.c_int, ctypes.c_uint64, _P, ctypes.c_uint64, _P]),
     "pwadv_compute_block_f64": (ctypes.c_int, [_P] * 4 + [_I64, _I64, _D, _D, _P, _P,
                                                            ctypes.c_uint32, _P]),
     "pwadv_formula_f64": (ctypes.c_int, [ctypes.c_int32, _P, _P, _I64, ctypes.c_int32, _P,

@@ -13,7 +13,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libpwadv.so"
 TRAFFIC_LIB = PKG / "libpwadv_traffic.so"  # optional: live DRAM counters (CUPTI)
 TRAFFIC_SRC = "pwadv_traffic.cpp"
-SOURCES = ["pwadv_advect.cu", "pwadv_aux.cu", "pwadv_roles.cu", "pwadv_api.cu"]
+SOURCES = ["pwadv_advect.cu", "pwadv_aux.cu", "pwadv_roles.cu", "pwadv_api.cu", "pwadv_sync.cu"]
 HEADERS = ["pwadv_device.cuh", "pwadv_internal.h"]
 
 

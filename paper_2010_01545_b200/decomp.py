@@ -605,6 +605,91 @@ class NcclBarrier:
             dist.all_reduce(self.flag, group=self.group)
 
 
+class FlagHandshake:
+    """Neighbour-only, stream-ordered barrier for the fused steps
+    (pwadv_signal_peers / pwadv_wait_peers, csrc/pwadv_sync.cu).
+
+    Call k (after step k's launches on `stream`): write k into my slot of
+    every neighbour's flag array (remote stores over NVLink into their
+    IPC-mapped memory, fenced after the step's writes), then make the stream
+    wait until every neighbour's slot in MY array holds >= k — i.e. until the
+    neighbours have finished step k too. Ranks that are not neighbours never
+    synchronise; no kernel and no NCCL call is involved, the GPU front end
+    carries both the writes and the wait. `registry` maps the flag arrays
+    (IpcPeerRegistry across processes, LocalPeerRegistry for ranks emulated
+    as threads — every rank must construct its handshake before any calls
+    one). Replaces NcclBarrier (one global all-reduce per step) on the fused
+    paths."""
+
+    def __init__(self, dec: Decomposition, registry, device=None, *, mode: str = "memop",
+                 timeout_s: float = 10.0):
+        """mode "memop": one batch of stream memory operations per call (the
+        default; validated with 8 ranks emulated on one GPU and across
+        processes). mode "kernel": a 32-thread kernel chained by programmatic
+        dependent launch doing release stores / acquire polls, with a
+        timeout that sets `err` instead of hanging (lower latency with 2-6
+        emulated ranks; see tools/handshake_latency.cu)."""
+        from . import _lib
+        if mode not in ("memop", "kernel"):
+            raise ValueError(f"unknown handshake mode {mode!r}")
+        self.mode = mode
+        self.timeout_ns = int(timeout_s * 1e9)
+        self.dec = dec
+        self.flags = torch.zeros(dec.size, dtype=torch.int64, device=device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.flags.device)
+        self.registry = registry
+        registry.publish(dec.rank, ((self.flags,),))
+        self.nbrs = sorted(set(neighbour_ranks(dec)) - {dec.rank})
+        self.k = 0
+        self._sig = self._wait = None
+        dev = self.flags.device.index or 0
+        m64, fl = ctypes.c_int(), ctypes.c_int()
+        _lib.check(_lib.lib().pwadv_handshake_caps(dev, ctypes.byref(m64), ctypes.byref(fl)))
+        self.caps = {"mem64": bool(m64.value), "flush_remote_writes": bool(fl.value)}
+        if not m64.value:
+            raise _lib.PwadvError(_lib.PWADV_E_CUDA, "64-bit stream memory operations unsupported")
+
+    @staticmethod
+    def slot_table(dec: Decomposition, my_flags: int, flags_of) -> tuple[list, list]:
+        """(signal, wait) device addresses for rank dec.rank: my slot in each
+        distinct neighbour's flag array (flags_of(rank) = its base address),
+        and each neighbour's slot in mine; slot r = byte offset 8*r."""
+        nbrs = sorted(set(neighbour_ranks(dec)) - {dec.rank})
+        return ([flags_of(r) + 8 * dec.rank for r in nbrs], [my_flags + 8 * r for r in nbrs])
+
+    def _build(self):
+        sig, wait = self.slot_table(self.dec, self.flags.data_ptr(),
+                                    lambda r: self.registry.pointers(r, 0)[0])
+        n = len(sig)
+        self._sig = (ctypes.c_void_p * max(n, 1))(*sig)
+        self._wait = (ctypes.c_void_p * max(n, 1))(*wait)
+
+    def __call__(self, stream=None) -> None:
+        from . import _lib, device as dv
+        if not self.nbrs:
+            return
+        if self._sig is None:
+            self._build()
+        self.k += 1
+        h = dv._stream_handle(stream, self.flags.device)
+        n = len(self.nbrs)
+        if self.mode == "memop":
+            _lib.check(_lib.lib().pwadv_handshake(self._sig, n, self._wait, n, self.k, h))
+        else:
+            _lib.check(_lib.lib().pwadv_handshake_kernel(self._sig, n, self._wait, n, self.k,
+                                                         ctypes.c_void_p(self.err.data_ptr()),
+                                                         self.timeout_ns, h))
+
+    def timed_out(self) -> bool:
+        """Kernel mode: some wait gave up after timeout_s (results are void)."""
+        return bool(int(self.err.item()))
+
+    def release(self) -> None:
+        """Unblock this rank's own pending waits (after a failed probe): write
+        the last awaited value into every slot of my flag array."""
+        self.flags.fill_(self.k)
+
+
 class ThreadStreamBarrier:
     """Barrier for ranks emulated as host threads on one GPU: every rank's
     stream waits on every other rank's event (kernels never wait on kernels)."""

@@ -168,3 +168,54 @@ def test_pull_evaluator_peer_table(px, py, shape):
         assert p.nx[_lib.NB_YM] == p.nx[_lib.NB_YP] == dec.local_dims.nx
         if px == 1:
             assert (p.u[_lib.NB_XM], p.u[_lib.NB_XP]) == (ptrs[dec.rank][0],) * 2
+
+
+@pytest.mark.parametrize("px,py", [(1, 2), (2, 2), (2, 4), (3, 2), (1, 1)])
+def test_flag_handshake_slot_table_pairs_up(px, py):
+    """Neighbour handshake wiring (host side): every signal rank r sends lands
+    in exactly the slot its neighbour waits on for r, neighbours are the
+    distinct 8-neighbourhood ranks (an undivided axis: none / itself), and
+    nobody signals or waits on a non-neighbour."""
+    from paper_2010_01545_b200.decomp import FlagHandshake, neighbour_ranks
+    g = pw.make_grid(6 * px, 6 * py, 4)
+    base = {r: 0x10000 * (r + 1) for r in range(px * py)}  # fake device addresses
+    sig, wait = {}, {}
+    for r in range(px * py):
+        dec = Decomposition(g, px, py, r)
+        sig[r], wait[r] = FlagHandshake.slot_table(dec, base[r], base.__getitem__)
+        nb = set(neighbour_ranks(dec)) - {r}
+        assert len(sig[r]) == len(wait[r]) == len(nb)
+        assert sorted((a - base[r]) // 8 for a in wait[r]) == sorted(nb)
+    for r in range(px * py):
+        for a in sig[r]:
+            owner = next(q for q in base if base[q] <= a < base[q] + 8 * px * py)
+            assert (a - base[owner]) // 8 == r and a in wait[owner]
+
+
+def _agree_worker(rank, port, oks, q):
+    try:
+        import torch.distributed as dist
+        import bench
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=len(oks))
+        q.put((rank, bench.agree_all(oks[rank], torch.device("cpu"))))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        q.put((rank, repr(e)))
+
+
+@pytest.mark.parametrize("oks", [(True, True), (True, False), (False, False)])
+def test_bench_ranks_agree_on_the_fused_path(oks):
+    """bench.agree_all: every rank takes the fused path only if every rank can
+    (a rank-local fallback would mix collectives and hang)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_agree_worker, args=(r, port, oks, q)) for r in range(len(oks))]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {r: all(oks) for r in range(len(oks))}, res

@@ -419,3 +419,162 @@ def test_pull_multi_unit_plans(kw):
     torch.cuda.synchronize()
     for a, b in zip(got, want):
         assert torch.equal(a.view(torch.int64), b.view(torch.int64)), kw
+
+
+# --- neighbour flag handshake (pwadv_signal_peers / pwadv_wait_peers) --------
+
+@pytest.mark.parametrize("px,py,shape,mode", [(1, 2, (30, 26, 64), "memop"), (2, 2, (25, 23, 6), "memop"),
+                                              (2, 4, (48, 40, 16), "memop"), (3, 2, (36, 30, 128), "memop"),
+                                              (1, 2, (30, 26, 64), "kernel"), (2, 2, (25, 23, 6), "kernel")])
+def test_emulated_fused_push_with_flag_handshake(px, py, shape, mode):
+    """PushStepper ordered by the neighbour-only flag handshake (stream-ordered
+    flag writes/waits, no host barrier, no kernel waiting on a kernel) ==
+    single-domain stepping, bitwise, halos included."""
+    from paper_2010_01545_b200.decomp import FlagHandshake, LocalPeerRegistry, PushStepper
+    gd = pw.make_grid(*shape)
+    spec = pw.GeneratorSpec.baseline(11)
+    co = pw.baseline_coefficients(11, gd.nz)
+    single = Stepper(device.fill(gd, spec), co, 0.1)
+    single.step(6)
+    want = single.fields
+    torch.cuda.synchronize()
+    n = px * py
+    hub = ThreadHubTransport(n)
+    reg, flag_reg = LocalPeerRegistry(), LocalPeerRegistry()
+    decs = [Decomposition(gd, px, py, r) for r in range(n)]
+    hs = [FlagHandshake(d, flag_reg, device="cuda", mode=mode, timeout_s=20.0)
+          for d in decs]  # all published up front
+
+    def rank(r):
+        dec = decs[r]
+        fs = dec.fill_local(spec)
+        ex = HaloExchanger(dec, device="cuda", transport=hub.bind(r))
+        st = PushStepper(dec, fs, co, 0.1, reg, hs[r], initial_exchange=ex.exchange)
+        st.step(6)
+        torch.cuda.current_stream().synchronize()
+        return dec, st.fields
+
+    for dec, final in run_ranks(n, rank):
+        for f, w in zip(final, want):
+            assert torch.equal(f.view(torch.int64), dec.local_view(w).contiguous().view(torch.int64)), dec.rank
+    assert all(h.k == 7 for h in hs)  # the initial handshake + one per step
+    assert not any(h.timed_out() for h in hs)
+
+
+@pytest.mark.parametrize("px,py,shape", [(1, 2, (40, 36, 64)), (2, 4, (64, 48, 64))])
+def test_emulated_pull_with_flag_handshake(px, py, shape):
+    """PullEvaluator (K1 pulling its halos from the neighbours' fields)
+    ordered by the flag handshake, evaluations interleaved with in-place
+    updates of the fields (so a missing order would read stale or torn
+    halos) == the single-domain result, bitwise, every round."""
+    import threading
+    from paper_2010_01545_b200.decomp import FlagHandshake, LocalPeerRegistry, PullEvaluator
+    gd = pw.make_grid(*shape)
+    spec = pw.GeneratorSpec.baseline(4)
+    co = pw.baseline_coefficients(4, gd.nz)
+    rounds = 4
+    g = device.fill(gd, spec)
+    wants = []
+    for k in range(rounds):
+        for f in g:  # in-place update of the fields between evaluations
+            f.mul_(1.0 + 0.25 * (k > 0))
+        device.wrap_halos(*g)
+        wants.append([o.clone() for o in device.advect(*g, co)])
+    torch.cuda.synchronize()
+    n = px * py
+    reg, flag_reg = LocalPeerRegistry(), LocalPeerRegistry()
+    decs = [Decomposition(gd, px, py, r) for r in range(n)]
+    hs = [FlagHandshake(d, flag_reg, device="cuda") for d in decs]
+    ready = threading.Barrier(n)
+
+    def rank(r):
+        dec = decs[r]
+        fs = dec.fill_local(spec)
+        ev = PullEvaluator(dec, fs, co, reg, hs[r])
+        ready.wait()  # every rank published its fields
+        got = []
+        for k in range(rounds):
+            if k:
+                hs[r]()  # neighbours done reading round k-1 before the update
+                for f in fs:
+                    f.mul_(1.25)
+            out = device.alloc_fields(dec.local_dims, "cuda")
+            ev.evaluate(out)  # handshake: neighbours' updates done, then K1 pulls
+            got.append(out)
+        torch.cuda.current_stream().synchronize()
+        return dec, got
+
+    for dec, got in run_ranks(n, rank):
+        for k in range(rounds):
+            for o, w in zip(got[k], wants[k]):
+                wl = dec.local_view(w).contiguous()
+                assert torch.equal(o[1:-1, 1:-1].contiguous().view(torch.int64),
+                                   wl[1:-1, 1:-1].contiguous().view(torch.int64)), (dec.rank, k)
+
+
+def _handshake_proc(rank, port, q):
+    """Rank of a 2-process (1x2) run on one GPU: ping-pong mailboxes in the
+    OTHER process's memory (CUDA IPC), ordered only by the flag handshake."""
+    try:
+        import torch.distributed as dist
+        import paper_2010_01545_b200 as pw2
+        from paper_2010_01545_b200 import _lib, decomp as dc, device as dv
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=2)
+        g = pw2.make_grid(8, 6, 4)
+        dec = dc.Decomposition(pw2.make_grid(8, 12, 4), 1, 2, rank)
+        hs = dc.FlagHandshake(dec, dc.IpcPeerRegistry(dec), device="cuda")
+        boxes = (dv.alloc_fields(g, "cuda"), dv.alloc_fields(g, "cuda"))  # my mailboxes (ping-pong)
+        mreg = dc.IpcPeerRegistry(dec)
+        mreg.publish(rank, boxes)
+        other = 1 - rank
+        seen = []
+        rounds = 40
+        for k in range(1, rounds + 1):
+            # my "step": read my mailbox written by the other rank in step k-1,
+            # write the other rank's mailbox k % 2 (K5 fill with seed k)
+            if k > 1:
+                seen.append([t.clone() for t in boxes[(k - 1) % 2]])
+            ptrs = mreg.pointers(other, k % 2)
+            _lib.check(_lib.lib().pwadv_fill_f64(*(ctypes.c_void_p(p) for p in ptrs), g.nx, g.ny, g.nz,
+                                                 0, 1000 * (rank + 1) + k, 0.0, 0.0, 0.0,
+                                                 dv._stream_handle(None, torch.device("cuda", 0))))
+            hs()
+        torch.cuda.synchronize()
+        bad = 0
+        for k, got in zip(range(1, rounds), seen):
+            want = dv.fill(g, pw2.GeneratorSpec.random(1000 * (other + 1) + k))
+            bad += sum(0 if torch.equal(a.view(torch.int64), b.view(torch.int64)) else 1
+                       for a, b in zip(got, want))
+        torch.cuda.synchronize()
+        dist.barrier()
+        mreg.close()
+        hs.registry.close()
+        q.put((rank, "ok", bad, hs.k, int(hs.flags[other].item())))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, "error", repr(e), 0, 0))
+
+
+def test_flag_handshake_across_processes_ipc():
+    """The handshake as bench.py runs it (IpcPeerRegistry over torch.distributed,
+    remote flag writes into CUDA-IPC-mapped memory), two processes on one GPU:
+    40 ping-pong rounds of cross-process mailbox writes, each read only after
+    the handshake — every mailbox holds exactly the other rank's round-k fill."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_handshake_proc, args=(r, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    for rank, status, bad, k, peer_flag in res:
+        assert status == "ok", (rank, bad)
+        assert bad == 0 and k == 40 and peer_flag == 40, (rank, bad, k, peer_flag)
