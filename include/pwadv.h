@@ -71,8 +71,8 @@ enum {
 #define PWADV_FLAG_DEBUG_NO_COMPUTE 0x100u
 #define PWADV_FLAG_DEBUG_NO_STORE 0x400u
 /* X-march work plan: never / always (where it applies) use the spare-tail
- * plan (main chunks + tail chunks run by the spare CTAs; default: when it
- * shortens the longest CTA by >= 5%) */
+ * plan (main chunks + tail chunks run by the spare CTAs; default: for plans
+ * of short units, <= 130 planes, when it shortens the longest CTA by >= 5%) */
 #define PWADV_FLAG_NO_SPARE_TAIL 0x1000u
 #define PWADV_FLAG_SPARE_TAIL 0x2000u
 

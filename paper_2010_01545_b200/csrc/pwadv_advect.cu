@@ -634,11 +634,14 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     static_assert(NZC == 0 || (MAXT == 512 && 384 % (NZC / 2) == 0), "compile-time layout: WS only");
     static_assert(!UA || (MAXT == 512 && NZC == 0), "unaligned runs: warp-specialised, run-time layout");
     static_assert(!PULL || (MAXT == 512 && !UA), "halo pull: warp-specialised, aligned runs");
-    // programmatic dependent launch (launch_box): wait until the previous grid
-    // on the stream has completed and its writes are visible (they may be our
-    // inputs) before any global access, and let the next grid be scheduled
-    // as our CTAs retire. No-ops for an ordinary launch.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // programmatic dependent launch (launch_box): let the next grid be
+    // scheduled as our CTAs retire, and wait until the previous grid on the
+    // stream has completed and its writes are visible (they may be our
+    // inputs) before any global access. The unit table and the ring barriers
+    // (shared memory and kernel parameters only) are set up BEFORE the wait,
+    // while the previous grid drains; tid 0 waits before the first bulk copy,
+    // every other thread after the CTA barrier that publishes the table.
+    // No-ops for an ordinary launch.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int S = t.stages;
     const int TJ = NZC ? 384 / (NZC / 2) : t.tj;
@@ -672,13 +675,14 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     const int k1c = UA ? (k1 < nz ? k1 : nz - 1) : k1;  // odd nz: k1 = nz is past the column
 
     const double tcx = a.tcx, tcy = a.tcy, dt = a.dt;
-    const double c1a = __ldg(a.tzc1 + k0), c1b = __ldg(a.tzc1 + k1c);
-    const double c2a = __ldg(a.tzc2 + k0), c2b = __ldg(a.tzc2 + k1c);
 
     const int64_t ny2 = a.ny + 2;
     const int64_t G = gridDim.x;
     const int64_t nunits = units_of(t, G);
-    if ((int64_t)blockIdx.x >= nunits) return;
+    if ((int64_t)blockIdx.x >= nunits) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        return;
+    }
 
     if (tid == 0) {
         int q = 0, k = 0;
@@ -718,6 +722,7 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
             rs->released[s] = 0;
         }
         fence_mbar_init();
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // inputs final from here on
         const int n0 = PULL ? 0 : (q < S ? q : S);  // pull: the producer warp issues all
         for (int n = 0; n < n0; ++n) {
             if constexpr (UA) issue_plane_ua(rs, a, n, n, CS, ring, full);
@@ -725,6 +730,9 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
         }
     }
     __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const double c1a = __ldg(a.tzc1 + k0), c1b = __ldg(a.tzc1 + k1c);
+    const double c2a = __ldg(a.tzc2 + k0), c2b = __ldg(a.tzc2 + k1c);
     const int total = rs->total;
     const int my_units = rs->nunits;
     if constexpr (WS) {
@@ -1446,13 +1454,19 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
         p->rounds = (units + grid - 1) / grid;
     }
     // Spare-tail plan. A single-round plan whose units do not fill the SMs
-    // (C1 512x512x64: 43 strips x 3 chunks = 129 CTAs of 171 planes, 19 SMs
-    // idle) is rebalanced: each strip gets m main chunks of L planes (one per
-    // CTA, all concurrent) and one tail chunk of nbx - m*L planes; the G - n*m
+    // is rebalanced: each strip gets m main chunks of L planes (one per CTA,
+    // all concurrent) and one tail chunk of nbx - m*L planes; the G - n*m
     // spare CTAs run the n tail chunks, ceil(n / spare) each in sequence. L
     // balances a main CTA's L + 2 planes against a spare CTA's tail planes
-    // (C1: m = 3, L = 154, tails of 50, 3 per spare CTA: 156 planes per CTA
-    // instead of 173, on all 148 SMs).
+    // (512x256x64, the C2 block per GPU at 2x4: 22 strips x 6 chunks = 132
+    // CTAs of 86 planes -> m = 6, L = 79, 16 spare CTAs: 81 planes per CTA).
+    // Measured in bursts of back-to-back launches (tools/sweep.py
+    // --burst-sleep, profiles/README.md) it pays only for SHORT units: +1% at
+    // 512x256x64, +2% at 256x256x64; with units of 150+ planes the classic
+    // plan's ~129 CTAs already saturate HBM and the tail CTAs' extra plane
+    // pairs and out-of-step halo columns cost more than the idle SMs (C1
+    // 512x512x64: 131.9 classic vs 130.1 spare, 768^2: 135.0 vs 131.5,
+    // 1024x512: 136.3 vs 132.0 Gpts/s). PWADV_FLAG_SPARE_TAIL forces it.
     p->spare = 0;
     p->mlen = 0;
     if (!L.pull && L.chunks <= 0 && L.grid <= 0 && full_rounds == 0 && per_sm == 1 &&
@@ -1477,7 +1491,8 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
             }
         }
         const int64_t cur = (nbx + p->nchunks - 1) / p->nchunks + 2;  // planes per CTA now
-        if (best_m > 0 && ((L.flags & PWADV_FLAG_SPARE_TAIL) || best_planes * 100 <= cur * 95)) {
+        const bool pays = cur <= 130 && best_planes * 100 <= cur * 95;
+        if (best_m > 0 && ((L.flags & PWADV_FLAG_SPARE_TAIL) || pays)) {
             p->spare = (int)best_sp;
             p->mlen = best_l;
             p->nchunks = (int)best_m;

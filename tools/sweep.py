@@ -17,7 +17,8 @@ from paper_2010_01545_b200 import device  # noqa: E402
 SHAPES = {"c1": (512, 512, 64), "c2": (1024, 1024, 64), "c3": (2048, 2048, 64),
           "c4blk": (2048, 1024, 128), "c0": (64, 64, 64), "c4full": (4096, 4096, 128),
           "c1odd": (512, 512, 63), "c3odd": (2048, 2048, 63), "tall": (128, 128, 1030),
-          "c2blk8": (512, 256, 64), "c2blk4": (512, 512, 64)}
+          "c2blk8": (512, 256, 64), "c2blk4": (512, 512, 64), "c3blk8": (1024, 512, 64),
+          "s256": (256, 256, 64), "s768": (768, 768, 64), "c4blk8": (1024, 1024, 128)}
 
 
 BURST_SLEEP = 0.0
