@@ -96,11 +96,15 @@ def main():
             kw = dict(v)
             name = kw.pop("variant")
             dbg = kw.pop("debug", 0)
+            pull = kw.pop("pull", False)
             opts = device.make_opts(name, **kw)
             opts.flags |= (dbg << 8)
             try:
                 plan = device.describe_plan(dims, None, opts)
-                if args.step:
+                if pull:  # K1 with the halo pull, the block as its own 8 neighbours
+                    bl = device.BoundLaunch(fields, co, out, opts=opts, pull=device.self_peers(fields))
+                    ms = time_it(bl, args.reps)
+                elif args.step:
                     ms = time_it(lambda: device.step(*fields, co, 0.1, out, opts=opts), args.reps)
                 else:
                     ms = time_it(lambda: device.advect(*fields, co, out, opts=opts), args.reps)
