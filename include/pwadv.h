@@ -75,6 +75,13 @@ enum {
  * of short units, <= 130 planes, when it shortens the longest CTA by >= 5%) */
 #define PWADV_FLAG_NO_SPARE_TAIL 0x1000u
 #define PWADV_FLAG_SPARE_TAIL 0x2000u
+/* Column-tile X-march (K1c: work unit = X chunk x y-strip x k-slab, one bulk
+ * copy per staged column, every (k, k+1) pair on the 16-byte grid even for odd
+ * nz): force it where it applies / never use it (default: the planner's
+ * choice). With it, tile_j selects the slab height
+ * KT = 768 / tile_j: 6 (KT 128), 12 (KT 64) or 24 (KT 32). */
+#define PWADV_FLAG_CTILE 0x4000u
+#define PWADV_FLAG_NO_CTILE 0x8000u
 
 /* Optional tuning / variant selection; pass NULL for defaults. */
 typedef struct pwadv_opts {
@@ -131,7 +138,9 @@ typedef struct pwadv_plan_info {
                               3 = general march (register x-window, cached loads: tall
                               columns, inputs with different 16-byte phases),
                               4 = X-march with unaligned tile runs (odd nz, 8-byte-aligned
-                              fields) */
+                              fields), 5 = column-tile X-march (k-slabs of
+                              2 x threads_per_column levels; strips counts
+                              y-strips x slabs) */
     int32_t tile_j, threads_per_column, stages, threads, grid;
     int64_t smem_bytes, strips;
     int32_t chunks;        /* X chunks of the strips after the full rounds */

@@ -43,6 +43,8 @@ FLAG_L2_UNIT_HEAD = 64
 FLAG_NO_PDL = 128
 FLAG_NO_SPARE_TAIL = 0x1000
 FLAG_SPARE_TAIL = 0x2000
+FLAG_CTILE = 0x4000
+FLAG_NO_CTILE = 0x8000
 ABI_VERSION = 2
 
 

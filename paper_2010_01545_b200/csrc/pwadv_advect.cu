@@ -45,6 +45,8 @@
 #include "pwadv_device.cuh"
 #include "pwadv_internal.h"
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <mutex>
 #include <type_traits>
@@ -153,6 +155,8 @@ struct TileCfg {
     // count still keeps every SM busy for about the same time
     int spare;
     int64_t mlen;
+    int nslab;  // column-tile kernel (k_advect_ctile): k-slabs per column; strips of the
+                // unit numbering are (y-strip, slab) pairs, slab fastest. 1 otherwise
 };
 
 // work units of a launch (unit_at's numbering)
@@ -1085,6 +1089,12 @@ __global__ void __launch_bounds__(MAXT, ctas_per_sm(MAXT))
     }
 }
 
+}  // namespace pwadv
+
+#include "pwadv_ctile.cuh"
+
+namespace pwadv {
+
 // ---------------------------------------------------------------------------
 // host-side planning and launch
 
@@ -1128,6 +1138,83 @@ static cudaError_t ensure_smem_attr(const void *kern, int device, int bytes)
         done.push_back({kern, device, bytes});
     }
     return e;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// libcuda link): resolved once.
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// a field (nx+2, ny+2, nz) as a 3-D tensor {nz, ny+2, nx+2}; box {kt+4, tj+2, 1}
+static int encode_field_map(CUtensorMap *m, const double *f, const BoxLaunch &L, int kt, int tj)
+{
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) return set_error(PWADV_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[3] = {(cuuint64_t)L.nz, (cuuint64_t)(L.ny + 2), (cuuint64_t)(L.nx + 2)};
+    const cuuint64_t strides[2] = {(cuuint64_t)L.nz * sizeof(double),
+                                   (cuuint64_t)((L.ny + 2) * L.nz) * sizeof(double)};
+    const cuuint32_t box[3] = {(cuuint32_t)(kt + 4), (cuuint32_t)(tj + 2), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(f), dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(PWADV_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return PWADV_OK;
+}
+
+// K1c / K4c launch (plan.ct): the fields' tensor maps are kernel parameters
+static int launch_ctile(const BoxLaunch &L, const BoxArgs &a, const TileCfg &t, const XmarchPlan &plan,
+                        bool fma, cudaStream_t stream)
+{
+    CtMaps maps;
+    int rc = encode_field_map(&maps.u, L.u, L, plan.kt, plan.tj);
+    if (rc == PWADV_OK) rc = encode_field_map(&maps.v, L.v, L, plan.kt, plan.tj);
+    if (rc == PWADV_OK) rc = encode_field_map(&maps.w, L.w, L, plan.kt, plan.tj);
+    if (rc != PWADV_OK) return rc;
+    void (*kern)(BoxArgs, TileCfg, CtMaps) = nullptr;
+#define PWADV_PICK_CT(KT)                                                                     \
+    if (plan.kt == KT)                                                                        \
+        kern = L.step ? (fma ? k_advect_ctile<true, true, KT> : k_advect_ctile<false, true, KT>) \
+                      : (fma ? k_advect_ctile<true, false, KT> : k_advect_ctile<false, false, KT>);
+    PWADV_PICK_CT(32)
+    PWADV_PICK_CT(64)
+    PWADV_PICK_CT(128)
+#undef PWADV_PICK_CT
+    if (!kern) return set_error(PWADV_E_ARG, "unsupported slab height %d", plan.kt);
+    const DeviceInfo *dev = device_info();
+    cudaError_t e = ensure_smem_attr((const void *)kern, dev->device, (int)plan.smem);
+    if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute", e);
+    if (L.flags & PWADV_FLAG_NO_PDL) {
+        kern<<<plan.grid, plan.threads, plan.smem, stream>>>(a, t, maps);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)plan.grid);
+        cfg.blockDim = dim3((unsigned)plan.threads);
+        cfg.dynamicSmemBytes = plan.smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, a, t, maps);
+        if (e != cudaSuccess) return set_cuda_error("advect launch", e);
+    }
+    count_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error("advect launch", e);
+    return PWADV_OK;
 }
 
 int launch_box(const BoxLaunch &L, cudaStream_t stream)
@@ -1181,6 +1268,7 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
     }
     if (tiled) {
         TileCfg t;
+        t.nslab = plan.ct ? plan.nslab : 1;
         t.tj = plan.tj;
         t.kp = plan.kp;
         t.stages = plan.stages;
@@ -1194,10 +1282,11 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         t.nchf = plan.nchf;
         t.spare = plan.spare;
         t.mlen = plan.mlen;
+        if (plan.ct) return launch_ctile(L, a, t, plan, fma, stream);
         void (*kern)(BoxArgs, TileCfg) = nullptr;
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
         // compile-time layout for the BASELINE depths at the default tile
-        const int nzc = (!plan.elem && plan.maxt == 512 && plan.tj * plan.kp == 384 &&
+        const int nzc = (!plan.elem && !plan.ct && plan.maxt == 512 && plan.tj * plan.kp == 384 &&
                          (L.nz == 64 || L.nz == 128) &&
                          !(L.flags & (PWADV_FLAG_GENERIC | PWADV_FLAG_DEBUG_NO_COMPUTE |
                                       PWADV_FLAG_DEBUG_NO_STORE)))
@@ -1218,13 +1307,13 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
             else kern = fix ? pick_ws<0, true, false, true>(L.step, fma)
                             : pick_ws<0, false, false, true>(L.step, fma);
         }
-        if (!kern) {
+        if (!kern && !plan.ct) {
             PWADV_PICK_NZ(64, false)
             PWADV_PICK_NZ(128, true)
         }
 #undef PWADV_PICK_NZ
 #define PWADV_PICK_ELEM(FX)                                                      \
-    if (plan.elem && fix == FX) {                                                \
+    if (!kern && plan.elem && fix == FX) {                                       \
         if (L.step)                                                              \
             kern = fma ? k_advect_xmarch<true, true, 512, FX, 0, true>           \
                        : k_advect_xmarch<false, true, 512, FX, 0, true>;         \
@@ -1327,68 +1416,12 @@ static size_t slot_doubles(int64_t tj, int64_t nz, bool ua)
     return (size_t)(ua ? ((run + 3) & ~(int64_t)1) : run);
 }
 
-bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
+// Work units for p->nstrips strips (y-strips, or y-strip x k-slab pairs of the
+// column-tile kernel) of nbx planes: full rounds of whole strips, the rest in
+// X chunks, optionally the spare-tail plan (plan_xmarch's notes below).
+static void plan_work(const BoxLaunch &L, const DeviceInfo &dev, int per_sm, XmarchPlan *p)
 {
-    if (L.flags & (PWADV_FLAG_SIMPLE | PWADV_FLAG_RIM | PWADV_FLAG_MARCH)) return false;
-    const int64_t nz = L.nz;
-    // 16-byte alignment and even nz for 16-byte-aligned tile runs and the
-    // paired loads/stores; otherwise UA (unaligned runs: the copies start up to
-    // one element early, scalar shared loads and stores, also into the peers'
-    // halos) — warp-specialised only, u, v, w with the same 16-byte phase
-    uintptr_t al = (uintptr_t)L.u | (uintptr_t)L.v | (uintptr_t)L.w | (uintptr_t)L.o0 |
-                   (uintptr_t)L.o1 | (uintptr_t)L.o2;
-    // fused push: the aligned form stores boundary pairs into the peers'
-    // halos with 16-byte stores too — 8-byte-aligned peers take the UA form
-    // (scalar stores); pwadv_step_push_f64 requires 8-byte-aligned peers
-    if (L.peers && !L.pull)
-        for (int d = 0; d < 8; ++d)
-            al |= (uintptr_t)L.peers->u[d] | (uintptr_t)L.peers->v[d] | (uintptr_t)L.peers->w[d];
-    const bool ua = (nz % 2 != 0) || (al & 15) || (L.flags & PWADV_FLAG_UNALIGNED);
-    const uintptr_t inpar = ((uintptr_t)L.u ^ (uintptr_t)L.v) | ((uintptr_t)L.u ^ (uintptr_t)L.w);
-    if (ua && ((al & 7) || (inpar & 8) || (L.max_threads > 0 && L.max_threads != 512) ||
-               (L.flags & (PWADV_FLAG_DEBUG_NO_COMPUTE | PWADV_FLAG_DEBUG_NO_STORE))))
-        return false;
-    if (nz > 1024) return false;
-    p->elem = ua ? 1 : 0;
-    const int kp = (int)((nz + 1) / 2);
-    const int64_t nby = L.y1 - L.y0, nbx = L.x1 - L.x0;
-    // thread budget per CTA (register file / CTA): 384 by default, which
-    // leaves ~168 registers per thread for the rolled x-window
-    // default: warp-specialised 512 threads (3 compute warpgroups of 160
-    // registers + a producer warpgroup); measured 125 Gpts/s at C1/C3 vs 110
-    // for the 384-thread kernel whose warps issue the refills themselves
-    int maxt = L.max_threads > 0 ? L.max_threads : 512;
-    if (maxt != 512 && maxt != 384 && maxt != 256 && maxt != 192 && maxt != 128) return false;
-    const int tile_threads = maxt == 512 ? 384 : maxt;  // 512: 3 compute + 1 producer warpgroup
-    const int per_sm = ctas_per_sm(maxt);
-    if (kp > maxt) return false;
-    int tj = L.tile_j > 0 ? L.tile_j : tile_threads / kp;
-    if (tj > tile_threads / kp) tj = tile_threads / kp;
-    if (tj < 1) return false;
-    if (tj > nby) tj = (int)nby;
-    const size_t bar_bytes = 2 * 16 * sizeof(uint64_t) + sizeof(RingState);
-    // shared memory per CTA: the SM's 228 KB split between resident CTAs
-    size_t smem_cap = (size_t)dev.smem_optin - bar_bytes - 1024;
-    if (per_sm > 1) smem_cap = (size_t)(228 * 1024) / per_sm - bar_bytes - 1024 - 1024;
-    int stages = 0;
-    for (;;) {
-        const size_t stage_bytes = (size_t)3 * slot_doubles(tj, nz, ua) * sizeof(double);
-        int smax = (int)(smem_cap / stage_bytes);
-        if (smax > 16) smax = 16;  // RingState::released
-        // default ring depth 5 (tools/sweep.py; see the note at the end)
-        stages = L.stages > 0 ? (L.stages < smax ? L.stages : smax) : (smax < 5 ? smax : 5);
-        if (stages >= 3) break;
-        if (tj == 1) return false;
-        tj = tj / 2;
-    }
-    p->maxt = maxt;
-    p->tj = tj;
-    p->kp = kp;
-    p->stages = stages;
-    p->threads = maxt == 512 ? 512 : round_up(tj * kp, 32);
-    p->smem = (size_t)stages * 3 * slot_doubles(tj, nz, ua) * sizeof(double) + 2 * stages * sizeof(uint64_t) +
-              sizeof(RingState);
-    p->nstrips = (nby + tj - 1) / tj;
+    const int64_t nbx = L.x1 - L.x0;
     // Work units dealt round-robin to one wave of CTAs. Whole strips fill
     // as many full rounds as there are (long units keep all CTAs marching in
     // step: at 4096x4096x128, 36 short units per CTA instead of 5 long ones
@@ -1500,6 +1533,160 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
             p->rounds = (n + best_sp - 1) / best_sp;
         }
     }
+}
+
+// Slab height of the column-tile plan: the least (slab levels x preference).
+// Measured at equal slab fill KT 128 >= KT 64 (within 1-2%) > KT 32 (~8%: two
+// columns per warp): nz 1024 -> 128, 1030 -> 64 (17 slabs, 5.6% idle levels
+// against 12% for 128), 160 -> 32 (tools/shape_sweep.py, profiles/README.md).
+static int ctile_kt(int64_t nz)
+{
+    int kt = 128;
+    double best = 0.0;
+    for (int c : {128, 64, 32}) {
+        const double pref = c == 128 ? 1.0 : (c == 64 ? 1.01 : 1.08);
+        const double cost = (double)((nz + c - 1) / c * c) * pref;
+        if (best == 0.0 || cost < best) {
+            best = cost;
+            kt = c;
+        }
+    }
+    return kt;
+}
+
+// Whole-column X-march vs column tiles, from a fit to the measured rates
+// (profiles/README.md, round 2): relative rate = busy-thread fraction x a
+// strip-width factor (whole columns: 1.0 at TJ >= 6, 0.97 / 0.95 / 0.93 /
+// 0.9 / 0.8 at TJ = 5 / 4 / 3 / 2 / 1; column tiles 0.98 / slab preference).
+// E.g. nz 64, 128: whole columns (1.0 vs 0.98); 130: whole (0.82 vs 0.74 —
+// 23% idle slab levels); 160, 192, 256 and deeper: tiles.
+static bool ctile_pays(int64_t nz)
+{
+    if (nz % 2 != 0) return false;
+    const int kt = ctile_kt(nz);
+    const double pref = kt == 128 ? 1.0 : (kt == 64 ? 1.01 : 1.08);
+    const double ct = 0.98 * (double)nz / (double)((nz + kt - 1) / kt * kt) / pref;
+    const int64_t kp = nz / 2;
+    if (kp > 384) return true;  // no whole-column plan
+    const int64_t tj = 384 / kp;
+    static const double width[6] = {0.0, 0.8, 0.9, 0.93, 0.95, 0.97};
+    const double whole = (double)(tj * kp) / 384.0 * (tj >= 6 ? 1.0 : width[tj]);
+    return ct > whole;
+}
+
+// Column-tile plan (k_advect_ctile). Applies to 16-byte-aligned fields with
+// even nz (tensor-map strides), without the fused halo pull / push, at the
+// 512-thread budget. Slab height KT from opts.tile_j (768 / tile_j) or the default below.
+static bool plan_ctile(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
+{
+    const int64_t nz = L.nz;
+    const uintptr_t al = (uintptr_t)L.u | (uintptr_t)L.v | (uintptr_t)L.w | (uintptr_t)L.o0 |
+                         (uintptr_t)L.o1 | (uintptr_t)L.o2;
+    if ((al & 15) || nz % 2 != 0 || L.peers || L.pull ||
+        (L.max_threads > 0 && L.max_threads != 512) ||
+        (L.flags & (PWADV_FLAG_DEBUG_NO_COMPUTE | PWADV_FLAG_DEBUG_NO_STORE | PWADV_FLAG_UNALIGNED |
+                    PWADV_FLAG_GENERIC)))
+        return false;
+    int kt = ctile_kt(nz);
+    if (L.tile_j > 0) {
+        if (L.tile_j != 6 && L.tile_j != 12 && L.tile_j != 24) return false;
+        kt = 768 / L.tile_j;
+    }
+    const int tj = 768 / kt;
+    const int64_t nby = L.y1 - L.y0;
+    const int64_t nslab = (nz + kt - 1) / kt;
+    const size_t stage_bytes = (size_t)3 * (((tj + 2) * (kt + 4) + 15) / 16 * 16) * sizeof(double);
+    const size_t bar_bytes = 2 * 16 * sizeof(uint64_t) + sizeof(RingState);
+    const size_t smem_cap = (size_t)dev.smem_optin - bar_bytes - 1024;
+    int smax = (int)(smem_cap / stage_bytes);
+    if (smax > 16) smax = 16;
+    const int stages = L.stages > 0 ? (L.stages < smax ? L.stages : smax) : (smax < 5 ? smax : 5);
+    if (stages < 3) return false;
+    *p = XmarchPlan{};
+    p->ct = 1;
+    p->kt = kt;
+    p->nslab = (int)nslab;
+    p->maxt = 512;
+    p->tj = tj;
+    p->kp = kt / 2;
+    p->stages = stages;
+    p->threads = 512;
+    p->smem = (size_t)stages * stage_bytes + 2 * stages * sizeof(uint64_t) + sizeof(RingState);
+    p->nstrips = (nby + tj - 1) / tj * nslab;
+    plan_work(L, dev, 1, p);
+    return true;
+}
+
+bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
+{
+    if (L.flags & (PWADV_FLAG_SIMPLE | PWADV_FLAG_RIM | PWADV_FLAG_MARCH)) return false;
+    // the column-tile X-march: forced, or the default where it is expected to
+    // be faster (ctile_pays: deep columns, whose whole-column strips shrink to
+    // 1-5 columns — measured 122-133 Gpts/s at nz 160-2048 against 106-124
+    // for the whole-column X-march and ~80 for K1m above 768)
+    if (!(L.flags & PWADV_FLAG_NO_CTILE) && ((L.flags & PWADV_FLAG_CTILE) || (L.tile_j <= 0 && ctile_pays(L.nz))) &&
+        plan_ctile(L, dev, p))
+        return true;
+    const int64_t nz = L.nz;
+    // 16-byte alignment and even nz for 16-byte-aligned tile runs and the
+    // paired loads/stores; otherwise UA (unaligned runs: the copies start up to
+    // one element early, scalar shared loads and stores, also into the peers'
+    // halos) — warp-specialised only, u, v, w with the same 16-byte phase
+    uintptr_t al = (uintptr_t)L.u | (uintptr_t)L.v | (uintptr_t)L.w | (uintptr_t)L.o0 |
+                   (uintptr_t)L.o1 | (uintptr_t)L.o2;
+    // fused push: the aligned form stores boundary pairs into the peers'
+    // halos with 16-byte stores too — 8-byte-aligned peers take the UA form
+    // (scalar stores); pwadv_step_push_f64 requires 8-byte-aligned peers
+    if (L.peers && !L.pull)
+        for (int d = 0; d < 8; ++d)
+            al |= (uintptr_t)L.peers->u[d] | (uintptr_t)L.peers->v[d] | (uintptr_t)L.peers->w[d];
+    const bool ua = (nz % 2 != 0) || (al & 15) || (L.flags & PWADV_FLAG_UNALIGNED);
+    const uintptr_t inpar = ((uintptr_t)L.u ^ (uintptr_t)L.v) | ((uintptr_t)L.u ^ (uintptr_t)L.w);
+    if (ua && ((al & 7) || (inpar & 8) || (L.max_threads > 0 && L.max_threads != 512) ||
+               (L.flags & (PWADV_FLAG_DEBUG_NO_COMPUTE | PWADV_FLAG_DEBUG_NO_STORE))))
+        return false;
+    if (nz > 1024) return false;
+    p->elem = ua ? 1 : 0;
+    const int kp = (int)((nz + 1) / 2);
+    const int64_t nby = L.y1 - L.y0;
+    // thread budget per CTA (register file / CTA): 384 by default, which
+    // leaves ~168 registers per thread for the rolled x-window
+    // default: warp-specialised 512 threads (3 compute warpgroups of 160
+    // registers + a producer warpgroup); measured 125 Gpts/s at C1/C3 vs 110
+    // for the 384-thread kernel whose warps issue the refills themselves
+    int maxt = L.max_threads > 0 ? L.max_threads : 512;
+    if (maxt != 512 && maxt != 384 && maxt != 256 && maxt != 192 && maxt != 128) return false;
+    const int tile_threads = maxt == 512 ? 384 : maxt;  // 512: 3 compute + 1 producer warpgroup
+    const int per_sm = ctas_per_sm(maxt);
+    if (kp > maxt) return false;
+    int tj = L.tile_j > 0 ? L.tile_j : tile_threads / kp;
+    if (tj > tile_threads / kp) tj = tile_threads / kp;
+    if (tj < 1) return false;
+    if (tj > nby) tj = (int)nby;
+    const size_t bar_bytes = 2 * 16 * sizeof(uint64_t) + sizeof(RingState);
+    // shared memory per CTA: the SM's 228 KB split between resident CTAs
+    size_t smem_cap = (size_t)dev.smem_optin - bar_bytes - 1024;
+    if (per_sm > 1) smem_cap = (size_t)(228 * 1024) / per_sm - bar_bytes - 1024 - 1024;
+    int stages = 0;
+    for (;;) {
+        const size_t stage_bytes = (size_t)3 * slot_doubles(tj, nz, ua) * sizeof(double);
+        int smax = (int)(smem_cap / stage_bytes);
+        if (smax > 16) smax = 16;  // RingState::released
+        // default ring depth 5 (tools/sweep.py; see the note at the end)
+        stages = L.stages > 0 ? (L.stages < smax ? L.stages : smax) : (smax < 5 ? smax : 5);
+        if (stages >= 3) break;
+        if (tj == 1) return false;
+        tj = tj / 2;
+    }
+    p->maxt = maxt;
+    p->tj = tj;
+    p->kp = kp;
+    p->stages = stages;
+    p->threads = maxt == 512 ? 512 : round_up(tj * kp, 32);
+    p->smem = (size_t)stages * 3 * slot_doubles(tj, nz, ua) * sizeof(double) + 2 * stages * sizeof(uint64_t) +
+              sizeof(RingState);
+    p->nstrips = (nby + tj - 1) / tj;
+    plan_work(L, dev, per_sm, p);
     // Ring depth: 5 stages (the default above) for every plan. Measured as
     // the bench runs it — bursts of back-to-back launches at full clocks
     // (tools/sweep.py --burst-sleep 0.3 --prewarm-ms 30, profiles/README.md):

@@ -327,7 +327,7 @@ int pwadv_describe_plan(int64_t nx, int64_t ny, int64_t nz, int64_t x0, int64_t 
     XmarchPlan p{};
     *out = pwadv_plan_info{};
     if (plan_xmarch(L, *dev, &p)) {
-        out->kernel = p.elem ? 4 : 1;
+        out->kernel = p.ct ? 5 : (p.elem ? 4 : 1);
         out->tile_j = p.tj;
         out->threads_per_column = p.kp;
         out->stages = p.stages;

@@ -42,6 +42,9 @@ struct XmarchPlan {
     int rot, nface, nchf;  // halo pull: strip rotation and the y-face strips' chunking
     int spare;             // spare-tail plan: CTAs running the strips' tail chunks (0 = off)
     int64_t mlen;          //   planes per main chunk (nchunks main chunks per strip)
+    int ct = 0;            // 1: column-tile X-march (k_advect_ctile): tj x kt tiles
+    int kt = 0;            //   levels per slab
+    int nslab = 1;         //   slabs per column (nstrips counts y-strips x slabs)
 };
 
 // cached attributes of the current device (lazily filled, thread-safe)

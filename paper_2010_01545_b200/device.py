@@ -93,8 +93,11 @@ def make_opts(variant: str = "xmarch", *, tile_j: int = 0, stages: int = 0, grid
     (one thread per point), "xmarch_generic" (the X-march with a run-time
     tile layout even where a compile-time one exists), "xmarch_elem" (the
     X-march with unaligned tile runs and scalar shared loads — what odd nz
-    and 8-byte-aligned fields run on), "march" (the general march K1m, no plane
-    ring); suffix "_fma" for the DFMA (not bit-exact) build."""
+    and 8-byte-aligned fields run on), "xmarch_ct" (the column-tile X-march:
+    k-slab work units, every pair on the 16-byte grid; tile_j 6/12/24 selects
+    the slab height 128/64/32), "xmarch_noct" (the X-march without the column-
+    tile form), "march" (the general march K1m, no plane ring); suffix "_fma"
+    for the DFMA (not bit-exact) build."""
     base = variant
     if variant.endswith("_fma"):
         flags |= _lib.FLAG_FMA
@@ -105,6 +108,10 @@ def make_opts(variant: str = "xmarch", *, tile_j: int = 0, stages: int = 0, grid
         flags |= _lib.FLAG_GENERIC
     elif base == "xmarch_elem":
         flags |= _lib.FLAG_UNALIGNED
+    elif base == "xmarch_ct":
+        flags |= _lib.FLAG_CTILE
+    elif base == "xmarch_noct":
+        flags |= _lib.FLAG_NO_CTILE
     elif base == "march":
         flags |= _lib.FLAG_MARCH
     elif base != "xmarch":
@@ -296,7 +303,7 @@ def describe_plan(dims: GridDims, box=None, opts: _lib.Opts | None = None, devic
     info = _lib.PlanInfo()
     _lib.check(_lib.lib().pwadv_describe_plan(dims.nx, dims.ny, dims.nz, x0, x1, y0, y1,
                                               _lib.opts_ptr(opts), int(device), ctypes.byref(info)))
-    return {"kernel": {1: "xmarch", 2: "simple", 3: "march", 4: "xmarch_elem"}[info.kernel], "tile_j": info.tile_j,
+    return {"kernel": {1: "xmarch", 2: "simple", 3: "march", 4: "xmarch_elem", 5: "xmarch_ct"}[info.kernel], "tile_j": info.tile_j,
             "threads_per_column": info.threads_per_column, "stages": info.stages,
             "threads": info.threads, "grid": info.grid, "smem_bytes": info.smem_bytes,
             "strips": info.strips, "chunks": info.chunks, "long_strips": info.long_strips,

@@ -482,8 +482,8 @@ def test_async_host_submissions_bitwise():
 
 @pytest.mark.parametrize("shape", [(5, 4, 300), (3, 3, 512), (2, 3, 1024), (2, 2, 1030), (4, 3, 3)])
 def test_tall_and_odd_columns_bitwise(shape):
-    # narrow X-march tiles (nz 300, 512), the one-thread-per-point fallback
-    # (nz 1024 > thread budget, odd nz), all against the oracle
+    # deep columns (nz 300, 512, 1024, 1030: column tiles), odd nz, all
+    # against the oracle; the whole-column X-march and K1m forced agree too
     nx, ny, nz = shape
     u, v, w = oracle.fill_random(nx, ny, nz, 17, baseline=True)
     co = oracle.baseline_coefficients(17, nz)
@@ -491,11 +491,16 @@ def test_tall_and_odd_columns_bitwise(shape):
     got, dims = gpu_advect(u, v, w, *args)
     assert_bitwise(got, oracle.advect(u, v, w, *args), shape)
     plan = device.describe_plan(dims)
-    assert plan["kernel"] == ("xmarch" if nz in (300, 512) else
-                              "xmarch_elem" if nz % 2 and nz < 1024 else "march")
+    # even deep columns: the column-tile X-march (k-slabs); odd nz: the UA
+    # form up to 767, K1m above
+    assert plan["kernel"] == ("xmarch_ct" if nz % 2 == 0 and nz > 128 else
+                              "xmarch_elem" if nz % 2 and nz < 768 else "march")
     # and the one-thread-per-point kernel, forced, agrees
     got_s, _ = gpu_advect(u, v, w, *args, "simple")
     assert_bitwise(got_s, oracle.advect(u, v, w, *args), (shape, "simple"))
+    for variant in ("xmarch_noct", "march"):
+        got_v, _ = gpu_advect(u, v, w, *args, variant)
+        assert_bitwise(got_v, oracle.advect(u, v, w, *args), (shape, variant))
 
 
 @pytest.mark.parametrize("shape", [(3, 120000, 64), (2, 60010, 128)])

@@ -29,9 +29,10 @@ def main():
     rng = np.random.default_rng(a.seed)
     bad, done = [], 0
     for n in range(a.cases):
-        nz = int(rng.choice([2, 3, 5, 8, 16, 31, 33, 63, 64, 65, 96, 99, 127, 128, 200, 257]))
+        nz = int(rng.choice([2, 3, 5, 8, 16, 31, 33, 63, 64, 65, 96, 99, 127, 128, 160, 200, 257,
+                              300, 514, 1030]))
         nx = int(rng.integers(1, 90))
-        ny = int(rng.integers(1, 400 if nz <= 64 else 120))
+        ny = int(rng.integers(1, 400 if nz <= 64 else (120 if nz <= 300 else 40)))
         seed = int(rng.integers(0, 2**31))
         u, v, w = oracle.fill_random(nx, ny, nz, seed, baseline=True)
         co = oracle.baseline_coefficients(seed, nz)
@@ -49,7 +50,9 @@ def main():
             kw["chunks"] = int(rng.integers(1, 9))
         if rng.random() < 0.3:
             kw["grid"] = int(rng.integers(1, 160))
-        variant = str(rng.choice(["xmarch", "xmarch_elem", "march", "simple"]))
+        variant = str(rng.choice(["xmarch", "xmarch_elem", "xmarch_ct", "march", "simple"]))
+        if variant == "xmarch_ct":  # tile_j selects the slab height (0: the planner's)
+            kw["tile_j"] = int(rng.choice([0, 6, 12, 24]))
         case = {"shape": [nx, ny, nz], "variant": variant, **kw}
         try:
             out = device.advect(*f, dco, opts=device.make_opts(variant, **kw))
