@@ -1156,18 +1156,25 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
     return fn;
 }
 
-// a field (nx+2, ny+2, nz) as a 3-D tensor {nz, ny+2, nx+2}; box {kt+4, tj+2, 1}
+// a field (nx+2, ny+2, nz): even nz as a 3-D tensor {nz, ny+2, nx+2}, box
+// {kt+4, tj+2, 1}; odd nz as a 2-D tensor of column-pair rows {2 nz,
+// (nx+2)(ny+2)/2}, box {kt+4, tj/2+2} (k_advect_ctile, ODD)
 static int encode_field_map(CUtensorMap *m, const double *f, const BoxLaunch &L, int kt, int tj)
 {
     PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
     if (!enc) return set_error(PWADV_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-    const cuuint64_t dims[3] = {(cuuint64_t)L.nz, (cuuint64_t)(L.ny + 2), (cuuint64_t)(L.nx + 2)};
-    const cuuint64_t strides[2] = {(cuuint64_t)L.nz * sizeof(double),
-                                   (cuuint64_t)((L.ny + 2) * L.nz) * sizeof(double)};
-    const cuuint32_t box[3] = {(cuuint32_t)(kt + 4), (cuuint32_t)(tj + 2), 1};
+    const bool odd = L.nz % 2 != 0;
+    const cuuint64_t dims3[3] = {(cuuint64_t)L.nz, (cuuint64_t)(L.ny + 2), (cuuint64_t)(L.nx + 2)};
+    const cuuint64_t dims2[2] = {(cuuint64_t)(2 * L.nz), (cuuint64_t)((L.nx + 2) * (L.ny + 2) / 2)};
+    const cuuint64_t strides3[2] = {(cuuint64_t)L.nz * sizeof(double),
+                                    (cuuint64_t)((L.ny + 2) * L.nz) * sizeof(double)};
+    const cuuint64_t strides2[1] = {(cuuint64_t)(2 * L.nz) * sizeof(double)};
+    const cuuint32_t box3[3] = {(cuuint32_t)(kt + 4), (cuuint32_t)(tj + 2), 1};
+    const cuuint32_t box2[2] = {(cuuint32_t)(kt + 4), (cuuint32_t)(tj / 2 + 2)};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(f), dims, strides,
-                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, odd ? 2 : 3, const_cast<double *>(f),
+                           odd ? dims2 : dims3, odd ? strides2 : strides3, odd ? box2 : box3, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_error(PWADV_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return PWADV_OK;
@@ -1183,13 +1190,16 @@ static int launch_ctile(const BoxLaunch &L, const BoxArgs &a, const TileCfg &t, 
     if (rc == PWADV_OK) rc = encode_field_map(&maps.w, L.w, L, plan.kt, plan.tj);
     if (rc != PWADV_OK) return rc;
     void (*kern)(BoxArgs, TileCfg, CtMaps) = nullptr;
-#define PWADV_PICK_CT(KT)                                                                     \
-    if (plan.kt == KT)                                                                        \
-        kern = L.step ? (fma ? k_advect_ctile<true, true, KT> : k_advect_ctile<false, true, KT>) \
-                      : (fma ? k_advect_ctile<true, false, KT> : k_advect_ctile<false, false, KT>);
-    PWADV_PICK_CT(32)
-    PWADV_PICK_CT(64)
-    PWADV_PICK_CT(128)
+#define PWADV_PICK_CT(KT, ODD)                                                                \
+    if (plan.kt == KT && odd == ODD)                                                          \
+        kern = L.step ? (fma ? k_advect_ctile<true, true, KT, ODD> : k_advect_ctile<false, true, KT, ODD>) \
+                      : (fma ? k_advect_ctile<true, false, KT, ODD> : k_advect_ctile<false, false, KT, ODD>);
+    const bool odd = L.nz % 2 != 0;
+    PWADV_PICK_CT(32, false)
+    PWADV_PICK_CT(64, false)
+    PWADV_PICK_CT(128, false)
+    PWADV_PICK_CT(64, true)
+    PWADV_PICK_CT(128, true)
 #undef PWADV_PICK_CT
     if (!kern) return set_error(PWADV_E_ARG, "unsupported slab height %d", plan.kt);
     const DeviceInfo *dev = device_info();
@@ -1544,6 +1554,7 @@ static int ctile_kt(int64_t nz)
     int kt = 128;
     double best = 0.0;
     for (int c : {128, 64, 32}) {
+        if (c < 64 && nz % 2) continue;  // odd nz: one column parity per warp
         const double pref = c == 128 ? 1.0 : (c == 64 ? 1.01 : 1.08);
         const double cost = (double)((nz + c - 1) / c * c) * pref;
         if (best == 0.0 || cost < best) {
@@ -1562,7 +1573,11 @@ static int ctile_kt(int64_t nz)
 // 23% idle slab levels); 160, 192, 256 and deeper: tiles.
 static bool ctile_pays(int64_t nz)
 {
-    if (nz % 2 != 0) return false;
+    // odd nz: the column-pair form (realigned odd columns, scalar stores on
+    // them) measured 80-95 Gpts/s against the UA form's 100-109 — it is the
+    // default only where the UA form does not run (nz > 767: 87-90 against
+    // K1m's 81-85)
+    if (nz % 2 != 0) return nz > 767;
     const int kt = ctile_kt(nz);
     const double pref = kt == 128 ? 1.0 : (kt == 64 ? 1.01 : 1.08);
     const double ct = 0.98 * (double)nz / (double)((nz + kt - 1) / kt * kt) / pref;
@@ -1574,15 +1589,14 @@ static bool ctile_pays(int64_t nz)
     return ct > whole;
 }
 
-// Column-tile plan (k_advect_ctile). Applies to 16-byte-aligned fields with
-// even nz (tensor-map strides), without the fused halo pull / push, at the
-// 512-thread budget. Slab height KT from opts.tile_j (768 / tile_j) or the default below.
+// Column-tile plan (k_advect_ctile). Applies to 16-byte-aligned fields,
+// without the fused halo pull / push, at the 512-thread budget. Slab height KT from opts.tile_j (768 / tile_j) or the default below.
 static bool plan_ctile(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
 {
     const int64_t nz = L.nz;
     const uintptr_t al = (uintptr_t)L.u | (uintptr_t)L.v | (uintptr_t)L.w | (uintptr_t)L.o0 |
                          (uintptr_t)L.o1 | (uintptr_t)L.o2;
-    if ((al & 15) || nz % 2 != 0 || L.peers || L.pull ||
+    if ((al & 15) || L.peers || L.pull ||
         (L.max_threads > 0 && L.max_threads != 512) ||
         (L.flags & (PWADV_FLAG_DEBUG_NO_COMPUTE | PWADV_FLAG_DEBUG_NO_STORE | PWADV_FLAG_UNALIGNED |
                     PWADV_FLAG_GENERIC)))
@@ -1592,10 +1606,19 @@ static bool plan_ctile(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
         if (L.tile_j != 6 && L.tile_j != 12 && L.tile_j != 24) return false;
         kt = 768 / L.tile_j;
     }
+    // odd nz: one column parity per warp (KT >= 64) for the warp-uniform
+    // realignment of odd columns' pairs
+    if (nz % 2 && kt < 64) {
+        if (L.tile_j > 0) return false;
+        kt = 64;
+    }
     const int tj = 768 / kt;
     const int64_t nby = L.y1 - L.y0;
     const int64_t nslab = (nz + kt - 1) / kt;
-    const size_t stage_bytes = (size_t)3 * (((tj + 2) * (kt + 4) + 15) / 16 * 16) * sizeof(double);
+    // CtLayout::CS: even nz (tj+2) column slots, odd nz two halves of tj/2+2
+    const int half = ((tj / 2 + 2) * (kt + 4) + 15) / 16 * 16;
+    const int box = nz % 2 ? half + (tj / 2 + 2) * (kt + 4) : (tj + 2) * (kt + 4);
+    const size_t stage_bytes = (size_t)3 * ((box + 15) / 16 * 16) * sizeof(double);
     const size_t bar_bytes = 2 * 16 * sizeof(uint64_t) + sizeof(RingState);
     const size_t smem_cap = (size_t)dev.smem_optin - bar_bytes - 1024;
     int smax = (int)(smem_cap / stage_bytes);

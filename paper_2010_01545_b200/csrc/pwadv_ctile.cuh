@@ -21,25 +21,37 @@
 // fill and store nothing. Arithmetic, operand wiring and the x-carried sums
 // are k_advect_xmarch's (bit-exact with kernel.py:73-185).
 //
-// Requirements (plan_ctile): even nz (the tensor map's column stride nz * 8
-// must be a multiple of 16 bytes), 16-byte-aligned fields, no halo pull /
-// push. Odd nz stays on the X-march's UA form.
+// Odd nz (ODD): the column stride nz * 8 is not a 16-byte multiple, so the
+// field is mapped as rows of column pairs instead (see k_advect_ctile).
+//
+// Requirements (plan_ctile): 16-byte-aligned fields, no halo pull / push.
 
 #include <cuda.h>
 
+#ifndef PWADV_CT_DBG
+#define PWADV_CT_DBG 0  // debug builds only (tools/build_variant.py): 1 = odd nz loads one half, 2 = no stores
+#endif
+
 namespace pwadv {
 
-template <int KT>
+template <int KT, bool ODD>
 struct CtLayout {
     static constexpr int KP = KT / 2;       // threads per column slab
     static constexpr int TJ = 384 / KP;     // columns per strip
     static constexpr int CW = KT + 4;       // doubles per staged column (slot)
     static constexpr int NC = TJ + 2;       // staged columns per field
-    static constexpr int CS = (NC * CW + 15) / 16 * 16;  // doubles per field slot (128-byte multiple)
-    static_assert(KT % 2 == 0 && 384 % KP == 0 && NC <= 64, "column-tile layout");
+    // odd nz: column-pair rows, even and odd global columns in two halves
+    static constexpr int NP = TJ / 2 + 2;   // pair rows per box (covers NC columns at any phase)
+    static constexpr int HALF = (NP * CW + 15) / 16 * 16;  // second half's offset (128-byte aligned:
+                                                           // a tensor copy's destination must be)
+    static constexpr int BOX = ODD ? 2 * NP * CW : NC * CW;  // doubles a field's plane tile delivers
+    static constexpr int SPAN = ODD ? HALF + NP * CW : NC * CW;
+    static constexpr int CS = (SPAN + 15) / 16 * 16;  // doubles per field slot (128-byte multiple)
+    static_assert(KT % 2 == 0 && 384 % KP == 0 && NC <= 64 && TJ % 2 == 0, "column-tile layout");
 };
 
-// the three fields' tensor maps (dims {nz, ny+2, nx+2}, box {KT+4, TJ+2, 1})
+// the three fields' tensor maps: even nz dims {nz, ny+2, nx+2}, box {KT+4,
+// TJ+2, 1}; odd nz (column-pair rows) dims {2 nz, (nx+2)(ny+2)/2}, box {KT+4, NP}
 struct CtMaps {
     CUtensorMap u, v, w;
 };
@@ -55,13 +67,43 @@ __device__ __forceinline__ void tma_load_3d(void *dst_smem, const CUtensorMap *m
         : "memory");
 }
 
-template <bool FMA, bool STEP, int KT>
+__device__ __forceinline__ void tma_load_2d(void *dst_smem, const CUtensorMap *map, int c0, int c1,
+                                            uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_u32(dst_smem)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ODD (odd nz): a field is viewed as rows of column PAIRS — global columns
+// g = i*(ny+2) + j, row g/2 holding columns 2r and 2r+1, 2 nz levels, a
+// 16-byte-multiple row stride — and a plane tile is two boxes per field of NP
+// pair rows from row G0/2 (G0 = the tile's first global column), landing in
+// two halves of the slot: the even columns' levels [kb-2, kb+KT+2) (inner
+// start kb - 2) and the odd columns' levels [kb-3, kb+KT+1) (inner start
+// nz + kb - 3: a box row must start on a 16-byte boundary, so an odd column's
+// staged copy sits one level higher in its slot). A tile column's half and row
+// follow from the parity of G0, which flips from plane to plane when ny+2 is
+// odd, so the consumers select their column offsets per plane. Every thread
+// keeps its pair at even levels (kb + 2 kp); a pair of an odd column is read
+// as the 16-byte-aligned (k0-1, k0) and realigned in registers, k0+1 from the
+// next lane by one shuffle (slot edge: from the slot) — the branch is warp-
+// uniform because one column parity owns a warp (KT >= 64, plan_ctile). In
+// global memory a pair is 16-byte aligned on even global columns only (g nz +
+// k0 even) — odd columns store scalars — and the top level nz - 1 is the first
+// of its pair. Levels a box reads past its column (the other column of the
+// pair, or the zero fill) feed only operands of levels that are not stored,
+// the zeroed level 0, or the top formula's unread k+1.
+template <bool FMA, bool STEP, int KT, bool ODD>
 __global__ void __launch_bounds__(512, 1)
     k_advect_ctile(const __grid_constant__ BoxArgs a, const __grid_constant__ TileCfg t,
                    const __grid_constant__ CtMaps maps)
 {
-    using Lay = CtLayout<KT>;
-    constexpr int KP = Lay::KP, TJ = Lay::TJ, CW = Lay::CW, CS = Lay::CS;
+    using Lay = CtLayout<KT, ODD>;
+    constexpr int KP = Lay::KP, TJ = Lay::TJ, CW = Lay::CW, CS = Lay::CS, HALF = Lay::HALF;
     constexpr int kComputeWarps = 12;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -120,8 +162,12 @@ __global__ void __launch_bounds__(512, 1)
 
     if (tid >= 32 * kComputeWarps) {  // producer warpgroup: warp 12 issues, 13-15 idle
         asm volatile("setmaxnreg.dec.sync.aligned.u32 32;\n" ::: "memory");
-        if (tid == 32 * kComputeWarps) {  // one thread: three boxes per plane
-            constexpr uint32_t kBox = (uint32_t)(Lay::NC * CW * sizeof(double));
+        if (tid == 32 * kComputeWarps) {  // one thread: three (odd nz: six) boxes per plane
+#if PWADV_CT_DBG & 1
+            constexpr uint32_t kBox = (uint32_t)((ODD ? Lay::BOX / 2 : Lay::BOX) * sizeof(double));
+#else
+            constexpr uint32_t kBox = (uint32_t)(Lay::BOX * sizeof(double));
+#endif
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.u)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.v)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.w)) : "memory");
@@ -135,9 +181,24 @@ __global__ void __launch_bounds__(512, 1)
                 const int jl = rs->uj0[k] - 1, kl = rs->dsto[k] - 2;
                 double *dst = ring + (size_t)st * 3 * CS;
                 mbar_arrive_expect_tx(&full[st], 3 * kBox);
-                tma_load_3d(dst, &maps.u, kl, jl, i, &full[st]);
-                tma_load_3d(dst + CS, &maps.v, kl, jl, i, &full[st]);
-                tma_load_3d(dst + 2 * CS, &maps.w, kl, jl, i, &full[st]);
+                if constexpr (ODD) {
+                    const int r0 = (int)(((int64_t)i * ny2 + jl) >> 1);
+                    const int ko = (int)nz + kl - 1;  // even: 16-byte-aligned box rows
+                    tma_load_2d(dst, &maps.u, kl, r0, &full[st]);
+                    tma_load_2d(dst + CS, &maps.v, kl, r0, &full[st]);
+                    tma_load_2d(dst + 2 * CS, &maps.w, kl, r0, &full[st]);
+#if PWADV_CT_DBG & 1
+                    (void)ko;
+#else
+                    tma_load_2d(dst + HALF, &maps.u, ko, r0, &full[st]);
+                    tma_load_2d(dst + CS + HALF, &maps.v, ko, r0, &full[st]);
+                    tma_load_2d(dst + 2 * CS + HALF, &maps.w, ko, r0, &full[st]);
+#endif
+                } else {
+                    tma_load_3d(dst, &maps.u, kl, jl, i, &full[st]);
+                    tma_load_3d(dst + CS, &maps.v, kl, jl, i, &full[st]);
+                    tma_load_3d(dst + 2 * CS, &maps.w, kl, jl, i, &full[st]);
+                }
             }
         }
         return;
@@ -146,7 +207,20 @@ __global__ void __launch_bounds__(512, 1)
 
     int cseq = 0, cst = 0;
     uint32_t cph = 0;
-    const int toff = tc * CW + s0;
+    // column offsets (doubles) of the thread's column and its j -+ 1
+    // neighbours in a staged plane whose first global column has parity pg
+    auto coff = [&](int pg, int dy) -> int {
+        if constexpr (ODD) {
+            const int x = pg + tc + dy;
+            return (x & 1) * HALF + (x >> 1) * CW;
+        } else {
+            (void)pg;
+            return (tc + dy) * CW;
+        }
+    };
+    const int e_m = coff(0, -1), e_z = coff(0, 0), e_p = coff(0, 1);
+    const int o_m = coff(1, -1), o_z = coff(1, 0), o_p = coff(1, 1);
+    const int podd = ODD ? (int)(ny2 & 1) : 0;  // G0's parity flips from plane to plane
     auto release = [&](int st) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);
@@ -162,18 +236,25 @@ __global__ void __launch_bounds__(512, 1)
             cph ^= 1u;
         }
     };
-    auto P = [&](const double *pl, int f, int dy) -> double2 {
-        return *reinterpret_cast<const double2 *>(pl + f * CS + dy * CW + toff);
+    // pl: a staged plane advanced to the column's slot; f: field; q: the
+    // column is an odd global column (ODD only; warp-uniform), its copy one
+    // level higher in the slot: the pair is realigned from (k0-1, k0)
+    auto P = [&](const double *pl, int f, int q) -> double2 {
+        const double2 x = *reinterpret_cast<const double2 *>(pl + f * CS + s0);
+        if (!ODD || !q) return x;
+        double d = __shfl_down_sync(0xffffffffu, x.x, 1);
+        if (fixQ) d = pl[f * CS + s0 + 2];
+        return make_double2(x.y, d);
     };
     // k0-1 / k0+2 of the pair: the neighbouring lane's value, or the slot's
-    auto M = [&](double2 p, const double *pl, int f, int dy) -> double {
+    auto M = [&](double2 p, const double *pl, int f, int q) -> double {
         double m = __shfl_up_sync(0xffffffffu, p.y, 1);
-        if (fixM) m = pl[f * CS + dy * CW + toff - 1];
+        if (fixM) m = pl[f * CS + s0 - 1 + q];
         return m;
     };
-    auto Q = [&](double2 p, const double *pl, int f, int dy) -> double {
+    auto Q = [&](double2 p, const double *pl, int f, int q) -> double {
         double v = __shfl_down_sync(0xffffffffu, p.x, 1);
-        if (fixQ) v = pl[f * CS + dy * CW + toff + 2];
+        if (fixQ) v = pl[f * CS + s0 + 2 + q];
         return v;
     };
 
@@ -186,23 +267,28 @@ __global__ void __launch_bounds__(512, 1)
         const int64_t ie = ib + (rs->first[k + 1] - rs->first[k]) - 2;
         const int64_t j0 = rs->uj0[k];
         const bool active = c < rs->utj[k];
-        // this thread's levels in this slab (nz even: a pair is in or out whole)
+        // this thread's levels in this slab (even nz: a pair is in or out
+        // whole, the top is a pair's second level; odd nz: its first)
         const int64_t k0 = (int64_t)rs->dsto[k] + 2 * kp;
-        const bool va = k0 < nz;
-        const bool top_b = k0 + 1 == nz - 1;
+        const bool va = k0 < nz, vb = k0 + 1 < nz;
+        const bool top_a = ODD && k0 == nz - 1, top_b = !ODD && k0 + 1 == nz - 1;
         const bool z_a = k0 == 0;
-        const int64_t kia = k0 < nz ? k0 : nz - 2;  // coefficient levels (clamped)
-        const int64_t kib = kia + 1;
+        const int64_t kia = k0 < nz ? k0 : nz - 1;  // coefficient levels (clamped)
+        const int64_t kib = k0 + 1 < nz ? k0 + 1 : nz - 1;
+        // parity of the first global column of plane ib-1's tile
+        int pg = ODD ? (int)((((ib - 1) * ny2) + (j0 - 1)) & 1) : 0;
         const double c1a = __ldg(a.tzc1 + kia), c1b = __ldg(a.tzc1 + kib);
         const double c2a = __ldg(a.tzc2 + kia), c2b = __ldg(a.tzc2 + kib);
 
         {  // plane ib-1 -> slot 2
             const double *pl = wait_next();
-            U0[2] = P(pl, 0, 0);
-            const double2 u1 = P(pl, 0, 1);
-            V0[2] = P(pl, 1, 0);
-            W0[2] = P(pl, 2, 0);
-            const double u0M = M(U0[2], pl, 0, 0);
+            const double *pz = pl + (pg ? o_z : e_z), *pp = pl + (pg ? o_p : e_p);
+            const int qz = ODD ? (pg + tc) & 1 : 0, qn = qz ^ (int)ODD;  // odd column / its neighbours
+            U0[2] = P(pz, 0, qz);
+            const double2 u1 = P(pp, 0, qn);
+            V0[2] = P(pz, 1, qz);
+            W0[2] = P(pz, 2, qz);
+            const double u0M = M(U0[2], pz, 0, qz);
             release(cst);
             advance();
             txu_a = __dadd_rn(U0[2].x, u1.x);
@@ -211,13 +297,16 @@ __global__ void __launch_bounds__(512, 1)
             rxu_b = __dadd_rn(U0[2].x, U0[2].y);
         }
         int pst = cst;
+        pg ^= podd;
         {  // plane ib -> slot 0
             const double *pl = wait_next();
-            U0[0] = P(pl, 0, 0);
-            V0[0] = P(pl, 1, 0);
-            W0[0] = P(pl, 2, 0);
-            VM[0] = P(pl, 1, -1);
-            W0M[0] = M(W0[0], pl, 2, 0);
+            const double *pz = pl + (pg ? o_z : e_z), *pm = pl + (pg ? o_m : e_m);
+            const int qz = ODD ? (pg + tc) & 1 : 0, qn = qz ^ (int)ODD;
+            U0[0] = P(pz, 0, qz);
+            V0[0] = P(pz, 1, qz);
+            W0[0] = P(pz, 2, qz);
+            VM[0] = P(pm, 1, qn);
+            W0M[0] = M(W0[0], pz, 2, qz);
             advance();
             sxu_a = __dadd_rn(U0[0].x, U0[2].x);
             sxu_b = __dadd_rn(U0[0].y, U0[2].y);
@@ -235,20 +324,26 @@ __global__ void __launch_bounds__(512, 1)
             const int lst = cst;
             const double *L = wait_next();                       // plane i+1
             const double *C = ring + (size_t)pst * 3 * CS;      // plane i
-            U0[rp] = P(L, 0, 0);
-            V0[rp] = P(L, 1, 0);
-            W0[rp] = P(L, 2, 0);
-            VM[rp] = P(L, 1, -1);
-            W0M[rp] = M(W0[rp], L, 2, 0);
-            const double2 u1c = P(C, 0, 1);
-            const double2 umc = P(C, 0, -1), v1c = P(C, 1, 1), w1c = P(C, 2, 1), wmc = P(C, 2, -1);
-            const double w1cM = M(w1c, C, 2, 1);
-            const double u0cM = M(U0[r], C, 0, 0);
-            const double u0cQ = Q(U0[r], C, 0, 0);
-            const double v0cM = M(V0[r], C, 1, 0);
-            const double v0cQ = Q(V0[r], C, 1, 0);
-            const double w0cQ = Q(W0[r], C, 2, 0);
-            const double vmcM = M(VM[r], C, 1, -1);
+            const int pgl = pg ^ podd;
+            const double *Lz = L + (pgl ? o_z : e_z), *Lm = L + (pgl ? o_m : e_m);
+            const double *Cz = C + (pg ? o_z : e_z), *Cm = C + (pg ? o_m : e_m);
+            const double *Cp = C + (pg ? o_p : e_p);
+            const int lq = ODD ? (pgl + tc) & 1 : 0, lqn = lq ^ (int)ODD;  // plane i+1
+            const int cq = ODD ? (pg + tc) & 1 : 0, cqn = cq ^ (int)ODD;    // plane i
+            U0[rp] = P(Lz, 0, lq);
+            V0[rp] = P(Lz, 1, lq);
+            W0[rp] = P(Lz, 2, lq);
+            VM[rp] = P(Lm, 1, lqn);
+            W0M[rp] = M(W0[rp], Lz, 2, lq);
+            const double2 u1c = P(Cp, 0, cqn);
+            const double2 umc = P(Cm, 0, cqn), v1c = P(Cp, 1, cqn), w1c = P(Cp, 2, cqn), wmc = P(Cm, 2, cqn);
+            const double w1cM = M(w1c, Cp, 2, cqn);
+            const double u0cM = M(U0[r], Cz, 0, cq);
+            const double u0cQ = Q(U0[r], Cz, 0, cq);
+            const double v0cM = M(V0[r], Cz, 1, cq);
+            const double v0cQ = Q(V0[r], Cz, 1, cq);
+            const double w0cQ = Q(W0[r], Cz, 2, cq);
+            const double vmcM = M(VM[r], Cm, 1, cqn);
             release(pst);  // plane i fully consumed by this warp
 
             const double2 u0m = U0[rm], u0c = U0[r], u0p = U0[rp];
@@ -267,13 +362,13 @@ __global__ void __launch_bounds__(512, 1)
             // the operand wiring of kernel.py:117-128, as k_advect_xmarch
             double su_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, u0m.x, sxu_a, u0p.x, nsxu_a,
                                        umc.x, __dadd_rn(vmc.x, vmp.x), u1c.x, __dadd_rn(v0c.x, v0p.x),
-                                       u0cM, __dadd_rn(w0cM, w0pM), u0c.y, szu, false);
+                                       u0cM, __dadd_rn(w0cM, w0pM), u0c.y, szu, top_a);
             double sv_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, v0m.x, txu_a, v0p.x, ntxu_a,
                                        vmc.x, __dadd_rn(v0c.x, vmc.x), v1c.x, __dadd_rn(v0c.x, v1c.x),
-                                       v0cM, __dadd_rn(w0cM, w1cM), v0c.y, szv, false);
+                                       v0cM, __dadd_rn(w0cM, w1cM), v0c.y, szv, top_a);
             double sw_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, w0m.x, rxu_a, w0p.x, nrxu_a,
                                        wmc.x, __dadd_rn(vmcM, vmc.x), w1c.x, __dadd_rn(v0cM, v0c.x),
-                                       w0cM, __dadd_rn(w0c.x, w0cM), w0c.y, szw, false);
+                                       w0cM, __dadd_rn(w0c.x, w0cM), w0c.y, szw, top_a);
             double su_b = pw_sums<FMA>(tcx, tcy, c1b, c2b, u0m.y, sxu_b, u0p.y, nsxu_b,
                                        umc.y, __dadd_rn(vmc.y, vmp.y), u1c.y, __dadd_rn(v0c.y, v0p.y),
                                        u0c.x, szu, u0cQ, __dadd_rn(w0c.y, w0p.y), top_b);
@@ -298,15 +393,27 @@ __global__ void __launch_bounds__(512, 1)
                 sw_a = fwd_update(w0c.x, dt, sw_a);
                 sw_b = fwd_update(w0c.y, dt, sw_b);
             }
-            if (active && va) {
-                store2(o0, su_a, su_b);
-                store2(o1, sv_a, sv_b);
-                store2(o2, sw_a, sw_b);
+            if (active && va && !(PWADV_CT_DBG & 2)) {
+                if (!ODD || (vb && ((pg + tc) & 1) == 0)) {  // on the 16-byte grid
+                    store2(o0, su_a, su_b);
+                    store2(o1, sv_a, sv_b);
+                    store2(o2, sw_a, sw_b);
+                } else {  // odd nz: odd global column, or the top (a pair's first level)
+                    __stcs(o0, su_a);
+                    __stcs(o1, sv_a);
+                    __stcs(o2, sw_a);
+                    if (vb) {
+                        __stcs(o0 + 1, su_b);
+                        __stcs(o1 + 1, sv_b);
+                        __stcs(o2 + 1, sw_b);
+                    }
+                }
             }
             o0 += ostep;
             o1 += ostep;
             o2 += ostep;
             pst = lst;
+            pg = pgl;
             advance();
         };
 
