@@ -1574,10 +1574,11 @@ static int ctile_kt(int64_t nz)
 static bool ctile_pays(int64_t nz)
 {
     // odd nz: the column-pair form (realigned odd columns, scalar stores on
-    // them) measured 80-95 Gpts/s against the UA form's 100-109 — it is the
-    // default only where the UA form does not run (nz > 767: 87-90 against
-    // K1m's 81-85)
-    if (nz % 2 != 0) return nz > 767;
+    // them) measured 80-95 Gpts/s against the UA form's 100-109 while the UA
+    // strips are >= 2 columns wide — it is the default once they shrink to one
+    // (nz > 383: 95.6 vs 91.2 at nz 511) and where the UA form does not run
+    // (nz > 767: 87-90 against K1m's 81-85)
+    if (nz % 2 != 0) return nz > 383;
     const int kt = ctile_kt(nz);
     const double pref = kt == 128 ? 1.0 : (kt == 64 ? 1.01 : 1.08);
     const double ct = 0.98 * (double)nz / (double)((nz + kt - 1) / kt * kt) / pref;
