@@ -1573,12 +1573,12 @@ static int ctile_kt(int64_t nz)
 // 23% idle slab levels); 160, 192, 256 and deeper: tiles.
 static bool ctile_pays(int64_t nz)
 {
-    // odd nz: the column-pair form (realigned odd columns, scalar stores on
-    // them) measured 80-95 Gpts/s against the UA form's 100-109 while the UA
-    // strips are >= 2 columns wide — it is the default once they shrink to one
-    // (nz > 383: 95.6 vs 91.2 at nz 511) and where the UA form does not run
-    // (nz > 767: 87-90 against K1m's 81-85)
-    if (nz % 2 != 0) return nz > 383;
+    // odd nz: the column-pair form (odd columns read with 8-byte loads and
+    // stored as scalars) against the UA form (every pair so): 101-105 vs
+    // 104-111 Gpts/s at nz 63-191, even at 255 (108 vs 107), ahead from
+    // there as the UA strips narrow (113 vs 107 at 512x512x255, 114 vs 88 at
+    // nz 511) and against K1m above 767 (104-106 vs 82-85)
+    if (nz % 2 != 0) return nz >= 255;
     const int kt = ctile_kt(nz);
     const double pref = kt == 128 ? 1.0 : (kt == 64 ? 1.01 : 1.08);
     const double ct = 0.98 * (double)nz / (double)((nz + kt - 1) / kt * kt) / pref;

@@ -28,6 +28,10 @@
 
 #include <cuda.h>
 
+#ifndef PWADV_CT_REALIGN_LDS
+#define PWADV_CT_REALIGN_LDS 1  // odd columns (odd nz): two 8-byte shared loads (default; 0 = the
+                                // 16-byte load + shuffle: 5-15% slower, profiles/r02_ct_odd_nz.jsonl)
+#endif
 #ifndef PWADV_CT_DBG
 #define PWADV_CT_DBG 0  // debug builds only (tools/build_variant.py): 1 = odd nz loads one half, 2 = no stores
 #endif
@@ -88,10 +92,11 @@ __device__ __forceinline__ void tma_load_2d(void *dst_smem, const CUtensorMap *m
 // staged copy sits one level higher in its slot). A tile column's half and row
 // follow from the parity of G0, which flips from plane to plane when ny+2 is
 // odd, so the consumers select their column offsets per plane. Every thread
-// keeps its pair at even levels (kb + 2 kp); a pair of an odd column is read
-// as the 16-byte-aligned (k0-1, k0) and realigned in registers, k0+1 from the
-// next lane by one shuffle (slot edge: from the slot) — the branch is warp-
-// uniform because one column parity owns a warp (KT >= 64, plan_ctile). In
+// keeps its pair at even levels (kb + 2 kp); a pair of an odd column is off
+// the 16-byte grid in its slot and is read with two 8-byte loads (measured
+// faster than the aligned (k0-1, k0) realigned by a shuffle) — the choice is
+// warp-uniform because one column parity owns a warp (KT >= 64, plan_ctile),
+// and compile-time per unit when ny+2 is even (run_unit's QV). In
 // global memory a pair is 16-byte aligned on even global columns only (g nz +
 // k0 even) — odd columns store scalars — and the top level nz - 1 is the first
 // of its pair. Levels a box reads past its column (the other column of the
@@ -240,6 +245,9 @@ __global__ void __launch_bounds__(512, 1)
     // column is an odd global column (ODD only; warp-uniform), its copy one
     // level higher in the slot: the pair is realigned from (k0-1, k0)
     auto P = [&](const double *pl, int f, int q) -> double2 {
+#if PWADV_CT_REALIGN_LDS
+        if (ODD && q) return make_double2(pl[f * CS + s0 + 1], pl[f * CS + s0 + 2]);
+#endif
         const double2 x = *reinterpret_cast<const double2 *>(pl + f * CS + s0);
         if (!ODD || !q) return x;
         double d = __shfl_down_sync(0xffffffffu, x.x, 1);
@@ -280,158 +288,187 @@ __global__ void __launch_bounds__(512, 1)
         const double c1a = __ldg(a.tzc1 + kia), c1b = __ldg(a.tzc1 + kib);
         const double c2a = __ldg(a.tzc2 + kia), c2b = __ldg(a.tzc2 + kib);
 
-        {  // plane ib-1 -> slot 2
-            const double *pl = wait_next();
-            const double *pz = pl + (pg ? o_z : e_z), *pp = pl + (pg ? o_p : e_p);
-            const int qz = ODD ? (pg + tc) & 1 : 0, qn = qz ^ (int)ODD;  // odd column / its neighbours
-            U0[2] = P(pz, 0, qz);
-            const double2 u1 = P(pp, 0, qn);
-            V0[2] = P(pz, 1, qz);
-            W0[2] = P(pz, 2, qz);
-            const double u0M = M(U0[2], pz, 0, qz);
-            release(cst);
-            advance();
-            txu_a = __dadd_rn(U0[2].x, u1.x);
-            txu_b = __dadd_rn(U0[2].y, u1.y);
-            rxu_a = __dadd_rn(u0M, U0[2].x);
-            rxu_b = __dadd_rn(U0[2].x, U0[2].y);
-        }
-        int pst = cst;
-        pg ^= podd;
-        {  // plane ib -> slot 0
-            const double *pl = wait_next();
-            const double *pz = pl + (pg ? o_z : e_z), *pm = pl + (pg ? o_m : e_m);
-            const int qz = ODD ? (pg + tc) & 1 : 0, qn = qz ^ (int)ODD;
-            U0[0] = P(pz, 0, qz);
-            V0[0] = P(pz, 1, qz);
-            W0[0] = P(pz, 2, qz);
-            VM[0] = P(pm, 1, qn);
-            W0M[0] = M(W0[0], pz, 2, qz);
-            advance();
-            sxu_a = __dadd_rn(U0[0].x, U0[2].x);
-            sxu_b = __dadd_rn(U0[0].y, U0[2].y);
-        }
-
-        const int64_t obase = (ib * ny2 + (j0 + c)) * nz + k0;
-        double *o0 = a.o0 + obase;
-        double *o1 = a.o1 + obase;
-        double *o2 = a.o2 + obase;
-        const int64_t ostep = ny2 * nz;
-
-        auto body = [&](auto R) {
-            constexpr int r = decltype(R)::value;
-            constexpr int rm = (r + 2) % 3, rp = (r + 1) % 3;
-            const int lst = cst;
-            const double *L = wait_next();                       // plane i+1
-            const double *C = ring + (size_t)pst * 3 * CS;      // plane i
-            const int pgl = pg ^ podd;
-            const double *Lz = L + (pgl ? o_z : e_z), *Lm = L + (pgl ? o_m : e_m);
-            const double *Cz = C + (pg ? o_z : e_z), *Cm = C + (pg ? o_m : e_m);
-            const double *Cp = C + (pg ? o_p : e_p);
-            const int lq = ODD ? (pgl + tc) & 1 : 0, lqn = lq ^ (int)ODD;  // plane i+1
-            const int cq = ODD ? (pg + tc) & 1 : 0, cqn = cq ^ (int)ODD;    // plane i
-            U0[rp] = P(Lz, 0, lq);
-            V0[rp] = P(Lz, 1, lq);
-            W0[rp] = P(Lz, 2, lq);
-            VM[rp] = P(Lm, 1, lqn);
-            W0M[rp] = M(W0[rp], Lz, 2, lq);
-            const double2 u1c = P(Cp, 0, cqn);
-            const double2 umc = P(Cm, 0, cqn), v1c = P(Cp, 1, cqn), w1c = P(Cp, 2, cqn), wmc = P(Cm, 2, cqn);
-            const double w1cM = M(w1c, Cp, 2, cqn);
-            const double u0cM = M(U0[r], Cz, 0, cq);
-            const double u0cQ = Q(U0[r], Cz, 0, cq);
-            const double v0cM = M(V0[r], Cz, 1, cq);
-            const double v0cQ = Q(V0[r], Cz, 1, cq);
-            const double w0cQ = Q(W0[r], Cz, 2, cq);
-            const double vmcM = M(VM[r], Cm, 1, cqn);
-            release(pst);  // plane i fully consumed by this warp
-
-            const double2 u0m = U0[rm], u0c = U0[r], u0p = U0[rp];
-            const double2 v0m = V0[rm], v0c = V0[r], v0p = V0[rp];
-            const double2 w0m = W0[rm], w0c = W0[r], w0p = W0[rp];
-            const double2 vmc = VM[r], vmp = VM[rp];
-            const double w0cM = W0M[r], w0pM = W0M[rp];
-
-            const double nsxu_a = __dadd_rn(u0c.x, u0p.x), nsxu_b = __dadd_rn(u0c.y, u0p.y);
-            const double ntxu_a = __dadd_rn(u0c.x, u1c.x), ntxu_b = __dadd_rn(u0c.y, u1c.y);
-            const double nrxu_a = __dadd_rn(u0cM, u0c.x), nrxu_b = __dadd_rn(u0c.x, u0c.y);
-            const double szu = __dadd_rn(w0c.x, w0p.x);
-            const double szv = __dadd_rn(w0c.x, w1c.x);
-            const double szw = __dadd_rn(w0c.x, w0c.y);
-
-            // the operand wiring of kernel.py:117-128, as k_advect_xmarch
-            double su_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, u0m.x, sxu_a, u0p.x, nsxu_a,
-                                       umc.x, __dadd_rn(vmc.x, vmp.x), u1c.x, __dadd_rn(v0c.x, v0p.x),
-                                       u0cM, __dadd_rn(w0cM, w0pM), u0c.y, szu, top_a);
-            double sv_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, v0m.x, txu_a, v0p.x, ntxu_a,
-                                       vmc.x, __dadd_rn(v0c.x, vmc.x), v1c.x, __dadd_rn(v0c.x, v1c.x),
-                                       v0cM, __dadd_rn(w0cM, w1cM), v0c.y, szv, top_a);
-            double sw_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, w0m.x, rxu_a, w0p.x, nrxu_a,
-                                       wmc.x, __dadd_rn(vmcM, vmc.x), w1c.x, __dadd_rn(v0cM, v0c.x),
-                                       w0cM, __dadd_rn(w0c.x, w0cM), w0c.y, szw, top_a);
-            double su_b = pw_sums<FMA>(tcx, tcy, c1b, c2b, u0m.y, sxu_b, u0p.y, nsxu_b,
-                                       umc.y, __dadd_rn(vmc.y, vmp.y), u1c.y, __dadd_rn(v0c.y, v0p.y),
-                                       u0c.x, szu, u0cQ, __dadd_rn(w0c.y, w0p.y), top_b);
-            double sv_b = pw_sums<FMA>(tcx, tcy, c1b, c2b, v0m.y, txu_b, v0p.y, ntxu_b,
-                                       vmc.y, __dadd_rn(v0c.y, vmc.y), v1c.y, __dadd_rn(v0c.y, v1c.y),
-                                       v0c.x, szv, v0cQ, __dadd_rn(w0c.y, w1c.y), top_b);
-            double sw_b = pw_sums<FMA>(tcx, tcy, c1b, c2b, w0m.y, rxu_b, w0p.y, nrxu_b,
-                                       wmc.y, __dadd_rn(vmc.x, vmc.y), w1c.y, __dadd_rn(v0c.x, v0c.y),
-                                       w0c.x, szw, w0cQ, __dadd_rn(w0c.y, w0cQ), top_b);
-            sxu_a = nsxu_a;
-            sxu_b = nsxu_b;
-            txu_a = ntxu_a;
-            txu_b = ntxu_b;
-            rxu_a = nrxu_a;
-            rxu_b = nrxu_b;
-            if (z_a) su_a = sv_a = sw_a = 0.0;
-            if constexpr (STEP) {
-                su_a = fwd_update(u0c.x, dt, su_a);
-                su_b = fwd_update(u0c.y, dt, su_b);
-                sv_a = fwd_update(v0c.x, dt, sv_a);
-                sv_b = fwd_update(v0c.y, dt, sv_b);
-                sw_a = fwd_update(w0c.x, dt, sw_a);
-                sw_b = fwd_update(w0c.y, dt, sw_b);
+        // the unit's steps, specialised on the parity of the thread's global
+        // column (odd nz): QV 0 / 1 when it is the same on every plane of the
+        // unit (ny+2 even; warp-uniform), 2 when it alternates from plane to
+        // plane, -1 for even nz — so the realignment and store choices of the
+        // common cases are compile-time
+        auto run_unit = [&](auto QVC) {
+            constexpr int QV = decltype(QVC)::value;
+            const int pflip = QV == 2 ? podd : 0;
+            auto qof = [&](int pgx) -> int {
+                if constexpr (QV < 0) {
+                    (void)pgx;
+                    return 0;
+                } else if constexpr (QV < 2) {
+                    (void)pgx;
+                    return QV;
+                } else {
+                    return (pgx + tc) & 1;
+                }
+            };
+            {  // plane ib-1 -> slot 2
+                const double *pl = wait_next();
+                const double *pz = pl + (pg ? o_z : e_z), *pp = pl + (pg ? o_p : e_p);
+                const int qz = qof(pg), qn = qz ^ (int)ODD;  // odd column / its neighbours
+                U0[2] = P(pz, 0, qz);
+                const double2 u1 = P(pp, 0, qn);
+                V0[2] = P(pz, 1, qz);
+                W0[2] = P(pz, 2, qz);
+                const double u0M = M(U0[2], pz, 0, qz);
+                release(cst);
+                advance();
+                txu_a = __dadd_rn(U0[2].x, u1.x);
+                txu_b = __dadd_rn(U0[2].y, u1.y);
+                rxu_a = __dadd_rn(u0M, U0[2].x);
+                rxu_b = __dadd_rn(U0[2].x, U0[2].y);
             }
-            if (active && va && !(PWADV_CT_DBG & 2)) {
-                if (!ODD || (vb && ((pg + tc) & 1) == 0)) {  // on the 16-byte grid
-                    store2(o0, su_a, su_b);
-                    store2(o1, sv_a, sv_b);
-                    store2(o2, sw_a, sw_b);
-                } else {  // odd nz: odd global column, or the top (a pair's first level)
-                    __stcs(o0, su_a);
-                    __stcs(o1, sv_a);
-                    __stcs(o2, sw_a);
-                    if (vb) {
-                        __stcs(o0 + 1, su_b);
-                        __stcs(o1 + 1, sv_b);
-                        __stcs(o2 + 1, sw_b);
+            int pst = cst;
+            pg ^= pflip;
+            {  // plane ib -> slot 0
+                const double *pl = wait_next();
+                const double *pz = pl + (pg ? o_z : e_z), *pm = pl + (pg ? o_m : e_m);
+                const int qz = qof(pg), qn = qz ^ (int)ODD;
+                U0[0] = P(pz, 0, qz);
+                V0[0] = P(pz, 1, qz);
+                W0[0] = P(pz, 2, qz);
+                VM[0] = P(pm, 1, qn);
+                W0M[0] = M(W0[0], pz, 2, qz);
+                advance();
+                sxu_a = __dadd_rn(U0[0].x, U0[2].x);
+                sxu_b = __dadd_rn(U0[0].y, U0[2].y);
+            }
+
+            const int64_t obase = (ib * ny2 + (j0 + c)) * nz + k0;
+            double *o0 = a.o0 + obase;
+            double *o1 = a.o1 + obase;
+            double *o2 = a.o2 + obase;
+            const int64_t ostep = ny2 * nz;
+
+            auto body = [&](auto R) {
+                constexpr int r = decltype(R)::value;
+                constexpr int rm = (r + 2) % 3, rp = (r + 1) % 3;
+                const int lst = cst;
+                const double *L = wait_next();                       // plane i+1
+                const double *C = ring + (size_t)pst * 3 * CS;      // plane i
+                const int pgl = pg ^ pflip;
+                const double *Lz = L + (pgl ? o_z : e_z), *Lm = L + (pgl ? o_m : e_m);
+                const double *Cz = C + (pg ? o_z : e_z), *Cm = C + (pg ? o_m : e_m);
+                const double *Cp = C + (pg ? o_p : e_p);
+                const int lq = qof(pgl), lqn = lq ^ (int)ODD;  // plane i+1
+                const int cq = qof(pg), cqn = cq ^ (int)ODD;    // plane i
+                U0[rp] = P(Lz, 0, lq);
+                V0[rp] = P(Lz, 1, lq);
+                W0[rp] = P(Lz, 2, lq);
+                VM[rp] = P(Lm, 1, lqn);
+                W0M[rp] = M(W0[rp], Lz, 2, lq);
+                const double2 u1c = P(Cp, 0, cqn);
+                const double2 umc = P(Cm, 0, cqn), v1c = P(Cp, 1, cqn), w1c = P(Cp, 2, cqn), wmc = P(Cm, 2, cqn);
+                const double w1cM = M(w1c, Cp, 2, cqn);
+                const double u0cM = M(U0[r], Cz, 0, cq);
+                const double u0cQ = Q(U0[r], Cz, 0, cq);
+                const double v0cM = M(V0[r], Cz, 1, cq);
+                const double v0cQ = Q(V0[r], Cz, 1, cq);
+                const double w0cQ = Q(W0[r], Cz, 2, cq);
+                const double vmcM = M(VM[r], Cm, 1, cqn);
+                release(pst);  // plane i fully consumed by this warp
+
+                const double2 u0m = U0[rm], u0c = U0[r], u0p = U0[rp];
+                const double2 v0m = V0[rm], v0c = V0[r], v0p = V0[rp];
+                const double2 w0m = W0[rm], w0c = W0[r], w0p = W0[rp];
+                const double2 vmc = VM[r], vmp = VM[rp];
+                const double w0cM = W0M[r], w0pM = W0M[rp];
+
+                const double nsxu_a = __dadd_rn(u0c.x, u0p.x), nsxu_b = __dadd_rn(u0c.y, u0p.y);
+                const double ntxu_a = __dadd_rn(u0c.x, u1c.x), ntxu_b = __dadd_rn(u0c.y, u1c.y);
+                const double nrxu_a = __dadd_rn(u0cM, u0c.x), nrxu_b = __dadd_rn(u0c.x, u0c.y);
+                const double szu = __dadd_rn(w0c.x, w0p.x);
+                const double szv = __dadd_rn(w0c.x, w1c.x);
+                const double szw = __dadd_rn(w0c.x, w0c.y);
+
+                // the operand wiring of kernel.py:117-128, as k_advect_xmarch
+                double su_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, u0m.x, sxu_a, u0p.x, nsxu_a,
+                                           umc.x, __dadd_rn(vmc.x, vmp.x), u1c.x, __dadd_rn(v0c.x, v0p.x),
+                                           u0cM, __dadd_rn(w0cM, w0pM), u0c.y, szu, top_a);
+                double sv_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, v0m.x, txu_a, v0p.x, ntxu_a,
+                                           vmc.x, __dadd_rn(v0c.x, vmc.x), v1c.x, __dadd_rn(v0c.x, v1c.x),
+                                           v0cM, __dadd_rn(w0cM, w1cM), v0c.y, szv, top_a);
+                double sw_a = pw_sums<FMA>(tcx, tcy, c1a, c2a, w0m.x, rxu_a, w0p.x, nrxu_a,
+                                           wmc.x, __dadd_rn(vmcM, vmc.x), w1c.x, __dadd_rn(v0cM, v0c.x),
+                                           w0cM, __dadd_rn(w0c.x, w0cM), w0c.y, szw, top_a);
+                double su_b = pw_sums<FMA>(tcx, tcy, c1b, c2b, u0m.y, sxu_b, u0p.y, nsxu_b,
+                                           umc.y, __dadd_rn(vmc.y, vmp.y), u1c.y, __dadd_rn(v0c.y, v0p.y),
+                                           u0c.x, szu, u0cQ, __dadd_rn(w0c.y, w0p.y), top_b);
+                double sv_b = pw_sums<FMA>(tcx, tcy, c1b, c2b, v0m.y, txu_b, v0p.y, ntxu_b,
+                                           vmc.y, __dadd_rn(v0c.y, vmc.y), v1c.y, __dadd_rn(v0c.y, v1c.y),
+                                           v0c.x, szv, v0cQ, __dadd_rn(w0c.y, w1c.y), top_b);
+                double sw_b = pw_sums<FMA>(tcx, tcy, c1b, c2b, w0m.y, rxu_b, w0p.y, nrxu_b,
+                                           wmc.y, __dadd_rn(vmc.x, vmc.y), w1c.y, __dadd_rn(v0c.x, v0c.y),
+                                           w0c.x, szw, w0cQ, __dadd_rn(w0c.y, w0cQ), top_b);
+                sxu_a = nsxu_a;
+                sxu_b = nsxu_b;
+                txu_a = ntxu_a;
+                txu_b = ntxu_b;
+                rxu_a = nrxu_a;
+                rxu_b = nrxu_b;
+                if (z_a) su_a = sv_a = sw_a = 0.0;
+                if constexpr (STEP) {
+                    su_a = fwd_update(u0c.x, dt, su_a);
+                    su_b = fwd_update(u0c.y, dt, su_b);
+                    sv_a = fwd_update(v0c.x, dt, sv_a);
+                    sv_b = fwd_update(v0c.y, dt, sv_b);
+                    sw_a = fwd_update(w0c.x, dt, sw_a);
+                    sw_b = fwd_update(w0c.y, dt, sw_b);
+                }
+                if (active && va && !(PWADV_CT_DBG & 2)) {
+                    if (!ODD || (vb && cq == 0)) {  // on the 16-byte grid
+                        store2(o0, su_a, su_b);
+                        store2(o1, sv_a, sv_b);
+                        store2(o2, sw_a, sw_b);
+                    } else {  // odd nz: odd global column, or the top (a pair's first level)
+                        __stcs(o0, su_a);
+                        __stcs(o1, sv_a);
+                        __stcs(o2, sw_a);
+                        if (vb) {
+                            __stcs(o0 + 1, su_b);
+                            __stcs(o1 + 1, sv_b);
+                            __stcs(o2 + 1, sw_b);
+                        }
                     }
                 }
-            }
-            o0 += ostep;
-            o1 += ostep;
-            o2 += ostep;
-            pst = lst;
-            pg = pgl;
-            advance();
-        };
+                o0 += ostep;
+                o1 += ostep;
+                o2 += ostep;
+                pst = lst;
+                pg = pgl;
+                advance();
+            };
 
-        using R0 = std::integral_constant<int, 0>;
-        using R1 = std::integral_constant<int, 1>;
-        using R2 = std::integral_constant<int, 2>;
-        const int nsteps = (int)(ie - ib);
-        int n = 0;
-        for (; n + 3 <= nsteps; n += 3) {
-            body(R0{});
-            body(R1{});
-            body(R2{});
+            using R0 = std::integral_constant<int, 0>;
+            using R1 = std::integral_constant<int, 1>;
+            using R2 = std::integral_constant<int, 2>;
+            const int nsteps = (int)(ie - ib);
+            int n = 0;
+            for (; n + 3 <= nsteps; n += 3) {
+                body(R0{});
+                body(R1{});
+                body(R2{});
+            }
+            if (n < nsteps) {
+                body(R0{});
+                if (n + 1 < nsteps) body(R1{});
+            }
+            release(pst);  // plane ie was only read as the x+1 plane
+        };
+        if constexpr (!ODD) {
+            run_unit(std::integral_constant<int, -1>{});
+        } else if (podd) {
+            run_unit(std::integral_constant<int, 2>{});
+        } else if ((pg + tc) & 1) {
+            run_unit(std::integral_constant<int, 1>{});
+        } else {
+            run_unit(std::integral_constant<int, 0>{});
         }
-        if (n < nsteps) {
-            body(R0{});
-            if (n + 1 < nsteps) body(R1{});
-        }
-        release(pst);  // plane ie was only read as the x+1 plane
     }
 }
 

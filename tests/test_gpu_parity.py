@@ -494,7 +494,7 @@ def test_tall_and_odd_columns_bitwise(shape):
     plan = device.describe_plan(dims)
     # even deep columns: the column-tile X-march (k-slabs); odd nz: the UA
     # form up to 767, K1m above
-    assert plan["kernel"] == ("xmarch_ct" if (nz % 2 == 0 and nz > 128) or nz > 383 else
+    assert plan["kernel"] == ("xmarch_ct" if (nz % 2 == 0 and nz > 128) or nz >= 255 else
                               "xmarch_elem")
     # and the one-thread-per-point kernel, forced, agrees
     got_s, _ = gpu_advect(u, v, w, *args, "simple")
@@ -845,7 +845,7 @@ def test_dropin_tour_example_runs():
 def test_general_march_kernel_bitwise(shape):
     """The general shapes (odd nz, tall columns, 8-byte-aligned fields): whole
     grid, a sub-box, the fused step and the FMA build against the oracle, on
-    the default plan ('xmarch_elem' for odd nz up to 383, column tiles above) and
+    the default plan ('xmarch_elem' for odd nz up to 253, column tiles above) and
     with K1m and the element ring each forced."""
     nx, ny, nz = shape
     u, v, w = oracle.fill_random(nx, ny, nz, 31, baseline=True)
@@ -855,7 +855,7 @@ def test_general_march_kernel_bitwise(shape):
     want = oracle.advect(u, v, w, *args)
     got, _ = gpu_advect(u, v, w, *args)
     if nz % 2:
-        assert device.describe_plan(dims)["kernel"] == ("xmarch_elem" if nz < 384 else "xmarch_ct")
+        assert device.describe_plan(dims)["kernel"] == ("xmarch_elem" if nz < 255 else "xmarch_ct")
     assert_bitwise(got, want, shape)
     # K1m and the element-ring X-march, each forced, agree too
     for variant in ("march", "xmarch_elem"):
