@@ -48,6 +48,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <climits>
 #include <mutex>
 #include <type_traits>
 #include <vector>
@@ -1184,11 +1185,35 @@ static int encode_field_map(CUtensorMap *m, const double *f, const BoxLaunch &L,
 static int launch_ctile(const BoxLaunch &L, const BoxArgs &a, const TileCfg &t, const XmarchPlan &plan,
                         bool fma, cudaStream_t stream)
 {
+    // the maps depend only on (fields, shape, slab height): a small per-thread
+    // cache keeps the encodes off the launch path of repeated launches
+    // (time steps, ping-pong buffers, graph capture)
+    struct MapEntry {
+        const double *u, *v, *w;
+        int64_t nx, ny, nz;
+        int kt;
+        CtMaps maps;
+    };
+    thread_local MapEntry cache[4];
+    thread_local int cache_next = 0;
     CtMaps maps;
-    int rc = encode_field_map(&maps.u, L.u, L, plan.kt, plan.tj);
-    if (rc == PWADV_OK) rc = encode_field_map(&maps.v, L.v, L, plan.kt, plan.tj);
-    if (rc == PWADV_OK) rc = encode_field_map(&maps.w, L.w, L, plan.kt, plan.tj);
-    if (rc != PWADV_OK) return rc;
+    bool hit = false;
+    for (const MapEntry &e : cache) {
+        if (e.u == L.u && e.v == L.v && e.w == L.w && e.nx == L.nx && e.ny == L.ny && e.nz == L.nz &&
+            e.kt == plan.kt && e.u) {
+            maps = e.maps;
+            hit = true;
+            break;
+        }
+    }
+    if (!hit) {
+        int rc = encode_field_map(&maps.u, L.u, L, plan.kt, plan.tj);
+        if (rc == PWADV_OK) rc = encode_field_map(&maps.v, L.v, L, plan.kt, plan.tj);
+        if (rc == PWADV_OK) rc = encode_field_map(&maps.w, L.w, L, plan.kt, plan.tj);
+        if (rc != PWADV_OK) return rc;
+        cache[cache_next] = MapEntry{L.u, L.v, L.w, L.nx, L.ny, L.nz, plan.kt, maps};
+        cache_next = (cache_next + 1) % 4;
+    }
     void (*kern)(BoxArgs, TileCfg, CtMaps) = nullptr;
 #define PWADV_PICK_CT(KT, ODD)                                                                \
     if (plan.kt == KT && odd == ODD)                                                          \
@@ -1601,6 +1626,11 @@ static bool plan_ctile(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
         (L.max_threads > 0 && L.max_threads != 512) ||
         (L.flags & (PWADV_FLAG_DEBUG_NO_COMPUTE | PWADV_FLAG_DEBUG_NO_STORE | PWADV_FLAG_UNALIGNED |
                     PWADV_FLAG_GENERIC)))
+        return false;
+    // TMA coordinates are 32-bit: planes and columns (even nz), column-pair
+    // rows (odd nz)
+    if (L.nx + 2 > INT32_MAX || L.ny + 2 > INT32_MAX || nz > INT32_MAX / 2 ||
+        (nz % 2 && (L.nx + 2) * (L.ny + 2) / 2 > INT32_MAX))
         return false;
     int kt = ctile_kt(nz);
     if (L.tile_j > 0) {
