@@ -2,7 +2,7 @@
 the same bits (a rare race in the mbarrier / refill protocol would show up as
 a changed digest or a hang). Prints one JSON line.
 
-    python tools/soak.py [--launches 100000] [--steps 3000] [--only k1,k4,pull,ua]
+    python tools/soak.py [--launches 100000] [--steps 3000] [--only k1,k4,pull,ua,ct]
 """
 import argparse
 import json
@@ -68,6 +68,27 @@ def main():
                 bad += digest(outu) != ref
         torch.cuda.synchronize()
         res["k1_ua_512x512x63"] = {"launches": n_ua, "mismatches": bad, "s": round(time.perf_counter() - t, 1)}
+    if "ct" in which:  # the column-tile form K1c: deep even columns and odd nz (pair rows)
+        for shape, seed in (((256, 256, 512), 3), ((128, 130, 1031), 4), ((130, 129, 1031), 6)):
+            dc = pw.make_grid(*shape)
+            fc = device.fill(dc, pw.GeneratorSpec.baseline(seed))
+            coc = device.DeviceCoefficients.from_host(pw.baseline_coefficients(seed, shape[2]), "cuda")
+            outc = device.alloc_fields(dc, "cuda")
+            assert device.describe_plan(dc)["kernel"] == "xmarch_ct"
+            device.advect(*fc, coc, outc)
+            ref = digest(outc)
+            n_ct = max(1, a.launches // 4)
+            bad = 0
+            t = time.perf_counter()
+            for n in range(n_ct):
+                device.advect(*fc, coc, outc)
+                if n % 1000 == 999:
+                    bad += digest(outc) != ref
+            torch.cuda.synchronize()
+            res["k1c_" + "x".join(map(str, shape))] = {"launches": n_ct, "mismatches": bad,
+                                                        "s": round(time.perf_counter() - t, 1)}
+            del fc, outc
+            torch.cuda.empty_cache()
     if not which & {"k1", "k4"}:
         print(json.dumps(res))
         return
