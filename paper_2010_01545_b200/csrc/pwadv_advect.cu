@@ -1596,14 +1596,22 @@ static int ctile_kt(int64_t nz)
 // 0.9 / 0.8 at TJ = 5 / 4 / 3 / 2 / 1; column tiles 0.98 / slab preference).
 // E.g. nz 64, 128: whole columns (1.0 vs 0.98); 130: whole (0.82 vs 0.74 —
 // 23% idle slab levels); 160, 192, 256 and deeper: tiles.
-static bool ctile_pays(int64_t nz)
+static bool ctile_pays(int64_t nz, int64_t ny)
 {
-    // odd nz: the column-pair form (odd columns read with 8-byte loads and
-    // stored as scalars) against the UA form (every pair so): 101-105 vs
-    // 104-111 Gpts/s at nz 63-191, even at 255 (108 vs 107), ahead from
-    // there as the UA strips narrow (113 vs 107 at 512x512x255, 114 vs 88 at
-    // nz 511) and against K1m above 767 (104-106 vs 82-85)
-    if (nz % 2 != 0) return nz >= 255;
+    // odd nz. With ny+2 even a unit's column parities are fixed and odd
+    // columns take shifted pairs (every thread's own loads and all stores on
+    // the 16-byte grid): 107-121 Gpts/s against the UA form's 102-112 at nz
+    // 63-255, 119-122 vs 87 at 511 — taken whenever its slabs are >= 90% busy
+    // (nz 63, 127, 191 yes; 33, 95 no: a half-empty slab). With ny+2 odd the
+    // parity alternates per plane (unshifted pairs, odd columns scalar): 89 vs
+    // the UA form's 107 at nz 63, ahead once the UA strips narrow (nz >= 255)
+    // and against K1m above 767.
+    if (nz % 2 != 0) {
+        if (nz >= 255) return true;
+        if ((ny + 2) % 2 != 0) return false;
+        const int kt = ctile_kt(nz);
+        return (double)nz >= 0.9 * (double)((nz + 1 + kt - 1) / kt * kt);
+    }
     const int kt = ctile_kt(nz);
     const double pref = kt == 128 ? 1.0 : (kt == 64 ? 1.01 : 1.08);
     const double ct = 0.98 * (double)nz / (double)((nz + kt - 1) / kt * kt) / pref;
@@ -1645,7 +1653,9 @@ static bool plan_ctile(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     }
     const int tj = 768 / kt;
     const int64_t nby = L.y1 - L.y0;
-    const int64_t nslab = (nz + kt - 1) / kt;
+    // odd nz: an odd column's pairs may start one level low (k_advect_ctile's
+    // shifted pairs), so the slabs cover nz + 1 levels
+    const int64_t nslab = (nz + (nz & 1) + kt - 1) / kt;
     // CtLayout::CS: even nz (tj+2) column slots, odd nz two halves of tj/2+2
     const int half = ((tj / 2 + 2) * (kt + 4) + 15) / 16 * 16;
     const int box = nz % 2 ? half + (tj / 2 + 2) * (kt + 4) : (tj + 2) * (kt + 4);
@@ -1678,7 +1688,7 @@ bool plan_xmarch(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
     // be faster (ctile_pays: deep columns, whose whole-column strips shrink to
     // 1-5 columns — measured 122-133 Gpts/s at nz 160-2048 against 106-124
     // for the whole-column X-march and ~80 for K1m above 768)
-    if (!(L.flags & PWADV_FLAG_NO_CTILE) && ((L.flags & PWADV_FLAG_CTILE) || (L.tile_j <= 0 && ctile_pays(L.nz))) &&
+    if (!(L.flags & PWADV_FLAG_NO_CTILE) && ((L.flags & PWADV_FLAG_CTILE) || (L.tile_j <= 0 && ctile_pays(L.nz, L.ny))) &&
         plan_ctile(L, dev, p))
         return true;
     const int64_t nz = L.nz;

@@ -32,6 +32,9 @@
 #define PWADV_CT_REALIGN_LDS 1  // odd columns (odd nz): two 8-byte shared loads (default; 0 = the
                                 // 16-byte load + shuffle: 5-15% slower, profiles/r02_ct_odd_nz.jsonl)
 #endif
+#ifndef PWADV_CT_SHIFTED
+#define PWADV_CT_SHIFTED 1  // odd nz, fixed column parity: odd columns' pairs at odd levels (A/B switch)
+#endif
 #ifndef PWADV_CT_DBG
 #define PWADV_CT_DBG 0  // debug builds only (tools/build_variant.py): 1 = odd nz loads one half, 2 = no stores
 #endif
@@ -241,28 +244,32 @@ __global__ void __launch_bounds__(512, 1)
             cph ^= 1u;
         }
     };
-    // pl: a staged plane advanced to the column's slot; f: field; q: the
-    // column is an odd global column (ODD only; warp-uniform), its copy one
-    // level higher in the slot: the pair is realigned from (k0-1, k0)
-    auto P = [&](const double *pl, int f, int q) -> double2 {
+    // pl: a staged plane advanced to the column's slot; f: field; sh: where
+    // the pair sits relative to slot index s0 (odd nz only, warp-uniform):
+    // 0 = on the 16-byte grid, +-1 = one level up / down (an odd column's
+    // copy sits one level higher in its slot) — read with two 8-byte loads
+    auto P = [&](const double *pl, int f, int sh) -> double2 {
+        if (ODD && sh) {
 #if PWADV_CT_REALIGN_LDS
-        if (ODD && q) return make_double2(pl[f * CS + s0 + 1], pl[f * CS + s0 + 2]);
+            return make_double2(pl[f * CS + s0 + sh], pl[f * CS + s0 + sh + 1]);
+#else
+            const double2 x = *reinterpret_cast<const double2 *>(pl + f * CS + s0 + sh - 1);
+            double d = __shfl_down_sync(0xffffffffu, x.x, 1);
+            if (fixQ) d = pl[f * CS + s0 + sh + 1];
+            return make_double2(x.y, d);
 #endif
-        const double2 x = *reinterpret_cast<const double2 *>(pl + f * CS + s0);
-        if (!ODD || !q) return x;
-        double d = __shfl_down_sync(0xffffffffu, x.x, 1);
-        if (fixQ) d = pl[f * CS + s0 + 2];
-        return make_double2(x.y, d);
+        }
+        return *reinterpret_cast<const double2 *>(pl + f * CS + s0);
     };
     // k0-1 / k0+2 of the pair: the neighbouring lane's value, or the slot's
-    auto M = [&](double2 p, const double *pl, int f, int q) -> double {
+    auto M = [&](double2 p, const double *pl, int f, int sh) -> double {
         double m = __shfl_up_sync(0xffffffffu, p.y, 1);
-        if (fixM) m = pl[f * CS + s0 - 1 + q];
+        if (fixM) m = pl[f * CS + s0 - 1 + sh];
         return m;
     };
-    auto Q = [&](double2 p, const double *pl, int f, int q) -> double {
+    auto Q = [&](double2 p, const double *pl, int f, int sh) -> double {
         double v = __shfl_down_sync(0xffffffffu, p.x, 1);
-        if (fixQ) v = pl[f * CS + s0 + 2 + q];
+        if (fixQ) v = pl[f * CS + s0 + 2 + sh];
         return v;
     };
 
@@ -275,18 +282,8 @@ __global__ void __launch_bounds__(512, 1)
         const int64_t ie = ib + (rs->first[k + 1] - rs->first[k]) - 2;
         const int64_t j0 = rs->uj0[k];
         const bool active = c < rs->utj[k];
-        // this thread's levels in this slab (even nz: a pair is in or out
-        // whole, the top is a pair's second level; odd nz: its first)
-        const int64_t k0 = (int64_t)rs->dsto[k] + 2 * kp;
-        const bool va = k0 < nz, vb = k0 + 1 < nz;
-        const bool top_a = ODD && k0 == nz - 1, top_b = !ODD && k0 + 1 == nz - 1;
-        const bool z_a = k0 == 0;
-        const int64_t kia = k0 < nz ? k0 : nz - 1;  // coefficient levels (clamped)
-        const int64_t kib = k0 + 1 < nz ? k0 + 1 : nz - 1;
         // parity of the first global column of plane ib-1's tile
         int pg = ODD ? (int)((((ib - 1) * ny2) + (j0 - 1)) & 1) : 0;
-        const double c1a = __ldg(a.tzc1 + kia), c1b = __ldg(a.tzc1 + kib);
-        const double c2a = __ldg(a.tzc2 + kia), c2b = __ldg(a.tzc2 + kib);
 
         // the unit's steps, specialised on the parity of the thread's global
         // column (odd nz): QV 0 / 1 when it is the same on every plane of the
@@ -295,7 +292,26 @@ __global__ void __launch_bounds__(512, 1)
         // common cases are compile-time
         auto run_unit = [&](auto QVC) {
             constexpr int QV = decltype(QVC)::value;
+            // odd nz, column parity fixed over the unit: an odd column's pairs
+            // start at odd levels (kb - 1 + 2kp), on the 16-byte grid in its
+            // slot and in global memory; only the neighbouring columns' pairs
+            // are off it (slot shift -1 / +1). Otherwise every pair starts at
+            // an even level and an odd column's own pairs are off the grid.
+            constexpr bool SS = PWADV_CT_SHIFTED && ODD && (QV == 0 || QV == 1);
             const int pflip = QV == 2 ? podd : 0;
+            // this thread's levels in this slab (even nz: a pair is in or out
+            // whole, the top is a pair's second level; odd nz: either)
+            const int64_t k0 = (int64_t)rs->dsto[k] + 2 * kp - (SS && QV == 1 ? 1 : 0);
+            const bool va = (!SS || k0 >= 0) && k0 < nz, vb = k0 + 1 < nz;
+            const bool top_a = ODD && k0 == nz - 1, top_b = k0 + 1 == nz - 1;
+            const bool z_a = k0 == 0, z_b = SS && k0 == -1;
+            const int64_t kia = k0 < 0 ? 0 : (k0 < nz ? k0 : nz - 1);  // coefficient levels (clamped)
+            const int64_t kib = k0 + 1 < nz ? k0 + 1 : nz - 1;
+            const double c1a = __ldg(a.tzc1 + kia), c1b = __ldg(a.tzc1 + kib);
+            const double c2a = __ldg(a.tzc2 + kia), c2b = __ldg(a.tzc2 + kib);
+            // slot shifts of the thread's own column and of its neighbours
+            auto sh_own = [&](int q) -> int { return SS ? 0 : q; };
+            auto sh_nbr = [&](int q) -> int { return SS ? (QV == 1 ? -1 : 1) : (ODD ? q ^ 1 : 0); };
             auto qof = [&](int pgx) -> int {
                 if constexpr (QV < 0) {
                     (void)pgx;
@@ -310,7 +326,7 @@ __global__ void __launch_bounds__(512, 1)
             {  // plane ib-1 -> slot 2
                 const double *pl = wait_next();
                 const double *pz = pl + (pg ? o_z : e_z), *pp = pl + (pg ? o_p : e_p);
-                const int qz = qof(pg), qn = qz ^ (int)ODD;  // odd column / its neighbours
+                const int qz = sh_own(qof(pg)), qn = sh_nbr(qof(pg));  // slot shifts: own / neighbours
                 U0[2] = P(pz, 0, qz);
                 const double2 u1 = P(pp, 0, qn);
                 V0[2] = P(pz, 1, qz);
@@ -328,7 +344,7 @@ __global__ void __launch_bounds__(512, 1)
             {  // plane ib -> slot 0
                 const double *pl = wait_next();
                 const double *pz = pl + (pg ? o_z : e_z), *pm = pl + (pg ? o_m : e_m);
-                const int qz = qof(pg), qn = qz ^ (int)ODD;
+                const int qz = sh_own(qof(pg)), qn = sh_nbr(qof(pg));
                 U0[0] = P(pz, 0, qz);
                 V0[0] = P(pz, 1, qz);
                 W0[0] = P(pz, 2, qz);
@@ -355,8 +371,8 @@ __global__ void __launch_bounds__(512, 1)
                 const double *Lz = L + (pgl ? o_z : e_z), *Lm = L + (pgl ? o_m : e_m);
                 const double *Cz = C + (pg ? o_z : e_z), *Cm = C + (pg ? o_m : e_m);
                 const double *Cp = C + (pg ? o_p : e_p);
-                const int lq = qof(pgl), lqn = lq ^ (int)ODD;  // plane i+1
-                const int cq = qof(pg), cqn = cq ^ (int)ODD;    // plane i
+                const int lq = sh_own(qof(pgl)), lqn = sh_nbr(qof(pgl));  // plane i+1
+                const int cq = sh_own(qof(pg)), cqn = sh_nbr(qof(pg));    // plane i
                 U0[rp] = P(Lz, 0, lq);
                 V0[rp] = P(Lz, 1, lq);
                 W0[rp] = P(Lz, 2, lq);
@@ -412,6 +428,7 @@ __global__ void __launch_bounds__(512, 1)
                 rxu_a = nrxu_a;
                 rxu_b = nrxu_b;
                 if (z_a) su_a = sv_a = sw_a = 0.0;
+                if (z_b) su_b = sv_b = sw_b = 0.0;
                 if constexpr (STEP) {
                     su_a = fwd_update(u0c.x, dt, su_a);
                     su_b = fwd_update(u0c.y, dt, su_b);
@@ -420,12 +437,12 @@ __global__ void __launch_bounds__(512, 1)
                     sw_a = fwd_update(w0c.x, dt, sw_a);
                     sw_b = fwd_update(w0c.y, dt, sw_b);
                 }
-                if (active && va && !(PWADV_CT_DBG & 2)) {
-                    if (!ODD || (vb && cq == 0)) {  // on the 16-byte grid
+                if (active && (va || (SS && vb)) && !(PWADV_CT_DBG & 2)) {
+                    if (!ODD || (va && vb && (SS || qof(pg) == 0))) {  // on the 16-byte grid
                         store2(o0, su_a, su_b);
                         store2(o1, sv_a, sv_b);
                         store2(o2, sw_a, sw_b);
-                    } else {  // odd nz: odd global column, or the top (a pair's first level)
+                    } else if (va) {  // odd nz: an odd global column (unshifted), or the top
                         __stcs(o0, su_a);
                         __stcs(o1, sv_a);
                         __stcs(o2, sw_a);
@@ -434,6 +451,10 @@ __global__ void __launch_bounds__(512, 1)
                             __stcs(o1 + 1, sv_b);
                             __stcs(o2 + 1, sw_b);
                         }
+                    } else {  // shifted odd column: level 0 is its first pair's second level
+                        __stcs(o0 + 1, su_b);
+                        __stcs(o1 + 1, sv_b);
+                        __stcs(o2 + 1, sw_b);
                     }
                 }
                 o0 += ostep;

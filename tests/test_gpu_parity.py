@@ -480,8 +480,23 @@ def test_async_host_submissions_bitwise():
     ctx.close()
 
 
+def default_kernel(ny, nz):
+    """The planner's kernel for a whole 16-byte-aligned grid (plan_xmarch,
+    ctile_pays): column tiles for even nz >= 160 (130 stays on whole columns),
+    for odd nz >= 255, and for odd nz with ny even whose slabs are >= 90% busy
+    (KT 64 or 128); the X-march (UA form for odd nz) otherwise."""
+    if nz % 2 == 0:
+        return "xmarch_ct" if nz >= 160 else "xmarch"
+    if nz >= 255:
+        return "xmarch_ct"
+    if ny % 2:
+        return "xmarch_elem"
+    kt = 64 if -(-nz // 64) * 64 * 1.01 < -(-nz // 128) * 128 else 128
+    return "xmarch_ct" if nz >= 0.9 * (-(-(nz + 1) // kt) * kt) else "xmarch_elem"
+
+
 @pytest.mark.parametrize("shape", [(5, 4, 300), (3, 3, 512), (2, 3, 1024), (2, 2, 1030), (4, 3, 3),
-                                   (3, 4, 1031), (2, 5, 769)])
+                                   (3, 4, 1031), (2, 5, 769), (4, 6, 63), (5, 8, 95), (3, 6, 127)])
 def test_tall_and_odd_columns_bitwise(shape):
     # deep columns (nz 300, 512, 1024, 1030: column tiles), odd nz, all
     # against the oracle; the whole-column X-march and K1m forced agree too
@@ -494,8 +509,7 @@ def test_tall_and_odd_columns_bitwise(shape):
     plan = device.describe_plan(dims)
     # even deep columns: the column-tile X-march (k-slabs); odd nz: the UA
     # form up to 767, K1m above
-    assert plan["kernel"] == ("xmarch_ct" if (nz % 2 == 0 and nz > 128) or nz >= 255 else
-                              "xmarch_elem")
+    assert plan["kernel"] == default_kernel(ny, nz), (shape, plan)
     # and the one-thread-per-point kernel, forced, agrees
     got_s, _ = gpu_advect(u, v, w, *args, "simple")
     assert_bitwise(got_s, oracle.advect(u, v, w, *args), (shape, "simple"))
@@ -845,7 +859,7 @@ def test_dropin_tour_example_runs():
 def test_general_march_kernel_bitwise(shape):
     """The general shapes (odd nz, tall columns, 8-byte-aligned fields): whole
     grid, a sub-box, the fused step and the FMA build against the oracle, on
-    the default plan ('xmarch_elem' for odd nz up to 253, column tiles above) and
+    the default plan (default_kernel: the UA form or column tiles) and
     with K1m and the element ring each forced."""
     nx, ny, nz = shape
     u, v, w = oracle.fill_random(nx, ny, nz, 31, baseline=True)
@@ -855,7 +869,7 @@ def test_general_march_kernel_bitwise(shape):
     want = oracle.advect(u, v, w, *args)
     got, _ = gpu_advect(u, v, w, *args)
     if nz % 2:
-        assert device.describe_plan(dims)["kernel"] == ("xmarch_elem" if nz < 255 else "xmarch_ct")
+        assert device.describe_plan(dims)["kernel"] == default_kernel(ny, nz)
     assert_bitwise(got, want, shape)
     # K1m and the element-ring X-march, each forced, agree too
     for variant in ("march", "xmarch_elem"):
