@@ -1593,9 +1593,10 @@ static int ctile_kt(int64_t nz)
 // Whole-column X-march vs column tiles, from a fit to the measured rates
 // (profiles/README.md, round 2): relative rate = busy-thread fraction x a
 // strip-width factor (whole columns: 1.0 at TJ >= 6, 0.97 / 0.95 / 0.93 /
-// 0.9 / 0.8 at TJ = 5 / 4 / 3 / 2 / 1; column tiles 0.98 / slab preference).
-// E.g. nz 64, 128: whole columns (1.0 vs 0.98); 130: whole (0.82 vs 0.74 —
-// 23% idle slab levels); 160, 192, 256 and deeper: tiles.
+// 0.9 / 0.8 at TJ = 5 / 4 / 3 / 2 / 1, x 0.92 off the compile-time layouts;
+// column tiles 0.98 / slab preference). E.g. nz 64, 128: whole columns (1.0
+// vs 0.98); 80, 96, 100, 130-150: whole (idle slab levels); 110-126, 160,
+// 192, 256 and deeper: tiles.
 static bool ctile_pays(int64_t nz, int64_t ny)
 {
     // odd nz. With ny+2 even a unit's column parities are fixed and odd
@@ -1619,7 +1620,12 @@ static bool ctile_pays(int64_t nz, int64_t ny)
     if (kp > 384) return true;  // no whole-column plan
     const int64_t tj = 384 / kp;
     static const double width[6] = {0.0, 0.8, 0.9, 0.93, 0.95, 0.97};
-    const double whole = (double)(tj * kp) / 384.0 * (tj >= 6 ? 1.0 : width[tj]);
+    // the whole-column tile has a compile-time layout only at nz 64 / 128
+    // (NZC); elsewhere its run-time layout costs ~8% at equal occupancy
+    // (nz 110 / 120: 117 / 122 Gpts/s against K1c's 128 / 131 with the same
+    // busy fraction; profiles/r02_monc_depths.jsonl)
+    const double layout = (nz == 64 || nz == 128) && 384 % kp == 0 ? 1.0 : 0.92;
+    const double whole = (double)(tj * kp) / 384.0 * (tj >= 6 ? 1.0 : width[tj]) * layout;
     return ct > whole;
 }
 

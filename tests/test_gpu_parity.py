@@ -480,23 +480,51 @@ def test_async_host_submissions_bitwise():
     ctx.close()
 
 
+def _ctile_kt(nz):
+    best, kt = None, 128
+    for c, pref in ((128, 1.0), (64, 1.01), (32, 1.08)):
+        if c < 64 and nz % 2:
+            continue
+        cost = -(-nz // c) * c * pref
+        if best is None or cost < best:
+            best, kt = cost, c
+    return kt
+
+
 def default_kernel(ny, nz):
-    """The planner's kernel for a whole 16-byte-aligned grid (plan_xmarch,
-    ctile_pays): column tiles for even nz >= 160 (130 stays on whole columns),
-    for odd nz >= 255, and for odd nz with ny even whose slabs are >= 90% busy
-    (KT 64 or 128); the X-march (UA form for odd nz) otherwise."""
-    if nz % 2 == 0:
-        return "xmarch_ct" if nz >= 160 else "xmarch"
-    if nz >= 255:
-        return "xmarch_ct"
-    if ny % 2:
+    """The planner's kernel for a whole 16-byte-aligned grid — a mirror of
+    plan_xmarch / ctile_pays / ctile_kt (pwadv_advect.cu), pinning the rate
+    model fitted to the round-2 measurements: odd nz takes column tiles from
+    255 up, and below when ny is even and a slab is >= 90% busy, else the UA
+    form; even nz compares busy fraction x strip-width x layout factors (the
+    whole-column tile has a compile-time layout only at nz 64 / 128)."""
+    kt = _ctile_kt(nz)
+    if nz % 2:
+        if nz >= 255 or (ny % 2 == 0 and nz >= 0.9 * (-(-(nz + 1) // kt) * kt)):
+            return "xmarch_ct"
         return "xmarch_elem"
-    kt = 64 if -(-nz // 64) * 64 * 1.01 < -(-nz // 128) * 128 else 128
-    return "xmarch_ct" if nz >= 0.9 * (-(-(nz + 1) // kt) * kt) else "xmarch_elem"
+    ct = 0.98 * nz / (-(-nz // kt) * kt) / {128: 1.0, 64: 1.01, 32: 1.08}[kt]
+    kp = nz // 2
+    if kp > 384:
+        return "xmarch_ct"
+    tj = 384 // kp
+    layout = 1.0 if nz in (64, 128) and 384 % kp == 0 else 0.92
+    whole = tj * kp / 384 * (1.0 if tj >= 6 else [0, 0.8, 0.9, 0.93, 0.95, 0.97][tj]) * layout
+    return "xmarch_ct" if ct > whole else "xmarch"
+
+
+def test_default_kernel_mirror_pins_measured_choices():
+    # the decisions the round-2 measurements made (profiles/r02_monc_depths.jsonl,
+    # r02_shape_sweep_ct.jsonl, r02_ct_odd_nz.jsonl)
+    assert [default_kernel(512, nz) for nz in (64, 80, 96, 100, 128, 130, 150)] == ["xmarch"] * 7
+    assert {default_kernel(512, nz) for nz in (110, 120, 160, 256, 512, 1024, 1030)} == {"xmarch_ct"}
+    assert [default_kernel(512, nz) for nz in (63, 127, 255)] == ["xmarch_ct"] * 3
+    assert [default_kernel(511, 63), default_kernel(512, 33), default_kernel(512, 95)] == ["xmarch_elem"] * 3
 
 
 @pytest.mark.parametrize("shape", [(5, 4, 300), (3, 3, 512), (2, 3, 1024), (2, 2, 1030), (4, 3, 3),
-                                   (3, 4, 1031), (2, 5, 769), (4, 6, 63), (5, 8, 95), (3, 6, 127)])
+                                   (3, 4, 1031), (2, 5, 769), (4, 6, 63), (5, 8, 95), (3, 6, 127),
+                                   (3, 5, 110), (4, 4, 126), (3, 3, 100), (2, 3, 150)])
 def test_tall_and_odd_columns_bitwise(shape):
     # deep columns (nz 300, 512, 1024, 1030: column tiles), odd nz, all
     # against the oracle; the whole-column X-march and K1m forced agree too
