@@ -1252,6 +1252,13 @@ static int launch_ctile(const BoxLaunch &L, const BoxArgs &a, const TileCfg &t, 
     return PWADV_OK;
 }
 
+// compile-time tile layouts beyond the BASELINE depths 64 / 128 (depths whose
+// whole-column tile fills the 384 compute threads exactly)
+#ifndef PWADV_NZC_MORE
+#define PWADV_NZC_MORE 1
+#endif
+#define PWADV_NZC_EXTRA(nz) (PWADV_NZC_MORE && ((nz) == 32 || (nz) == 48 || (nz) == 96))
+
 int launch_box(const BoxLaunch &L, cudaStream_t stream)
 {
     BoxArgs a;
@@ -1322,7 +1329,7 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         const bool fix = (32 % plan.kp) != 0;  // a column straddles a warp boundary
         // compile-time layout for the BASELINE depths at the default tile
         const int nzc = (!plan.elem && !plan.ct && plan.maxt == 512 && plan.tj * plan.kp == 384 &&
-                         (L.nz == 64 || L.nz == 128) &&
+                         (L.nz == 64 || L.nz == 128 || PWADV_NZC_EXTRA(L.nz)) &&
                          !(L.flags & (PWADV_FLAG_GENERIC | PWADV_FLAG_DEBUG_NO_COMPUTE |
                                       PWADV_FLAG_DEBUG_NO_STORE)))
                             ? (int)L.nz : 0;
@@ -1339,12 +1346,18 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
                        // work stays out of the other kernels)
             if (nzc == 64) kern = pick_ws<64, false, false, true>(L.step, fma);
             else if (nzc == 128) kern = pick_ws<128, true, false, true>(L.step, fma);
+            // (the extra compile-time depths take the run-time-layout pull kernel)
             else kern = fix ? pick_ws<0, true, false, true>(L.step, fma)
                             : pick_ws<0, false, false, true>(L.step, fma);
         }
         if (!kern && !plan.ct) {
             PWADV_PICK_NZ(64, false)
             PWADV_PICK_NZ(128, true)
+#if PWADV_NZC_MORE
+            PWADV_PICK_NZ(32, false)
+            PWADV_PICK_NZ(48, true)
+            PWADV_PICK_NZ(96, true)
+#endif
         }
 #undef PWADV_PICK_NZ
 #define PWADV_PICK_ELEM(FX)                                                      \
@@ -1621,10 +1634,11 @@ static bool ctile_pays(int64_t nz, int64_t ny)
     const int64_t tj = 384 / kp;
     static const double width[6] = {0.0, 0.8, 0.9, 0.93, 0.95, 0.97};
     // the whole-column tile has a compile-time layout only at nz 64 / 128
-    // (NZC); elsewhere its run-time layout costs ~8% at equal occupancy
+    // and 32 / 48 / 96 (NZC); elsewhere its run-time layout costs ~8% at
+    // equal occupancy
     // (nz 110 / 120: 117 / 122 Gpts/s against K1c's 128 / 131 with the same
     // busy fraction; profiles/r02_monc_depths.jsonl)
-    const double layout = (nz == 64 || nz == 128) && 384 % kp == 0 ? 1.0 : 0.92;
+    const double layout = (nz == 64 || nz == 128 || PWADV_NZC_EXTRA(nz)) ? 1.0 : 0.92;
     const double whole = (double)(tj * kp) / 384.0 * (tj >= 6 ? 1.0 : width[tj]) * layout;
     return ct > whole;
 }

@@ -497,7 +497,8 @@ def default_kernel(ny, nz):
     model fitted to the round-2 measurements: odd nz takes column tiles from
     255 up, and below when ny is even and a slab is >= 90% busy, else the UA
     form; even nz compares busy fraction x strip-width x layout factors (the
-    whole-column tile has a compile-time layout only at nz 64 / 128)."""
+    whole-column tile has a compile-time layout only at nz 32 / 48 / 64 / 96 /
+    128)."""
     kt = _ctile_kt(nz)
     if nz % 2:
         if nz >= 255 or (ny % 2 == 0 and nz >= 0.9 * (-(-(nz + 1) // kt) * kt)):
@@ -508,7 +509,7 @@ def default_kernel(ny, nz):
     if kp > 384:
         return "xmarch_ct"
     tj = 384 // kp
-    layout = 1.0 if nz in (64, 128) and 384 % kp == 0 else 0.92
+    layout = 1.0 if nz in (32, 48, 64, 96, 128) else 0.92
     whole = tj * kp / 384 * (1.0 if tj >= 6 else [0, 0.8, 0.9, 0.93, 0.95, 0.97][tj]) * layout
     return "xmarch_ct" if ct > whole else "xmarch"
 
