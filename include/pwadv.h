@@ -79,7 +79,8 @@ enum {
  * copy per staged column, every (k, k+1) pair on the 16-byte grid even for odd
  * nz): force it where it applies / never use it (default: the planner's
  * choice). With it, tile_j selects the slab height
- * KT = 768 / tile_j: 6 (KT 128), 12 (KT 64) or 24 (KT 32). */
+ * KT = 768 / tile_j: 6 (KT 128), 8 (96), 12 (64), 16 (48) or 24 (32); odd nz
+ * takes 128 or 64 only. */
 #define PWADV_FLAG_CTILE 0x4000u
 #define PWADV_FLAG_NO_CTILE 0x8000u
 

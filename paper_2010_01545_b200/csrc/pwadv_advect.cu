@@ -1221,7 +1221,9 @@ static int launch_ctile(const BoxLaunch &L, const BoxArgs &a, const TileCfg &t, 
                       : (fma ? k_advect_ctile<true, false, KT, ODD> : k_advect_ctile<false, false, KT, ODD>);
     const bool odd = L.nz % 2 != 0;
     PWADV_PICK_CT(32, false)
+    PWADV_PICK_CT(48, false)
     PWADV_PICK_CT(64, false)
+    PWADV_PICK_CT(96, false)
     PWADV_PICK_CT(128, false)
     PWADV_PICK_CT(64, true)
     PWADV_PICK_CT(128, true)
@@ -1584,16 +1586,28 @@ static void plan_work(const BoxLaunch &L, const DeviceInfo &dev, int per_sm, Xma
 }
 
 // Slab height of the column-tile plan: the least (slab levels x preference).
-// Measured at equal slab fill KT 128 >= KT 64 (within 1-2%) > KT 32 (~8%: two
-// columns per warp): nz 1024 -> 128, 1030 -> 64 (17 slabs, 5.6% idle levels
-// against 12% for 128), 160 -> 32 (tools/shape_sweep.py, profiles/README.md).
+// Measured at equal slab fill KT 128 ~ 96 >= 64 ~ 48 (within 1-2%) > 32 (5-8%:
+// two columns per warp): nz 1024 -> 128, 1030 -> 96 (11 slabs, 2.5% idle
+// levels), 190 -> 96, 140 -> 48, 160 -> 32 (tools/shape_sweep.py,
+// profiles/r02_ct_slab_heights.jsonl).
+static double ct_pref(int kt)
+{
+    switch (kt) {
+    case 128: return 1.0;
+    case 96: return 1.0;
+    case 64: return 1.01;
+    case 48: return 1.01;
+    default: return 1.07;  // 32: two columns per warp
+    }
+}
+
 static int ctile_kt(int64_t nz)
 {
     int kt = 128;
     double best = 0.0;
-    for (int c : {128, 64, 32}) {
-        if (c < 64 && nz % 2) continue;  // odd nz: one column parity per warp
-        const double pref = c == 128 ? 1.0 : (c == 64 ? 1.01 : 1.08);
+    for (int c : {128, 96, 64, 48, 32}) {
+        if (nz % 2 && (c / 2) % 32) continue;  // odd nz: one column parity per warp
+        const double pref = ct_pref(c);
         const double cost = (double)((nz + c - 1) / c * c) * pref;
         if (best == 0.0 || cost < best) {
             best = cost;
@@ -1627,7 +1641,7 @@ static bool ctile_pays(int64_t nz, int64_t ny)
         return (double)nz >= 0.9 * (double)((nz + 1 + kt - 1) / kt * kt);
     }
     const int kt = ctile_kt(nz);
-    const double pref = kt == 128 ? 1.0 : (kt == 64 ? 1.01 : 1.08);
+    const double pref = ct_pref(kt);
     const double ct = 0.98 * (double)nz / (double)((nz + kt - 1) / kt * kt) / pref;
     const int64_t kp = nz / 2;
     if (kp > 384) return true;  // no whole-column plan
@@ -1662,12 +1676,13 @@ static bool plan_ctile(const BoxLaunch &L, const DeviceInfo &dev, XmarchPlan *p)
         return false;
     int kt = ctile_kt(nz);
     if (L.tile_j > 0) {
-        if (L.tile_j != 6 && L.tile_j != 12 && L.tile_j != 24) return false;
+        if (L.tile_j != 6 && L.tile_j != 8 && L.tile_j != 12 && L.tile_j != 16 && L.tile_j != 24)
+            return false;
         kt = 768 / L.tile_j;
     }
-    // odd nz: one column parity per warp (KT >= 64) for the warp-uniform
-    // realignment of odd columns' pairs
-    if (nz % 2 && kt < 64) {
+    // odd nz: one column parity per warp (KT 64 / 128) for the warp-uniform
+    // choice of odd columns' slot shifts
+    if (nz % 2 && (kt / 2) % 32) {
         if (L.tile_j > 0) return false;
         kt = 64;
     }

@@ -7,7 +7,7 @@
 // CTA and three staged columns per computed one) and nz > 768 does not fit
 // the ring at all (it ran on K1m, ~60% of HBM). Here a work unit is (X chunk,
 // y-strip, k-slab): the CTA's tile is TJ columns x KT levels, KT a compile-
-// time 32 / 64 / 128 (TJ = 768 / KT), and each plane tile of a field is ONE
+// time 32 / 48 / 64 / 96 / 128 (TJ = 768 / KT), and each plane tile of a field is ONE
 // 3-D tensor-map TMA box (cp.async.bulk.tensor, SASS UTMALDG) of KT + 4
 // levels x TJ + 2 columns x 1 plane starting at level kb - 2 — the hardware
 // walks the TJ + 2 column runs and zero-fills levels outside [0, nz) and

@@ -37,7 +37,7 @@ SHAPES = [(9, 7, 64), (13, 30, 63), (20, 25, 96), (7, 26, 97), (5, 12, 130), (6,
           (1, 24, 64), (11, 1, 65), (4, 12, 31)]
 
 
-@pytest.mark.parametrize("tile_j", [6, 12, 24])
+@pytest.mark.parametrize("tile_j", [6, 8, 12, 16, 24])
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
 def test_ctile_bitwise_against_oracle(shape, tile_j):
     nx, ny, nz = shape
@@ -46,7 +46,7 @@ def test_ctile_bitwise_against_oracle(shape, tile_j):
     want = oracle.advect(*ins, *args)
     opts = device.make_opts("xmarch_ct", tile_j=tile_j)
     plan = device.describe_plan(dims, opts=opts)
-    if nz % 2 and tile_j == 24:  # odd nz needs one column parity per warp: KT >= 64
+    if nz % 2 and tile_j in (8, 16, 24):  # odd nz needs one column parity per warp: KT 64 / 128
         assert plan["kernel"] != "xmarch_ct", plan
     else:
         assert plan["kernel"] == "xmarch_ct", plan

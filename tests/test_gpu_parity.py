@@ -482,8 +482,8 @@ def test_async_host_submissions_bitwise():
 
 def _ctile_kt(nz):
     best, kt = None, 128
-    for c, pref in ((128, 1.0), (64, 1.01), (32, 1.08)):
-        if c < 64 and nz % 2:
+    for c, pref in ((128, 1.0), (96, 1.0), (64, 1.01), (48, 1.01), (32, 1.07)):
+        if nz % 2 and (c // 2) % 32:
             continue
         cost = -(-nz // c) * c * pref
         if best is None or cost < best:
@@ -504,7 +504,7 @@ def default_kernel(ny, nz):
         if nz >= 255 or (ny % 2 == 0 and nz >= 0.9 * (-(-(nz + 1) // kt) * kt)):
             return "xmarch_ct"
         return "xmarch_elem"
-    ct = 0.98 * nz / (-(-nz // kt) * kt) / {128: 1.0, 64: 1.01, 32: 1.08}[kt]
+    ct = 0.98 * nz / (-(-nz // kt) * kt) / {128: 1.0, 96: 1.0, 64: 1.01, 48: 1.01, 32: 1.07}[kt]
     kp = nz // 2
     if kp > 384:
         return "xmarch_ct"
@@ -517,8 +517,9 @@ def default_kernel(ny, nz):
 def test_default_kernel_mirror_pins_measured_choices():
     # the decisions the round-2 measurements made (profiles/r02_monc_depths.jsonl,
     # r02_shape_sweep_ct.jsonl, r02_ct_odd_nz.jsonl)
-    assert [default_kernel(512, nz) for nz in (64, 80, 96, 100, 128, 130, 150)] == ["xmarch"] * 7
-    assert {default_kernel(512, nz) for nz in (110, 120, 160, 256, 512, 1024, 1030)} == {"xmarch_ct"}
+    assert [default_kernel(512, nz) for nz in (64, 80, 96, 100, 128, 150)] == ["xmarch"] * 6
+    assert {default_kernel(512, nz) for nz in (110, 120, 130, 140, 160, 190, 256, 270, 512, 1024,
+                                               1030)} == {"xmarch_ct"}
     assert [default_kernel(512, nz) for nz in (63, 127, 255)] == ["xmarch_ct"] * 3
     assert [default_kernel(511, 63), default_kernel(512, 33), default_kernel(512, 95)] == ["xmarch_elem"] * 3
 
