@@ -186,6 +186,25 @@ def pcie_concurrent(hin, hout, dev):
     return best
 
 
+def transfer_model_row(dims, h2d, d2h, seconds_per_step) -> dict:
+    """the measured host<->device path next to the
+    reference's own transfer model (pkg/src/pwadvect/transfer.py): its volume
+    per invocation is 3 fields x 8 B x interior cells each way
+    (transfer_volume, :52-58), moved at the FPGA card's calibrated end-to-end
+    rate of 5.85 GB/s (END_TO_END_BANDWIDTH, :29) and serialised with the
+    kernel (end_to_end, :91-107; the paper's dominant cost).
+    Here H2D, K1 and D2H of consecutive chunks and grids overlap."""
+    model_bytes = 2 * 3 * dims.cells * 8
+    model_dma_s = model_bytes / 5.85e9
+    return {"model_volume_bytes": model_bytes, "model_end_to_end_GBs": 5.85,
+            "model_dma_seconds": round(model_dma_s, 6),
+            "measured_bytes": int(h2d + d2h), "measured_seconds_per_step": round(seconds_per_step, 6),
+            "measured_GBs_both_ways": round((h2d + d2h) / seconds_per_step / 1e9, 2),
+            "speedup_vs_model_dma_alone": round(model_dma_s / seconds_per_step, 2),
+            "what": "reference transfer.py constants (FPGA card DMA, serialised with the kernel) vs "
+                    "this path's whole step (H2D + K1 + D2H, overlapped), same grid"}
+
+
 def host_info() -> dict:
     """CPU model, logical CPUs and numpy version of this host."""
     import numpy as np
@@ -672,7 +691,8 @@ def run_ours(args):
                "pcie_concurrent_GBs_each_way": round(pcie_gbs, 1),
                "pcie_bound": round(pcie_gbs * 1e9 / (h2d / dims.cells) / 1e9, 3),
                "frac_of_pcie_bound": round(dims.cells * ke / (t1 - t0) / (pcie_gbs * 1e9 / (h2d / dims.cells)), 3),
-               "bitwise_equal_to_device_run": bool(same)}
+               "bitwise_equal_to_device_run": bool(same),
+               "vs_reference_transfer_model": transfer_model_row(dims, h2d, d2h, (t1 - t0) / ke)}
 
     # config 4 (stepping, N=1) end to end through the public stepping API: the
     # state is uploaded from pinned host memory once, stepped, one probe value
