@@ -1304,6 +1304,11 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream)
         // more strips than one launch's unit tables hold (very long y): split
         // the box along y at a strip boundary and launch the halves in order
         const int64_t half = (nby / 2 + plan.tj - 1) / plan.tj * plan.tj;
+        if (half >= nby) {  // one strip already (column tiles of extreme depth): the march kernel
+            BoxLaunch m = L;
+            m.flags |= PWADV_FLAG_MARCH;
+            return launch_box(m, stream);
+        }
         BoxLaunch lo = L, hi = L;
         lo.y1 = L.y0 + half;
         hi.y0 = L.y0 + half;
