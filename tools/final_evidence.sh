@@ -3,7 +3,9 @@
 # the GPU suite, the bench lines of every BASELINE config and the reference
 # arm, the C1 launch list, and `ncu --set full` captures of one launch per
 # workload (each command first runs without ncu and must exit 0). Outputs go
-# to gpurun_out/ev/; tools/ncu_summary.py turns the reports into profiles/.
+# to gpurun_out/ev/ (reports exported to raw/details/source text on the box and
+# deleted: gpurun copies back at most 64 MiB); tools/ncu_summary.py turns the
+# raw CSVs into profiles/.
 #
 #   /usr/local/graft/bin/gpurun --timeout 3000 -- bash tools/final_evidence.sh
 set -u
@@ -29,7 +31,14 @@ cap() {  # cap NAME KREGEX ARGS...: plain run, then one --set full capture of th
   python tools/one_launch.py "$@" > "$OUT/ol_$name.log" 2>&1 && \
     ncu --set full --clock-control none --import-source on -k "regex:$kre" -s 2 -c 1 \
         -o "$OUT/ncu_$name" python tools/one_launch.py "$@" > "$OUT/ncu_$name.log" 2>&1
-  echo "cap_$name=$?"
+  local rc=$?
+  echo "cap_$name=$rc"
+  if [ -f "$OUT/ncu_$name.ncu-rep" ]; then  # keep the exports (gpurun copies back <= 64 MiB)
+    ncu -i "$OUT/ncu_$name.ncu-rep" --page raw --csv > "$OUT/ncu_${name}_raw.csv" 2>/dev/null
+    ncu -i "$OUT/ncu_$name.ncu-rep" --page details > "$OUT/ncu_${name}_details.txt" 2>/dev/null
+    ncu -i "$OUT/ncu_$name.ncu-rep" --page source --csv > "$OUT/ncu_${name}_source.csv" 2>/dev/null
+    rm -f "$OUT/ncu_$name.ncu-rep"
+  fi
 }
 cap c1 xmarch 512x512x64 --n 4
 cap c2 xmarch 1024x1024x64 --n 4
@@ -39,3 +48,4 @@ cap pull xmarch 512x256x64 --n 4 --pull
 cap ct ctile 256x256x512 --n 4
 cap ctodd ctile 512x512x63 --n 4
 ls -la "$OUT" > "$OUT/ls.txt"
+du -sh "$OUT" >> "$OUT/ls.txt"
