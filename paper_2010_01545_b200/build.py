@@ -13,8 +13,13 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libpwadv.so"
 TRAFFIC_LIB = PKG / "libpwadv_traffic.so"  # optional: live DRAM counters (CUPTI)
 TRAFFIC_SRC = "pwadv_traffic.cpp"
-SOURCES = ["pwadv_advect.cu", "pwadv_aux.cu", "pwadv_roles.cu", "pwadv_api.cu", "pwadv_sync.cu"]
-HEADERS = ["pwadv_device.cuh", "pwadv_internal.h"]
+# translation units, compiled in parallel (the kernel instantiations are split
+# over the pwadv_k_* units so no single nvcc run dominates the build)
+SOURCES = ["pwadv_k_small.cu", "pwadv_k_ct.cu", "pwadv_k_nzc2.cu", "pwadv_k_pull.cu", "pwadv_k_ws.cu",
+           "pwadv_k_nzc0.cu", "pwadv_k_nzc1.cu", "pwadv_k_ctodd.cu", "pwadv_advect.cu", "pwadv_api.cu",
+           "pwadv_aux.cu", "pwadv_roles.cu", "pwadv_sync.cu"]
+HEADERS = ["pwadv_device.cuh", "pwadv_internal.h", "pwadv_xmarch.cuh", "pwadv_ctile.cuh", "pwadv_kernels.h"]
+OBJ = PKG.parent / "build" / "obj"
 
 
 def nvcc_path() -> str:
@@ -86,17 +91,30 @@ def build_traffic(force: bool = False) -> Path | None:
     return TRAFFIC_LIB
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not stale():
-        return LIB
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc_path(), *nvcc_flags(verbose), "-shared", "-o", str(tmp),
-           *[str(CSRC / s) for s in SOURCES]]
+def _nvcc(cmd: list[str], verbose: bool) -> None:
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
     if verbose:
         sys.stderr.write(res.stderr)
+
+
+def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> Path:
+    """Compile every translation unit for sm_100a (in parallel, `jobs` nvcc
+    processes, default: the host's cores) and link libpwadv.so in-tree."""
+    if not force and not stale():
+        return LIB
+    from concurrent.futures import ThreadPoolExecutor
+    OBJ.mkdir(parents=True, exist_ok=True)
+    objs = [OBJ / (Path(s).stem + ".o") for s in SOURCES]
+    flags = nvcc_flags(verbose)
+    with ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as pool:
+        for f in [pool.submit(_nvcc, [nvcc_path(), *flags, "-c", "-o", str(o), str(CSRC / s)], verbose)
+                  for s, o in zip(SOURCES, objs)]:
+            f.result()
+    tmp = LIB.with_suffix(".so.tmp")
+    _nvcc([nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
+           *[str(o) for o in objs]], verbose)
     os.replace(tmp, LIB)
     return LIB
 

@@ -480,6 +480,10 @@ def test_async_host_submissions_bitwise():
     ctx.close()
 
 
+# depths with a compile-time whole-column layout (pwadv_k_nzc*.cu, has_nzc)
+NZC_DEPTHS = set(range(16, 129, 8)) | {100}
+
+
 def _ctile_kt(nz):
     best, kt = None, 128
     for c, pref in ((128, 1.0), (96, 1.0), (64, 1.01), (48, 1.01), (32, 1.07)):
@@ -497,8 +501,7 @@ def default_kernel(ny, nz):
     model fitted to the round-2 measurements: odd nz takes column tiles from
     255 up, and below when ny is even and a slab is >= 90% busy, else the UA
     form; even nz compares busy fraction x strip-width x layout factors (the
-    whole-column tile has a compile-time layout only at nz 32 / 48 / 64 / 96 /
-    128)."""
+    whole-column tile has a compile-time layout only at NZC_DEPTHS)."""
     kt = _ctile_kt(nz)
     if nz % 2:
         if nz >= 255 or (ny % 2 == 0 and nz >= 0.9 * (-(-(nz + 1) // kt) * kt)):
@@ -509,7 +512,7 @@ def default_kernel(ny, nz):
     if kp > 384:
         return "xmarch_ct"
     tj = 384 // kp
-    layout = 1.0 if nz in (32, 48, 64, 96, 128) else 0.92
+    layout = 1.0 if nz in NZC_DEPTHS else 0.92
     whole = tj * kp / 384 * (1.0 if tj >= 6 else [0, 0.8, 0.9, 0.93, 0.95, 0.97][tj]) * layout
     return "xmarch_ct" if ct > whole else "xmarch"
 
@@ -517,8 +520,8 @@ def default_kernel(ny, nz):
 def test_default_kernel_mirror_pins_measured_choices():
     # the decisions the round-2 measurements made (profiles/r02_monc_depths.jsonl,
     # r02_shape_sweep_ct.jsonl, r02_ct_odd_nz.jsonl)
-    assert [default_kernel(512, nz) for nz in (64, 80, 96, 100, 128, 150)] == ["xmarch"] * 6
-    assert {default_kernel(512, nz) for nz in (110, 120, 130, 140, 160, 190, 256, 270, 512, 1024,
+    assert [default_kernel(512, nz) for nz in (64, 80, 96, 100, 104, 120, 128, 150)] == ["xmarch"] * 8
+    assert {default_kernel(512, nz) for nz in (110, 130, 140, 160, 190, 256, 270, 512, 1024,
                                                1030)} == {"xmarch_ct"}
     assert [default_kernel(512, nz) for nz in (63, 127, 255)] == ["xmarch_ct"] * 3
     assert [default_kernel(511, 63), default_kernel(512, 33), default_kernel(512, 95)] == ["xmarch_elem"] * 3

@@ -29,7 +29,8 @@ def main():
     rng = np.random.default_rng(a.seed)
     bad, done = [], 0
     for n in range(a.cases):
-        nz = int(rng.choice([2, 3, 5, 8, 16, 31, 32, 33, 48, 63, 64, 65, 96, 99, 110, 127, 128, 160, 200, 257,
+        nz = int(rng.choice([2, 3, 5, 8, 16, 24, 31, 32, 33, 40, 48, 56, 63, 64, 65, 72, 88, 96, 99, 100,
+                              104, 110, 112, 120, 127, 128, 160, 200, 257,
                               300, 514, 1030]))
         nx = int(rng.integers(1, 90))
         ny = int(rng.integers(1, 400 if nz <= 64 else (120 if nz <= 300 else 40)))
