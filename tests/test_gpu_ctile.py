@@ -157,3 +157,20 @@ def test_compile_time_depths_every_plane(nz):
     torch.cuda.synchronize()
     r = oracle.compare_streamed(fields, nxt, co.tcx, co.tcy, co.tzc1, co.tzc2, dt=0.1)
     assert r["bitwise_equal"], r
+
+
+@pytest.mark.parametrize("shape", [(1024, 512, 256), (512, 514, 255), (256, 256, 2048)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_ctile_large_grids_every_plane(shape):
+    """K1c at full size (134-136M points; even slabs, odd nz pair rows,
+    2048-level columns in 16 slabs): the default plan, every plane of su, sv,
+    sw against the streamed C oracle, bitwise."""
+    nx, ny, nz = shape
+    dims = pw.make_grid(nx, ny, nz)
+    assert device.describe_plan(dims)["kernel"] == "xmarch_ct"
+    fields = device.fill(dims, pw.GeneratorSpec.baseline(21))
+    co = pw.baseline_coefficients(21, nz)
+    out = device.advect(*fields, co)
+    torch.cuda.synchronize()
+    r = oracle.compare_streamed(fields, out, co.tcx, co.tcy, co.tzc1, co.tzc2, slab=32)
+    assert r["bitwise_equal"] and r["planes_checked"] == nx, r
