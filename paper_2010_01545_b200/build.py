@@ -16,7 +16,7 @@ TRAFFIC_SRC = "pwadv_traffic.cpp"
 # translation units, compiled in parallel (the kernel instantiations are split
 # over the pwadv_k_* units so no single nvcc run dominates the build)
 SOURCES = ["pwadv_k_small.cu", "pwadv_k_ct.cu", "pwadv_k_nzc2.cu", "pwadv_k_pull.cu", "pwadv_k_ws.cu",
-           "pwadv_k_nzc0.cu", "pwadv_k_nzc1.cu", "pwadv_k_ctodd.cu", "pwadv_advect.cu", "pwadv_api.cu",
+           "pwadv_k_nzc0.cu", "pwadv_k_nzc1.cu", "pwadv_k_nzc3.cu", "pwadv_k_ctodd.cu", "pwadv_advect.cu", "pwadv_api.cu",
            "pwadv_aux.cu", "pwadv_roles.cu", "pwadv_sync.cu"]
 HEADERS = ["pwadv_device.cuh", "pwadv_internal.h", "pwadv_xmarch.cuh", "pwadv_ctile.cuh", "pwadv_kernels.h"]
 OBJ = PKG.parent / "build" / "obj"

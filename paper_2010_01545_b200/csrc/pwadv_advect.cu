@@ -494,8 +494,11 @@ static bool ctile_pays(int64_t nz, int64_t ny)
     // costs ~8% at equal occupancy
     // (nz 110 / 120: 117 / 122 Gpts/s against K1c's 128 / 131 with the same
     // busy fraction; profiles/r02_monc_depths.jsonl)
-    const double layout = has_nzc((int)nz) ? 1.0 : 0.92;
-    const double whole = (double)(tj * kp) / 384.0 * (tj >= 6 ? 1.0 : width[tj]) * layout;
+    // (with a compile-time layout the narrow strips cost nothing measurable
+    // down to TJ = 4: nz 192 at 133.6 Gpts/s, 152 at 128-131 — the width
+    // factors are the run-time layout's)
+    const double whole = (double)(tj * kp) / 384.0 *
+                         (has_nzc((int)nz) ? 1.0 : (tj >= 6 ? 1.0 : width[tj]) * 0.92);
     return ct > whole;
 }
 

@@ -37,6 +37,14 @@ bool has_nzc(int nz)
     case 112:
     case 120:
     case 128:
+    case 136:
+    case 144:
+    case 152:
+    case 160:
+    case 168:
+    case 176:
+    case 184:
+    case 192:
         return true;
     default:
         return false;
@@ -47,7 +55,8 @@ XmarchKern kern_xmarch_nzc(int nz, bool step, bool fma)
 {
     if (XmarchKern k = kern_nzc_part0(nz, step, fma)) return k;
     if (XmarchKern k = kern_nzc_part1(nz, step, fma)) return k;
-    return kern_nzc_part2(nz, step, fma);
+    if (XmarchKern k = kern_nzc_part2(nz, step, fma)) return k;
+    return kern_nzc_part3(nz, step, fma);
 }
 
 }  // namespace pwadv

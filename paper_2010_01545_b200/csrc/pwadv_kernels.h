@@ -26,6 +26,7 @@ CtileKern kern_ctile(int kt, bool odd, bool step, bool fma);
 XmarchKern kern_nzc_part0(int nz, bool step, bool fma);
 XmarchKern kern_nzc_part1(int nz, bool step, bool fma);
 XmarchKern kern_nzc_part2(int nz, bool step, bool fma);
+XmarchKern kern_nzc_part3(int nz, bool step, bool fma);
 CtileKern kern_ctile_even(int kt, bool step, bool fma);
 CtileKern kern_ctile_odd(int kt, bool step, bool fma);
 XmarchKern kern_generic_small(int maxt, bool fix, bool step, bool fma);

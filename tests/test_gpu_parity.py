@@ -481,7 +481,7 @@ def test_async_host_submissions_bitwise():
 
 
 # depths with a compile-time whole-column layout (pwadv_k_nzc*.cu, has_nzc)
-NZC_DEPTHS = set(range(16, 129, 8)) | {100}
+NZC_DEPTHS = set(range(16, 193, 8)) | {100}
 
 
 def _ctile_kt(nz):
@@ -512,17 +512,20 @@ def default_kernel(ny, nz):
     if kp > 384:
         return "xmarch_ct"
     tj = 384 // kp
-    layout = 1.0 if nz in NZC_DEPTHS else 0.92
-    whole = tj * kp / 384 * (1.0 if tj >= 6 else [0, 0.8, 0.9, 0.93, 0.95, 0.97][tj]) * layout
+    if nz in NZC_DEPTHS:
+        whole = tj * kp / 384
+    else:
+        whole = tj * kp / 384 * (1.0 if tj >= 6 else [0, 0.8, 0.9, 0.93, 0.95, 0.97][tj]) * 0.92
     return "xmarch_ct" if ct > whole else "xmarch"
 
 
 def test_default_kernel_mirror_pins_measured_choices():
     # the decisions the round-2 measurements made (profiles/r02_monc_depths.jsonl,
     # r02_shape_sweep_ct.jsonl, r02_ct_odd_nz.jsonl)
-    assert [default_kernel(512, nz) for nz in (64, 80, 96, 100, 104, 120, 128, 150)] == ["xmarch"] * 8
-    assert {default_kernel(512, nz) for nz in (110, 130, 140, 160, 190, 256, 270, 512, 1024,
-                                               1030)} == {"xmarch_ct"}
+    assert [default_kernel(512, nz) for nz in (64, 80, 96, 100, 104, 120, 128, 150, 152, 176,
+                                               192)] == ["xmarch"] * 11
+    assert {default_kernel(512, nz) for nz in (110, 130, 136, 140, 144, 160, 190, 256, 270, 512,
+                                               1024, 1030)} == {"xmarch_ct"}
     assert [default_kernel(512, nz) for nz in (63, 127, 255)] == ["xmarch_ct"] * 3
     assert [default_kernel(511, 63), default_kernel(512, 33), default_kernel(512, 95)] == ["xmarch_elem"] * 3
 

@@ -30,7 +30,7 @@ def main():
     bad, done = [], 0
     for n in range(a.cases):
         nz = int(rng.choice([2, 3, 5, 8, 16, 24, 31, 32, 33, 40, 48, 56, 63, 64, 65, 72, 88, 96, 99, 100,
-                              104, 110, 112, 120, 127, 128, 160, 200, 257,
+                              104, 110, 112, 120, 127, 128, 136, 152, 160, 176, 192, 200, 257,
                               300, 514, 1030]))
         nx = int(rng.integers(1, 90))
         ny = int(rng.integers(1, 400 if nz <= 64 else (120 if nz <= 300 else 40)))
