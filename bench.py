@@ -581,17 +581,17 @@ def run_ours(args):
     # captured with the very libpwadv.so loaded here (build hash)
     key = f"{args.config}:{args.variant}:{nx}x{ny}x{nz}"
     tr = ncu_traffic(key) or {}
-    if tr and tr.get("lib_sha16") != _lib.build_id():
+    if tr and tr.get("build_id") != _lib.build_id():
         tr = {}
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4),
                 "traffic": live.get("dram_bytes") if live else None,
                 "traffic_source": live.get("source") if live else None,
                 "traffic_live": live,
-                "lib_sha16": _lib.build_id(),
+                "build_id": _lib.build_id(),
                 "ncu": ({k: tr.get(k) for k in ("duration_us", "dram_read", "dram_write",
                                                 "dram_throughput_pct", "fp64_pipe_pct",
-                                                "issue_active_pct", "registers", "lib_sha16",
+                                                "issue_active_pct", "registers", "build_id",
                                                 "source")} if tr else None),
                 "peak_source": peak_src, "kernel_ms": round(kern_ms, 5),
                 "algorithmic_bytes_per_launch": BYTES_PER_POINT * pts_rank,

@@ -99,6 +99,11 @@ typedef struct pwadv_opts {
 } pwadv_opts;
 
 int pwadv_abi_version(void);
+/* Identity of the build: 16 hex digits of the sha256 over the library's
+ * sources, headers and nvcc flags (build.py), fixed at compile time. nvcc
+ * object code is not bit-reproducible (per-compilation module ids), so
+ * profiles are stamped with this instead of a hash of the binary. */
+const char *pwadv_source_id(void);
 const char *pwadv_last_error(void);
 
 /* Launch-count instrumentation: kernels launched by this library on the

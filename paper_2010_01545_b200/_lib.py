@@ -81,6 +81,7 @@ NB_XM, NB_XP, NB_YM, NB_YP, NB_XMYM, NB_XMYP, NB_XPYM, NB_XPYP = range(8)
 # name -> (restype, argtypes); every symbol include/pwadv.h declares
 SIGNATURES = {
     "pwadv_abi_version": (ctypes.c_int, []),
+    "pwadv_source_id": (ctypes.c_char_p, []),
     "pwadv_last_error": (ctypes.c_char_p, []),
     "pwadv_launch_count": (ctypes.c_uint64, []),
     "pwadv_reset_launch_count": (None, []),
@@ -166,12 +167,14 @@ _build_id = None
 
 
 def build_id() -> str:
-    """sha256 (first 16 hex) of the libpwadv.so this process loads: stamps
-    profiles (profiles/ncu_traffic.json) to the build they were taken with."""
+    """The source id compiled into the libpwadv.so this process loads
+    (pwadv_source_id: sha256 over its sources, headers and nvcc flags, see
+    build.source_id): stamps profiles (profiles/ncu_traffic.json) to the build
+    they were taken with. Not a hash of the binary — nvcc output differs from
+    build to build of the same sources (per-compilation module ids)."""
     global _build_id
     if _build_id is None:
-        import hashlib
-        _build_id = hashlib.sha256(LIB_PATH.read_bytes()).hexdigest()[:16]
+        _build_id = lib().pwadv_source_id().decode()
     return _build_id
 
 

@@ -99,6 +99,19 @@ def _nvcc(cmd: list[str], verbose: bool) -> None:
         sys.stderr.write(res.stderr)
 
 
+def source_id(extra: list[str] | None = None) -> str:
+    """16 hex digits of the sha256 over every source and header of libpwadv
+    and the nvcc flags: compiled into the library (pwadv_source_id)."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted(SOURCES + HEADERS):
+        h.update(f.encode())
+        h.update((CSRC / f).read_bytes())
+    h.update((PKG.parent / "include" / "pwadv.h").read_bytes())
+    h.update(" ".join(nvcc_flags() + list(extra or [])).encode())
+    return h.hexdigest()[:16]
+
+
 def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> Path:
     """Compile every translation unit for sm_100a (in parallel, `jobs` nvcc
     processes, default: the host's cores) and link libpwadv.so in-tree."""
@@ -107,7 +120,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> Path:
     from concurrent.futures import ThreadPoolExecutor
     OBJ.mkdir(parents=True, exist_ok=True)
     objs = [OBJ / (Path(s).stem + ".o") for s in SOURCES]
-    flags = nvcc_flags(verbose)
+    flags = nvcc_flags(verbose) + [f'-DPWADV_SOURCE_ID="{source_id()}"']
     with ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as pool:
         for f in [pool.submit(_nvcc, [nvcc_path(), *flags, "-c", "-o", str(o), str(CSRC / s)], verbose)
                   for s, o in zip(SOURCES, objs)]:

@@ -150,6 +150,11 @@ struct DeviceGuard {
 extern "C" {
 
 int pwadv_abi_version(void) { return PWADV_ABI_VERSION; }
+
+#ifndef PWADV_SOURCE_ID
+#define PWADV_SOURCE_ID "unknown"
+#endif
+const char *pwadv_source_id(void) { return PWADV_SOURCE_ID; }
 const char *pwadv_last_error(void) { return g_err; }
 uint64_t pwadv_launch_count(void) { return g_launches; }
 void pwadv_reset_launch_count(void) { g_launches = 0; }

@@ -22,7 +22,9 @@ def main():
     from concurrent.futures import ThreadPoolExecutor
     objs = [obj / (Path(s).stem + ".o") for s in B.SOURCES]
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as pool:
-        for f in [pool.submit(subprocess.run, [B.nvcc_path(), *B.nvcc_flags(), *defines, "-c", "-o", str(o),
+        sid = B.source_id(defines)
+        for f in [pool.submit(subprocess.run, [B.nvcc_path(), *B.nvcc_flags(), *defines,
+                                               f'-DPWADV_SOURCE_ID="{sid}"', "-c", "-o", str(o),
                                                str(B.CSRC / s)], check=True)
                   for s, o in zip(B.SOURCES, objs)]:
             f.result()

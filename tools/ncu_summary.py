@@ -43,7 +43,7 @@ def summarise(key, rep, rnd="r02"):
     # the entry only while the loaded library has the same hash
     sys.path.insert(0, str(ROOT))
     from paper_2010_01545_b200 import _lib
-    out["lib_sha16"] = _lib.build_id()
+    out["build_id"] = _lib.build_id()
     dst.write_text(raw)
     return out
 
