@@ -108,7 +108,9 @@ def source_id(extra: list[str] | None = None) -> str:
         h.update(f.encode())
         h.update((CSRC / f).read_bytes())
     h.update((PKG.parent / "include" / "pwadv.h").read_bytes())
-    h.update(" ".join(nvcc_flags() + list(extra or [])).encode())
+    # the flags without the (checkout-dependent) include path
+    flags = [f for f in nvcc_flags() if not f.startswith(str(PKG.parent))]
+    h.update(" ".join(flags + list(extra or [])).encode())
     return h.hexdigest()[:16]
 
 
