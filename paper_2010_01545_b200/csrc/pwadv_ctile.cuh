@@ -1,6 +1,6 @@
-// pwadv_ctile.cuh — K1c: the X-march with column tiles (k-slabs), included by
-// pwadv_advect.cu after k_advect_xmarch (it shares BoxArgs, TileCfg, unit_at,
-// RingState and the ring protocol).
+// pwadv_ctile.cuh — K1c: the X-march with column tiles (k-slabs), included at
+// the end of pwadv_xmarch.cuh (it shares BoxArgs, TileCfg, unit_at, RingState
+// and the ring protocol with k_advect_xmarch); instantiated in pwadv_k_ct*.cu.
 //
 // k_advect_xmarch stages a whole column height per plane tile, so deep
 // columns shrink its strip (TJ = 384 / (nz/2): nz = 512 leaves one column per
@@ -94,17 +94,19 @@ __device__ __forceinline__ void tma_load_2d(void *dst_smem, const CUtensorMap *m
 // nz + kb - 3: a box row must start on a 16-byte boundary, so an odd column's
 // staged copy sits one level higher in its slot). A tile column's half and row
 // follow from the parity of G0, which flips from plane to plane when ny+2 is
-// odd, so the consumers select their column offsets per plane. Every thread
-// keeps its pair at even levels (kb + 2 kp); a pair of an odd column is off
-// the 16-byte grid in its slot and is read with two 8-byte loads (measured
-// faster than the aligned (k0-1, k0) realigned by a shuffle) — the choice is
-// warp-uniform because one column parity owns a warp (KT >= 64, plan_ctile),
-// and compile-time per unit when ny+2 is even (run_unit's QV). In
-// global memory a pair is 16-byte aligned on even global columns only (g nz +
-// k0 even) — odd columns store scalars — and the top level nz - 1 is the first
-// of its pair. Levels a box reads past its column (the other column of the
-// pair, or the zero fill) feed only operands of levels that are not stored,
-// the zeroed level 0, or the top formula's unread k+1.
+// odd, so the consumers select their column offsets per plane. Two pairings
+// (run_unit's QV): when ny+2 is even a column's parity is fixed over a unit
+// and an odd column's pairs start at odd levels (kb - 1 + 2kp) — its own pairs
+// and all stores are on the 16-byte grid, only the neighbouring columns' pairs
+// are off it (slot shift -1 / +1), read with two 8-byte loads; when ny+2 is odd
+// every pair starts at an even level (kb + 2kp) and an odd column's own pairs
+// are off the grid (8-byte loads, scalar stores). Either choice is warp-
+// uniform (one column parity owns a warp: KT 64 / 128, plan_ctile). The top
+// level nz - 1 is the first or second level of its pair, level 0 may be a
+// shifted pair's second level (the first, level -1, is not stored). Levels a
+// box reads past its column (the other column of the pair, or the zero fill)
+// feed only operands of levels that are not stored, the zeroed level 0, or the
+// top formula's unread k+1.
 template <bool FMA, bool STEP, int KT, bool ODD>
 __global__ void __launch_bounds__(512, 1)
     k_advect_ctile(const __grid_constant__ BoxArgs a, const __grid_constant__ TileCfg t,
