@@ -57,13 +57,14 @@ def main():
         fu = device.fill(du, pw.GeneratorSpec.baseline(5))
         cou = device.DeviceCoefficients.from_host(pw.baseline_coefficients(5, 63), "cuda")
         outu = device.alloc_fields(du, "cuda")
-        device.advect(*fu, cou, outu)
+        ua = device.make_opts("xmarch_elem")  # forced: the default plan here is K1c's pair rows
+        device.advect(*fu, cou, outu, opts=ua)
         ref = digest(outu)
         n_ua = max(1, a.launches // 4)
         bad = 0
         t = time.perf_counter()
         for n in range(n_ua):
-            device.advect(*fu, cou, outu)
+            device.advect(*fu, cou, outu, opts=ua)
             if n % 1000 == 999:
                 bad += digest(outu) != ref
         torch.cuda.synchronize()
