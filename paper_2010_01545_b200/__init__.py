@@ -2,10 +2,10 @@
 
 Import surface mirrors the reference package facade for the hot path
 (pkg/src/pwadvect/__init__.py:11-34: grid, kernel and schedules names; the
-submodules `grid`, `kernel` and `schedules` mirror the reference modules of
-those names) and adds the device-resident API (`device`), the x-y
-decomposition with halo exchange (`decomp`) and the fused time-stepping
-driver (`stepper`).
+reference's module paths `.grid`, `.kernel` and `.schedules` resolve to
+`layout`, `stencil` and `engines` — registered below, no wrapper files) and
+adds the device-resident API (`device`), the x-y decomposition with halo
+exchange (`decomp`) and the fused time-stepping driver (`stepper`).
 All compute runs in libpwadv.so (hand-written sm_100a CUDA); there is no CPU
 fallback.
 """
@@ -19,5 +19,14 @@ from .stencil import (COMPUTE_ROLES, AdvectionCoefficients, FlopProfile, advect_
                       run_reference)
 from .engines import (VARIANTS, OutputComparison, ScheduleSpec, Slab, TrafficReport,
                       compare_outputs, partition_domain, run_schedule)
+
+import sys as _sys
+
+from . import engines as _engines, layout as _layout, stencil as _stencil
+
+for _name, _mod in (("grid", _layout), ("kernel", _stencil), ("schedules", _engines)):
+    _sys.modules[f"{__name__}.{_name}"] = _mod
+    globals()[_name] = _mod
+del _name, _mod
 
 __version__ = "0.1.0"

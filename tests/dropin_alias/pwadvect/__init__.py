@@ -3,7 +3,8 @@ test files unchanged (tests/test_gpu_reference_suite.py).
 
 The hot-path modules `pwadvect.grid`, `pwadvect.kernel` and
 `pwadvect.schedules` ARE this repository's package
-(paper_2010_01545_b200.grid / .kernel / .schedules): every stencil
+(paper_2010_01545_b200.layout / .stencil / .engines, registered by the
+package under the module paths .grid / .kernel / .schedules): every stencil
 evaluation, generator fill and schedule run goes to libpwadv.so on the GPU.
 The out-of-scope FPGA modelling modules (dataflow, transfer, params, refdata,
 cli — SURVEY.md §2) are loaded unmodified from the stock reference installed
