@@ -588,6 +588,9 @@ def run_ours(args):
                 "traffic": live.get("dram_bytes") if live else None,
                 "traffic_source": live.get("source") if live else None,
                 "traffic_live": live,
+                # fp64-pipe utilisation of the same launch, live (north star: "also reports
+                # fp64 pipe utilisation"); the kernel is HBM-bound, so this is headroom
+                "fp64_pipe_pct": round(live["fp64_pipe_pct"], 2) if live and "fp64_pipe_pct" in live else None,
                 "build_id": _lib.build_id(),
                 "ncu": ({k: tr.get(k) for k in ("duration_us", "dram_read", "dram_write",
                                                 "dram_throughput_pct", "fp64_pipe_pct",

@@ -33,9 +33,15 @@
 
 namespace {
 
-const char *kMetrics[] = {"dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"};
+// out[] order of pwadv_traffic_end; the fp64-pipe percentage is combined over
+// ranges weighted by each range's duration, the other values are summed
+const char *kMetrics[] = {"dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+                          "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+                          "sm__inst_executed_pipe_fp64.sum"};
+constexpr size_t kTimeMetric = 2, kPctMetric = 3;
 constexpr size_t kNumMetrics = sizeof(kMetrics) / sizeof(kMetrics[0]);
 constexpr size_t kMaxRanges = 256;
+static_assert(kNumMetrics == PWADV_TRAFFIC_NVALUES, "pwadv_traffic.h out[] layout");
 
 thread_local char g_err[512];
 
@@ -228,8 +234,10 @@ int end_locked(double *out, int *nranges)
         ev.rangeIndex = r;
         ev.pMetricValues = v;
         CUPTI_TRY(cuptiProfilerHostEvaluateToGpuValues(&ev));
-        for (size_t m = 0; m < kNumMetrics; ++m) out[m] += v[m];
+        for (size_t m = 0; m < kNumMetrics; ++m)
+            out[m] += m == kPctMetric ? v[m] * v[kTimeMetric] : v[m];
     }
+    out[kPctMetric] = out[kTimeMetric] > 0.0 ? out[kPctMetric] / out[kTimeMetric] : 0.0;
     *nranges = (int)gi.numTotalRanges;
     return 0;
 }
@@ -249,10 +257,12 @@ int pwadv_traffic_begin(int device)
     return rc;
 }
 
-// Stop counting (the caller has synchronised its launches). out[0] = DRAM
-// bytes read, out[1] = DRAM bytes written, out[2] = summed kernel duration in
-// ns, all summed over the *nranges kernels launched since begin.
-int pwadv_traffic_end(double out[3], int *nranges)
+// Stop counting (the caller has synchronised its launches). Over the *nranges
+// kernels launched since begin: out[0] = DRAM bytes read, out[1] = DRAM bytes
+// written, out[2] = summed kernel duration in ns, out[3] = fp64-pipe active
+// cycles in % of peak (duration-weighted mean), out[4] = fp64 warp
+// instructions executed.
+int pwadv_traffic_end(double out[PWADV_TRAFFIC_NVALUES], int *nranges)
 {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!g_s.active) return fail("no active traffic session");
@@ -268,5 +278,7 @@ int pwadv_traffic_end(double out[3], int *nranges)
 const char *pwadv_traffic_last_error(void) { return g_err; }
 
 int pwadv_traffic_max_ranges(void) { return (int)kMaxRanges; }
+
+int pwadv_traffic_num_values(void) { return (int)kNumMetrics; }
 
 }  // extern "C"

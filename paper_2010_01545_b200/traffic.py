@@ -44,6 +44,8 @@ def lib():
             L.pwadv_traffic_last_error.restype = ctypes.c_char_p
             L.pwadv_traffic_max_ranges.argtypes = []
             L.pwadv_traffic_max_ranges.restype = ctypes.c_int
+            L.pwadv_traffic_num_values.argtypes = []
+            L.pwadv_traffic_num_values.restype = ctypes.c_int
             _lib = L
         return _lib
 
@@ -81,17 +83,19 @@ def measure(fn, *, plan_bytes: float | None = None, device: int | None = None,
             fn()
             torch.cuda.synchronize()
         finally:
-            vals = (ctypes.c_double * 3)()
+            vals = (ctypes.c_double * L.pwadv_traffic_num_values())()
             n = ctypes.c_int(0)
             rc = L.pwadv_traffic_end(vals, ctypes.byref(n))
         if rc != 0:
             raise TrafficUnavailable(_err(L))
-    rd, wr, ns = float(vals[0]), float(vals[1]), float(vals[2])
+    rd, wr, ns, fp64_pct, fp64_inst = (float(x) for x in vals[:5])
     out = {"dram_read_bytes": rd, "dram_write_bytes": wr, "dram_bytes": rd + wr,
            "kernel_us": ns / 1e3, "kernels": int(n.value),
+           "fp64_pipe_pct": fp64_pct, "fp64_warp_inst": fp64_inst,
            "l2": "flushed before the launches" if flush else "as left by previous launches",
-           "source": "CUPTI range profiler (dram__bytes_read.sum + dram__bytes_write.sum), "
-                     "libpwadv_traffic.so"}
+           "source": "CUPTI range profiler (dram__bytes_read.sum + dram__bytes_write.sum; "
+                     "fp64 pipe: sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active, "
+                     "sm__inst_executed_pipe_fp64.sum), libpwadv_traffic.so"}
     if plan_bytes:
         out["plan_bytes"] = float(plan_bytes)
         out["ratio_to_plan"] = (rd + wr) / float(plan_bytes)

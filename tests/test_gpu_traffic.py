@@ -30,6 +30,11 @@ def test_k1_c1_dram_bytes_near_plan():
     assert 0.70 * 24 * dims.cells <= r["dram_write_bytes"] <= 1.05 * 24 * dims.cells, r
     assert 0.8 <= r["ratio_to_plan"] <= 1.1, r
     assert r["kernel_us"] > 50, r
+    # fp64 pipe (no tensor cores: not a contraction): busy but not the bound;
+    # the census is 63 flop per point (operation_census), carried sums reuse
+    # some of them across levels, every flop is one lane of a DADD/DMUL
+    assert 20.0 <= r["fp64_pipe_pct"] <= 100.0, r
+    assert 20 * dims.cells / 32 <= r["fp64_warp_inst"] <= 130 * dims.cells / 32, r
 
 
 def test_sum_over_several_launches_and_step():
@@ -44,6 +49,7 @@ def test_sum_over_several_launches_and_step():
     r = traffic.measure(three, plan_bytes=3 * 48 * dims.cells)
     assert r["kernels"] == 3, r
     assert r["dram_read_bytes"] > 0 and r["dram_write_bytes"] > 0
+    assert 0.0 < r["fp64_pipe_pct"] <= 100.0 and r["fp64_warp_inst"] > 0, r
 
 
 def test_run_schedule_reports_measured_traffic():

@@ -21,8 +21,8 @@ from tests.golden_data import GOLDEN
 ROOT = Path(__file__).resolve().parent.parent
 
 
-def header_functions():
-    text = (ROOT / "include" / "pwadv.h").read_text()
+def header_functions(name="pwadv.h"):
+    text = (ROOT / "include" / name).read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(pwadv_[a-z0-9_]+)\s*\(", text)))
 
@@ -36,6 +36,36 @@ def test_library_exports_every_header_symbol():
         assert n in _lib.SIGNATURES, f"{n} missing from the ctypes binding"
     assert set(_lib.SIGNATURES) == set(names)
     assert L.pwadv_abi_version() == _lib.ABI_VERSION
+
+
+def test_traffic_library_exports_every_header_symbol():
+    """include/pwadv_traffic.h against libpwadv_traffic.so (the optional CUPTI
+    counters library). Its exports are read with nm (it links libcuda, absent
+    without a driver); where it loads, the value count and the no-session
+    error are checked too, without touching a GPU."""
+    import subprocess
+    from paper_2010_01545_b200 import traffic
+    if not traffic._LIB.exists():
+        pytest.skip("libpwadv_traffic.so not built")
+    names = header_functions("pwadv_traffic.h")
+    assert names == ["pwadv_traffic_begin", "pwadv_traffic_end", "pwadv_traffic_last_error",
+                     "pwadv_traffic_max_ranges", "pwadv_traffic_num_values"]
+    nm = subprocess.run(["nm", "-D", "--defined-only", str(traffic._LIB)], capture_output=True,
+                        text=True, check=True).stdout
+    exported = {line.split()[-1] for line in nm.splitlines() if " T " in line}
+    assert set(names) <= exported, set(names) - exported
+    nvals = int(re.search(r"PWADV_TRAFFIC_NVALUES\s+(\d+)",
+                          (ROOT / "include" / "pwadv_traffic.h").read_text()).group(1))
+    assert nvals == 5
+    try:
+        L = traffic.lib()
+    except OSError:
+        return
+    assert L.pwadv_traffic_num_values() == nvals
+    assert L.pwadv_traffic_max_ranges() >= 1
+    vals, n = (ctypes.c_double * nvals)(), ctypes.c_int(0)
+    assert L.pwadv_traffic_end(vals, ctypes.byref(n)) == -1
+    assert b"no active traffic session" in L.pwadv_traffic_last_error()
 
 
 def test_library_is_sm100a_cubin():
