@@ -290,8 +290,9 @@ def step_barrier(dec, dev, stream):
         ok = ev.query()
         if not ok:
             err = "probe handshake did not complete within 5 s"
-    except _lib.PwadvError as exc:
-        err = str(exc)
+    except Exception as exc:  # any failure on this rank: all ranks fall back together
+        err = f"{type(exc).__name__}: {exc}"
+        ok = False
     if agree_all(ok, dev):
         return hs, "neighbour flag handshake (stream memory ops, NVLink)"
     if hs is not None:
@@ -400,6 +401,15 @@ def run_ours(args):
                 st = decomp.PushStepper(dec, fields, co, 0.1, decomp.IpcPeerRegistry(dec),
                                         barrier, opts=opts,
                                         initial_exchange=lambda f: exch.exchange(f, stream=stream))
+            except Exception as exc:
+                err = f"{type(exc).__name__}: {exc}"
+            # every rank mapped its neighbours' buffers before any rank's first
+            # fused step waits on them
+            if not agree_all(err is None, dev):
+                err = err or "setup failed on another rank"
+            try:
+                if err is not None:
+                    raise RuntimeError(err)
                 st.step(1, stream=stream)
                 ref_out = device.alloc_fields(dims, dev)
                 exch.step_overlapped(st.sets[0], co, 0.1, ref_out, opts=opts, stream=stream)
@@ -413,8 +423,8 @@ def run_ours(args):
                     err = "fused step differs from the NCCL-exchange step"
                 elif not rank_parity["bitwise_equal"]:
                     err = f"fused step differs from the oracle: {rank_parity}"
-            except _lib.PwadvError as exc:
-                err = str(exc)
+            except Exception as exc:
+                err = err or f"{type(exc).__name__}: {exc}"
             if agree_all(err is None, dev):
                 step_path = f"K4 + peer stores (CUDA IPC) + {barrier_kind}"
 
@@ -443,6 +453,13 @@ def run_ours(args):
             try:
                 ev = decomp.PullEvaluator(dec, fields, co, decomp.IpcPeerRegistry(dec),
                                           barrier, opts=opts)
+            except Exception as exc:
+                err = f"{type(exc).__name__}: {exc}"
+            if not agree_all(err is None, dev):
+                err = err or "setup failed on another rank"
+            try:
+                if err is not None:
+                    raise RuntimeError(err)
                 ev.evaluate(out, stream=stream)
                 ref_out = device.alloc_fields(dims, dev)
                 exch.advect_overlapped(fields, co, ref_out, opts=opts, stream=stream)
@@ -457,8 +474,8 @@ def run_ours(args):
                     err = "pulled evaluation differs from the NCCL-exchange evaluation"
                 elif not rank_parity["bitwise_equal"]:
                     err = f"pulled evaluation differs from the oracle: {rank_parity}"
-            except _lib.PwadvError as exc:
-                err = str(exc)
+            except Exception as exc:
+                err = err or f"{type(exc).__name__}: {exc}"
             if agree_all(err is None, dev):
                 step_path = f"K1 with halo pull (peer loads over NVLink, CUDA IPC) + {barrier_kind}"
 

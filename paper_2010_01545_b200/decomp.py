@@ -486,9 +486,16 @@ class IpcPeerRegistry:
 
     def publish(self, rank: int, sets) -> None:
         import torch.distributed as dist
-        mine = [self.export(s) for s in sets]
+        from . import _lib
+        try:  # a rank that cannot export still joins the gather (no rank left waiting)
+            mine = [self.export(s) for s in sets]
+        except _lib.PwadvError as exc:
+            mine = f"rank {rank}: {exc}"
         everyone = [None] * self.dec.size
         dist.all_gather_object(everyone, mine, group=self.group)
+        failed = [e for e in everyone if isinstance(e, str)]
+        if failed:
+            raise _lib.PwadvError("CUDA IPC export failed: " + "; ".join(failed))
         self.sets[rank] = tuple(tuple(t.data_ptr() for t in s) for s in sets)
         for r in set(neighbour_ranks(self.dec)) - {rank}:
             self.sets[r] = self.map_remote(everyone[r])
