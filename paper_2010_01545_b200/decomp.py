@@ -495,7 +495,7 @@ class IpcPeerRegistry:
         dist.all_gather_object(everyone, mine, group=self.group)
         failed = [e for e in everyone if isinstance(e, str)]
         if failed:
-            raise _lib.PwadvError("CUDA IPC export failed: " + "; ".join(failed))
+            raise _lib.PwadvError(-1, "CUDA IPC export failed: " + "; ".join(failed))
         self.sets[rank] = tuple(tuple(t.data_ptr() for t in s) for s in sets)
         for r in set(neighbour_ranks(self.dec)) - {rank}:
             self.sets[r] = self.map_remote(everyone[r])
