@@ -13,6 +13,16 @@ subprocess with pytest:
 * test_schedules.py   (pkg/tests/test_schedules.py:63-188: variants, engines,
                        traffic closed forms, comparator)
 * test_acceptance.py  criteria 7-9 (pkg/tests/test_acceptance.py:116-192)
+* test_cli.py         the `bench` command's tests (pkg/tests/test_cli.py:35-79):
+                       the stock CLI (cli.py:120-163), unmodified, calling OUR
+                       run_schedule per variant — checksums, traffic columns,
+                       determinism of the report rows
+
+and the reference's demos that call the hot path (the callers SURVEY.md §8b
+lists), unchanged: demos/01_stencil_basics.py and 02_schedule_traffic.py run
+once against the drop-in and once against the stock package; their outputs
+(checksums, identities, traffic counters) must be identical line for line
+apart from the wall-time column.
 
 No test is skipped or expected to fail. baseline/_ref is not in git (the
 reference is installed there once); without it this file skips.
@@ -29,6 +39,7 @@ pytestmark = pytest.mark.gpu
 
 ROOT = Path(__file__).resolve().parent.parent
 STOCK_TESTS = ROOT / "baseline" / "_ref" / "tests"
+STOCK_DEMOS = ROOT / "baseline" / "_ref" / "demos"
 ALIAS = ROOT / "tests" / "dropin_alias"
 
 FILES = {
@@ -36,6 +47,7 @@ FILES = {
     "test_grid.py": None,
     "test_schedules.py": None,
     "test_acceptance.py": "criterion_7 or criterion_8 or criterion_9",
+    "test_cli.py": "bench",
 }
 
 
@@ -68,3 +80,33 @@ def test_reference_test_file_unchanged(name):
     if name == "test_acceptance.py":
         for n in (7, 8, 9):
             assert f"ACCEPTANCE PASS  {n}" in out, out[-2000:]
+
+
+def _demo_output(path, pythonpath):
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join(str(p) for p in pythonpath)
+    res = subprocess.run([sys.executable, str(path)], env=env, capture_output=True, text=True,
+                         cwd=path.parent, timeout=900)
+    assert res.returncode == 0, (res.stdout + res.stderr)[-3000:]
+    return res.stdout
+
+
+def _without_wall(line: str) -> str:
+    """demo 02's table rows end in a wall-time column (schedules.py:220-228)."""
+    head = line.split(" ", 1)[0]
+    if head in ("reference", "column_buffered", "y_batched", "x_reordered"):
+        return line.rsplit(None, 1)[0]
+    return line
+
+
+@pytest.mark.parametrize("demo", ["01_stencil_basics.py", "02_schedule_traffic.py"])
+def test_reference_demo_unchanged(demo):
+    path = STOCK_DEMOS / demo
+    if not path.exists():
+        pytest.skip("stock reference demos not installed in baseline/_ref")
+    ours = _demo_output(path, [ALIAS, ROOT])
+    stock = _demo_output(path, [ROOT / "baseline" / "_ref"])
+    a = [_without_wall(x) for x in ours.splitlines()]
+    b = [_without_wall(x) for x in stock.splitlines()]
+    assert a == b, "\n".join(f"{x!r} | {y!r}" for x, y in zip(a, b) if x != y)
+    assert "checksum" in ours

@@ -3,7 +3,7 @@
 # bench.py --impl reference and tests/test_gpu_reference_suite.py. Run in the
 # dev container (needs /root/reference); baseline/_ref is git-ignored and
 # travels to the GPU box with the gpurun snapshot. The reference's own tests
-# are copied beside the package, unmodified.
+# and demos are copied beside the package, unmodified.
 set -euo pipefail
 ROOT="$(cd "$(dirname "$0")/.." && pwd)"
 SRC=/root/reference/pkg
@@ -13,5 +13,6 @@ rm -rf "$ROOT/baseline/_ref"
 python -m pip install --no-index --no-build-isolation --no-deps \
     --find-links /opt/wheelhouse --target "$ROOT/baseline/_ref" "$TMP/pkg"
 cp -r "$SRC/tests" "$ROOT/baseline/_ref/tests"
+cp -r "$SRC/demos" "$ROOT/baseline/_ref/demos"   # the hot path's callers, run unchanged too
 rm -rf "$TMP"
 echo "installed: $(ls "$ROOT/baseline/_ref")"
