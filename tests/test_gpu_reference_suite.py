@@ -110,3 +110,23 @@ def test_reference_demo_unchanged(demo):
     b = [_without_wall(x) for x in stock.splitlines()]
     assert a == b, "\n".join(f"{x!r} | {y!r}" for x, y in zip(a, b) if x != y)
     assert "checksum" in ours
+
+
+def test_whole_reference_suite_unchanged():
+    """Every stock test file in one run (the FPGA modelling tests included:
+    those modules are the stock files, but their grids, fields and any
+    stencil they evaluate come from the drop-in): nothing may fail or skip."""
+    if not STOCK_TESTS.exists():
+        pytest.skip("stock reference tests not installed in baseline/_ref")
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([str(ALIAS), str(ROOT)])
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
+                          "--rootdir", str(STOCK_TESTS), str(STOCK_TESTS)], env=env,
+                         capture_output=True, text=True, cwd=STOCK_TESTS, timeout=1800)
+    tail = (res.stdout + res.stderr)[-4000:]
+    assert res.returncode == 0, tail
+    last = res.stdout.strip().splitlines()[-1]
+    n = int(last.split(" passed")[0].split()[-1])
+    n_stock = sum(line.lstrip().startswith("def test_") for f in STOCK_TESTS.glob("test_*.py")
+                  for line in f.read_text().splitlines())
+    assert n >= n_stock and "skipped" not in last and "failed" not in last, last
