@@ -256,8 +256,9 @@ def measure_live_traffic(args, dims, fields, co, out, opts, stepping, ws, dev):
     if args.no_traffic:
         return None
     if stepping:
-        nxt = device.alloc_fields(dims, dev)
-        fn = lambda: device.step(*fields, co, 0.1, nxt, opts=opts)  # noqa: E731
+        # into the spare set `out` (a fourth field set does not fit at the full
+        # 4096x4096x128 grid: three sets are 155 GB)
+        fn = lambda: device.step(*fields, co, 0.1, out, opts=opts)  # noqa: E731
     else:
         fn = lambda: device.advect(*fields, co, out, opts=opts)  # noqa: E731
     try:
