@@ -255,6 +255,8 @@ def measure_live_traffic(args, dims, fields, co, out, opts, stepping, ws, dev):
     from paper_2010_01545_b200 import device, traffic
     if args.no_traffic:
         return None
+    if ws > 1 and dist_env()[1] != 0:
+        return None  # N>1: rank 0's block only (the ranks' blocks are alike)
     if stepping:
         # into the spare set `out` (a fourth field set does not fit at the full
         # 4096x4096x128 grid: three sets are 155 GB)
@@ -265,6 +267,8 @@ def measure_live_traffic(args, dims, fields, co, out, opts, stepping, ws, dev):
         r = traffic.measure(fn, plan_bytes=BYTES_PER_POINT * dims.cells, device=dev.index)
     except traffic.TrafficUnavailable as exc:
         return {"error": str(exc)[:300]}
+    except Exception as exc:  # noqa: BLE001  a diagnostic must never take the bench line down
+        return {"error": f"{type(exc).__name__}: {exc}"[:300]}
     r["what"] = ("one launch of the dominant kernel on this rank's block; plan_bytes = "
                  "the algorithmic 48 B/point")
     return r
@@ -334,12 +338,24 @@ def run_ours(args):
     from paper_2010_01545_b200 import _lib, device
 
     ws, rank, local = dist_env()
+    # PWADV_BENCH_SHARE_GPU=1: a dry run of the N>1 control path on a box with
+    # fewer GPUs than ranks — every rank on cuda:0 (time-sliced), gloo instead
+    # of NCCL (which refuses two ranks on one device), halo messages staged
+    # through the host. Exercises the IPC mapping, the handshake, the
+    # self-checks, the agreed fallbacks and the JSON line; its rates are not
+    # measurements and the line says so (tests/test_gpu_multi.py).
+    share = ws > 1 and os.environ.get("PWADV_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     nx, ny, nz, desc = CONFIGS[args.config]
     px, py = decomposition(ws)
     stepping = args.config == "c4"
@@ -750,6 +766,11 @@ def run_ours(args):
     # rank, halos included as the exchange left them) through its own PCIe
     # link; value = global points / max-over-ranks wall time
     if ws > 1 and not stepping and not args.no_e2e:
+        # a rank-local failure (pinned allocation, context) must not leave the
+        # other ranks in a collective: the ranks agree after the setup, and a
+        # rank that fails inside the timed loop still joins the reductions
+        err, ctx = None, None
+        ke = max(3, min(args.steps, args.e2e_steps))
         try:
             ctx = device.HostContext(dims, local)
             hin = [torch.empty(dims.padded_shape, dtype=torch.float64, pin_memory=True) for _ in range(3)]
@@ -757,29 +778,42 @@ def run_ours(args):
             for h, f in zip(hin, fields):
                 h.copy_(f)
             tz = [co.tz[0].cpu().numpy(), co.tz[1].cpu().numpy()]
-            ke = max(3, min(args.steps, args.e2e_steps))
             for _ in range(2):
                 ctx.submit_host(*hin, *hout, co.tcx, co.tcy, *tz, chunks=args.chunks)
             ctx.sync()
+        except Exception as exc:  # noqa: BLE001 — never lose the device-timed line
+            err = f"{type(exc).__name__}: {exc}"[:300]
+        if not agree_all(err is None, dev):
+            e2e = {"error": err or "host path setup failed on another rank"}
+        else:
             barrier()
-            t0 = time.perf_counter()
-            for _ in range(ke):
-                h2d, d2h = ctx.submit_host(*hin, *hout, co.tcx, co.tcy, *tz, chunks=args.chunks)
-            ctx.sync()
-            el = torch.tensor([time.perf_counter() - t0, float(h2d), float(d2h)],
-                              dtype=torch.float64, device=dev)
-            ctx.close()
+            el = [float("inf"), 0.0, 0.0]
+            try:
+                t0 = time.perf_counter()
+                for _ in range(ke):
+                    h2d, d2h = ctx.submit_host(*hin, *hout, co.tcx, co.tcy, *tz, chunks=args.chunks)
+                ctx.sync()
+                el = [time.perf_counter() - t0, float(h2d), float(d2h)]
+            except Exception as exc:  # noqa: BLE001
+                err = f"{type(exc).__name__}: {exc}"[:300]
+            el = torch.tensor(el, dtype=torch.float64, device=dev)
             mx = el[:1].clone()
             dist.all_reduce(mx, op=dist.ReduceOp.MAX)
             tot = el[1:].clone()
             dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-            e2e = {"value": global_points * ke / float(mx.item()) / 1e9, "unit": UNIT,
-                   "h2d_bytes_per_step": int(tot[0].item()), "d2h_bytes_per_step": int(tot[1].item()),
-                   "bytes_summed_over_ranks": True, "steps": ke,
-                   "api": "pwadv_ctx_submit_host + pwadv_ctx_sync per rank (C ABI; pinned host "
-                          "blocks incl. halos; each rank on its own PCIe link)"}
-        except Exception as exc:  # noqa: BLE001 — never lose the device-timed line
-            e2e = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+            if float(mx.item()) == float("inf"):
+                e2e = {"error": err or "host path failed on another rank"}
+            else:
+                e2e = {"value": global_points * ke / float(mx.item()) / 1e9, "unit": UNIT,
+                       "h2d_bytes_per_step": int(tot[0].item()), "d2h_bytes_per_step": int(tot[1].item()),
+                       "bytes_summed_over_ranks": True, "steps": ke,
+                       "api": "pwadv_ctx_submit_host + pwadv_ctx_sync per rank (C ABI; pinned host "
+                              "blocks incl. halos; each rank on its own PCIe link)"}
+        if ctx is not None:
+            try:
+                ctx.close()
+            except Exception:  # noqa: BLE001
+                pass
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -797,6 +831,8 @@ def run_ours(args):
                        "global_grid": f"{gx}x{gy}x{nz}", "points_per_gpu": pts_rank,
                        "decomposition": f"{px}x{py}", "variant": args.variant,
                        **({"multi_gpu_step": step_path} if step_path else {}),
+                       **({"dry_run": "PWADV_BENCH_SHARE_GPU=1: all ranks time-slice one GPU over "
+                                      "gloo — a control-path check, not a measurement"} if share else {}),
                        "bit_exact": not args.variant.endswith("_fma"),
                        "l2": f"inputs larger than L2 ({3 * dims.padded_len * 8 / 1e6:.0f} MB read per "
                              f"step vs 126 MB L2); no flush", "plan": plan},

@@ -238,6 +238,20 @@ class DistTransport:
                    for k, t, peer, _ in ops]
             for req in dist.batch_isend_irecv(p2p):
                 req.wait()
+        elif any(t.is_cuda for _, t, _, _ in ops):
+            # gloo has no point-to-point for CUDA tensors: stage through the
+            # host (dry runs of the multi-rank paths with the ranks sharing
+            # one GPU, tests/test_gpu_multi.py; never a measured path)
+            torch.cuda.current_stream().synchronize()  # the packed faces are final
+            staged = [(k, t, t.cpu() if k == "send" else torch.empty(t.shape, dtype=t.dtype), peer, tag)
+                      for k, t, peer, tag in ops]
+            reqs = [(dist.isend if k == "send" else dist.irecv)(h, peer, group=self.group, tag=tag)
+                    for k, _, h, peer, tag in staged]
+            for r in reqs:
+                r.wait()
+            for k, t, h, _, _ in staged:
+                if k == "recv":
+                    t.copy_(h)
         else:
             reqs = [(dist.isend if k == "send" else dist.irecv)(t, peer, group=self.group, tag=tag)
                     for k, t, peer, tag in ops]
