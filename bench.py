@@ -285,6 +285,7 @@ def step_barrier(dec, dev, stream):
     hs, ok, err = None, False, None
     try:
         hs = decomp.FlagHandshake(dec, decomp.IpcPeerRegistry(dec), dev)
+        injected_failure("handshake")  # (after the registry's gather, which every rank joins)
         probe = torch.cuda.Stream(dev)
         hs(probe)
         ev = torch.cuda.Event()
@@ -306,6 +307,16 @@ def step_barrier(dec, dev, stream):
     print(f"bench: flag handshake unavailable ({err or 'on another rank'}); NCCL barrier",
           file=sys.stderr)
     return decomp.NcclBarrier(dev), "NCCL all-reduce barrier"
+
+
+def injected_failure(where: str) -> None:
+    """Test hook (tests/test_gpu_multi.py): PWADV_BENCH_FAIL=<where> makes the
+    LAST rank fail at that point — after the registry's gather, where a real
+    rank-local failure (a peer mapping, the capability query) would surface —
+    to prove that all ranks fall back together."""
+    ws, rank, _ = dist_env()
+    if ws > 1 and rank == ws - 1 and os.environ.get("PWADV_BENCH_FAIL") == where:
+        raise RuntimeError(f"injected failure at {where} on rank {rank}")
 
 
 def agree_all(ok: bool, dev) -> bool:
@@ -418,6 +429,7 @@ def run_ours(args):
                 st = decomp.PushStepper(dec, fields, co, 0.1, decomp.IpcPeerRegistry(dec),
                                         barrier, opts=opts,
                                         initial_exchange=lambda f: exch.exchange(f, stream=stream))
+                injected_failure("fused")
             except Exception as exc:
                 err = f"{type(exc).__name__}: {exc}"
             # every rank mapped its neighbours' buffers before any rank's first
@@ -470,6 +482,7 @@ def run_ours(args):
             try:
                 ev = decomp.PullEvaluator(dec, fields, co, decomp.IpcPeerRegistry(dec),
                                           barrier, opts=opts)
+                injected_failure("fused")
             except Exception as exc:
                 err = f"{type(exc).__name__}: {exc}"
             if not agree_all(err is None, dev):

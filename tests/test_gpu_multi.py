@@ -151,3 +151,37 @@ def test_bench_under_torchrun(config):
     assert ("halo pull" in step) if config == "c1" else ("peer stores" in step), (step, r.stderr[-1500:])
     assert d["parity"]["bitwise_equal"] is True, d["parity"]
     assert ("dry_run" in d["config"]) == (NGPU < 2)
+
+
+@pytest.mark.skipif(NGPU < 1, reason="needs a GPU")
+@pytest.mark.parametrize("where,config", [("handshake", "c1"), ("fused", "c1"), ("fused", "c4")])
+def test_bench_ranks_fall_back_together(where, config):
+    """A failure on ONE rank (injected on the last: PWADV_BENCH_FAIL) while the
+    others succeed: all ranks must take the same fallback — the all-reduce
+    barrier when the flag handshake cannot be set up, the exchange-and-overlap
+    step when the fused path cannot — and still print the line (ADVICE r1:
+    ranks that diverge here hang in mismatched collectives)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(root / "bench.py"),
+           "--gpus", "2", "--config", config, "--steps", "5", "--warmup", "3", "--no-cpu", "--no-e2e",
+           "--no-traffic"]
+    env = dict(os.environ, PWADV_BENCH_FAIL=where)
+    if NGPU < 2:
+        env["PWADV_BENCH_SHARE_GPU"] = "1"
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    step = d["config"].get("multi_gpu_step", "")
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    if where == "handshake":
+        assert "all-reduce barrier" in step, step
+        assert d["parity"]["bitwise_equal"] is True, d["parity"]
+    else:
+        assert step.startswith("NCCL exchange overlapped"), step
