@@ -507,7 +507,9 @@ def run_ours(args):
             except Exception as exc:
                 err = err or f"{type(exc).__name__}: {exc}"
             if agree_all(err is None, dev):
-                step_path = f"K1 with halo pull (peer loads over NVLink, CUDA IPC) + {barrier_kind}"
+                how = ("fused into K1's bulk copies" if ev.mode == "fused"
+                       else "K2p gather kernel, then the planner's kernel")
+                step_path = f"K1 with halo pull ({how}; peer loads over NVLink, CUDA IPC) + {barrier_kind}"
 
                 def one_step(events=None):
                     ev.evaluate(out, stream=stream, events=events)

@@ -236,6 +236,24 @@ int pwadv_step_pull_f64(const double *u, const double *v, const double *w,
                         const double *tzc1, const double *tzc2, double dt,
                         const pwadv_peers *src, const pwadv_opts *opts, void *stream);
 
+/*
+ * K2p — the halo exchange as one gather kernel: every halo cell of this
+ * block's u, v, w (x-halo planes, y-halo columns, the four corner columns)
+ * loaded from the neighbours' CURRENT interiors in `src` (peer loads over
+ * NVLink for another GPU's block) — the cells a two-phase periodic exchange
+ * (the reference's wrap_halos, grid.py:203-208) delivers; an undivided axis
+ * names this block itself. For decomposed blocks off the aligned X-march
+ * (deep columns on K1c, odd nz, 8-byte-aligned fields), where the fused pull
+ * of pwadv_advect_pull_f64 does not apply: gather, then pwadv_advect_f64 /
+ * pwadv_step_f64 with the planner's kernel. Writes only this block's halos and
+ * reads only interiors, so neighbouring blocks may gather concurrently; the
+ * neighbours' interiors must be final (one handshake before the call).
+ * Buffers 8-byte aligned.
+ */
+int pwadv_pull_halos_f64(double *u, double *v, double *w,
+                         int64_t nx, int64_t ny, int64_t nz,
+                         const pwadv_peers *src, void *stream);
+
 /* CUDA IPC helpers for the peer buffers of pwadv_step_push_f64 (one process
  * per GPU): export a device allocation (handle: 64 opaque bytes, plus the
  * pointer's byte offset inside its allocation), open a peer's export, close. */

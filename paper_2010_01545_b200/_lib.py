@@ -94,6 +94,7 @@ SIGNATURES = {
     "pwadv_step_push_f64": (ctypes.c_int, [_P] * 6 + [_I64] * 3 + [_D, _D, _P, _P, _D, _P, _P, _P]),
     "pwadv_advect_pull_f64": (ctypes.c_int, [_P] * 6 + [_I64] * 3 + [_D, _D, _P, _P, _P, _P, _P]),
     "pwadv_step_pull_f64": (ctypes.c_int, [_P] * 6 + [_I64] * 3 + [_D, _D, _P, _P, _D, _P, _P, _P]),
+    "pwadv_pull_halos_f64": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I64, _P, _P]),
     "pwadv_ipc_export": (ctypes.c_int, [_P, _P, ctypes.POINTER(ctypes.c_uint64)]),
     "pwadv_ipc_open": (ctypes.c_int, [_P, ctypes.c_uint64, ctypes.POINTER(_P)]),
     "pwadv_ipc_close": (ctypes.c_int, [_P, ctypes.c_uint64]),

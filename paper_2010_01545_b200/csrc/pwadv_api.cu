@@ -246,6 +246,22 @@ int pwadv_step_pull_f64(const double *u, const double *v, const double *w, doubl
                    nx + 1, 1, ny + 1, opts, stream, src, true);
 }
 
+int pwadv_pull_halos_f64(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
+                         const pwadv_peers *src, void *stream)
+{
+    int rc = check_dims(nx, ny, nz);
+    if (rc) return rc;
+    if ((rc = check_ptrs({u, v, w}))) return rc;
+    if ((rc = check_peers(src, nx, ny, 8))) return rc;
+    // the corner neighbours sit on my x neighbours' rows and my y neighbours' columns
+    if (src->nx[PWADV_NB_XMYM] != src->nx[PWADV_NB_XM] || src->nx[PWADV_NB_XMYP] != src->nx[PWADV_NB_XM] ||
+        src->nx[PWADV_NB_XPYM] != src->nx[PWADV_NB_XP] || src->nx[PWADV_NB_XPYP] != src->nx[PWADV_NB_XP] ||
+        src->ny[PWADV_NB_XMYM] != src->ny[PWADV_NB_YM] || src->ny[PWADV_NB_XPYM] != src->ny[PWADV_NB_YM] ||
+        src->ny[PWADV_NB_XMYP] != src->ny[PWADV_NB_YP] || src->ny[PWADV_NB_XPYP] != src->ny[PWADV_NB_YP])
+        return set_error(PWADV_E_RANGE, "corner peer extents inconsistent with an x-y decomposition");
+    return launch_pull_halos3(u, v, w, nx, ny, nz, src, (cudaStream_t)stream);
+}
+
 // Base address of the allocation containing `ptr`, through the driver's
 // cuMemGetAddressRange (fetched with cudaGetDriverEntryPoint: no libcuda link).
 static int allocation_base(const void *ptr, uintptr_t *base)

@@ -63,6 +63,47 @@ __global__ void k_wrap3(double *f0, double *f1, double *f2, int nf, int64_t nx, 
     }
 }
 
+// K2p — the halo wrap of one block of an x-y decomposition, gathered from
+// the neighbours' buffers (peer loads over NVLink for another GPU's block):
+// every halo cell (i, j) of this block takes the neighbour's interior cell
+// that a two-phase periodic exchange (wrap_halos, grid.py:203-208: the X pass,
+// then the Y pass over the X halos) would have delivered — x-halo planes from
+// XM's last / XP's first interior plane, y-halo columns from YM's last / YP's
+// first interior column, the four corner columns from the diagonal
+// neighbours. Along an undivided axis the neighbour is this block itself and
+// the copy is the plain wrap. Only this block's halos are written, only
+// interiors are read: concurrent gathers of neighbouring blocks never touch
+// the same cell.
+struct PeerSrc {
+    const double *f[3][8];
+    int64_t nx[8], ny[8];
+};
+
+__global__ void k_pull_halos3(double *f0, double *f1, double *f2, int64_t nx, int64_t ny,
+                              int64_t nz, const __grid_constant__ PeerSrc p)
+{
+    const int64_t ncols = 2 * (ny + 2) + 2 * nx;
+    const int64_t total = ncols * nz;
+    double *fs[3] = {f0, f1, f2};
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = idx % nz, h = idx / nz;
+        int64_t i;
+        const int64_t j = halo_col(h, nx, ny, &i);
+        const int xs = i == 0 ? -1 : (i == nx + 1 ? 1 : 0);
+        const int ys = j == 0 ? -1 : (j == ny + 1 ? 1 : 0);
+        int d;
+        if (xs < 0) d = ys < 0 ? PWADV_NB_XMYM : (ys > 0 ? PWADV_NB_XMYP : PWADV_NB_XM);
+        else if (xs > 0) d = ys < 0 ? PWADV_NB_XPYM : (ys > 0 ? PWADV_NB_XPYP : PWADV_NB_XP);
+        else d = ys < 0 ? PWADV_NB_YM : PWADV_NB_YP;
+        const int64_t si = xs < 0 ? p.nx[d] : (xs > 0 ? 1 : i);
+        const int64_t sj = ys < 0 ? p.ny[d] : (ys > 0 ? 1 : j);
+        const int64_t dst = (i * (ny + 2) + j) * nz + k;
+        const int64_t src = (si * (p.ny[d] + 2) + sj) * nz + k;
+        for (int m = 0; m < 3; ++m) fs[m][dst] = p.f[m][d][src];
+    }
+}
+
 // One axis of the periodic wrap (an undivided axis of a decomposition).
 // axis 0: planes 0 <- nx, nx+1 <- 1 (all j); axis 1: columns 0 <- ny,
 // ny+1 <- 1 for all i in 0..nx+1.
@@ -245,6 +286,22 @@ int launch_wrap3(double *u, double *v, double *w, int nf, int64_t nx, int64_t ny
     const int64_t total = (2 * (ny + 2) + 2 * nx) * nz;
     k_wrap3<<<grid_for(total, 256), 256, 0, s>>>(u, v, w, nf, nx, ny, nz);
     return check_launch("wrap_halos");
+}
+
+int launch_pull_halos3(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
+                       const pwadv_peers *src, cudaStream_t s)
+{
+    PeerSrc p;
+    for (int d = 0; d < 8; ++d) {
+        p.f[0][d] = src->u[d];
+        p.f[1][d] = src->v[d];
+        p.f[2][d] = src->w[d];
+        p.nx[d] = src->nx[d];
+        p.ny[d] = src->ny[d];
+    }
+    const int64_t total = (2 * (ny + 2) + 2 * nx) * nz;
+    k_pull_halos3<<<grid_for(total, 256), 256, 0, s>>>(u, v, w, nx, ny, nz, p);
+    return check_launch("pull_halos");
 }
 
 int launch_wrap_axis3(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,

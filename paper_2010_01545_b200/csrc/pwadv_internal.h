@@ -65,6 +65,8 @@ int launch_box(const BoxLaunch &L, cudaStream_t stream);
 // auxiliary kernels (pwadv_aux.cu)
 int launch_wrap3(double *u, double *v, double *w, int nf, int64_t nx, int64_t ny, int64_t nz,
                  cudaStream_t s);
+int launch_pull_halos3(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
+                       const pwadv_peers *src, cudaStream_t s);
 int launch_wrap_axis3(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz,
                       int axis, cudaStream_t s);
 int launch_fill(double *u, double *v, double *w, int64_t nx, int64_t ny, int64_t nz, int mode,

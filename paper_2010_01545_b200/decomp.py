@@ -579,6 +579,22 @@ class PullEvaluator:
         registry.publish(dec.rank, (self.fields,))
         self.peers = None
         self._launches: dict = {}
+        # "fused": the halo cells loaded by K1's own bulk copies (the aligned
+        # X-march); "gather": the K2p gather kernel fills this block's halos
+        # from the neighbours, then the planner's kernel runs — for blocks the
+        # planner gives to another kernel (deep columns on K1c, odd nz) or
+        # that the fused pull does not take. The choice is this rank's own:
+        # both forms read only the neighbours' interiors and write only here.
+        self.mode = self._choose_mode()
+
+    def _choose_mode(self) -> str:
+        from . import device as dv
+        try:
+            plan = dv.describe_plan(self.dec.local_dims, None, self.opts,
+                                    self.fields[0].device.index or 0)
+        except Exception:  # noqa: BLE001  (no plan report: let the fused launch decide)
+            return "fused"
+        return "fused" if plan["kernel"] == "xmarch" else "gather"
 
     def _build_peers(self):
         from . import _lib
@@ -593,7 +609,7 @@ class PullEvaluator:
                  events=None) -> None:
         """su, sv, sw (or, with dt, the forward-Euler update) of this block into
         `out`; with `events` (a list) an event pair around the launch is appended."""
-        from . import device as dv
+        from . import _lib, device as dv
         first = self.peers is None
         if (first or sync) and self.barrier is not None:
             self.barrier(stream)
@@ -605,9 +621,22 @@ class PullEvaluator:
             if len(self._launches) > 8:
                 self._launches.clear()
             launch = self._launches[key] = dv.BoundLaunch(self.fields, self.coeffs, out,
-                                                          opts=self.opts, dt=dt, pull=self.peers)
+                                                          opts=self.opts, dt=dt, pull=self.peers,
+                                                          gather=self.mode == "gather")
         ev = dv.event_pair(events, stream)
-        launch(stream)
+        try:
+            launch(stream)
+        except _lib.PwadvError as exc:
+            if self.mode != "fused" or exc.code != _lib.PWADV_E_ARG:
+                raise
+            # a block the fused pull does not take (the launch was refused
+            # before anything ran): gather + the planner's kernel from now on
+            self.mode = "gather"
+            self._launches.clear()
+            launch = self._launches[key] = dv.BoundLaunch(self.fields, self.coeffs, out,
+                                                          opts=self.opts, dt=dt, pull=self.peers,
+                                                          gather=True)
+            launch(stream)
         dv.close_event_pair(ev, stream)
 
 

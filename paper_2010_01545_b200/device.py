@@ -183,11 +183,18 @@ class BoundLaunch:
     otherwise exceed the kernel time of a small per-GPU block."""
 
     def __init__(self, fields, coeffs, out, *, box=None, opts: _lib.Opts | None = None,
-                 dt: float | None = None, pull: "_lib.Peers | None" = None):
+                 dt: float | None = None, pull: "_lib.Peers | None" = None,
+                 gather: bool = False):
+        """pull: the neighbours' buffers — fused into the kernel's bulk copies
+        (the aligned X-march), or with gather=True as the K2p halo gather
+        (pwadv_pull_halos_f64 into this block's halos) followed by the plain
+        launch with the planner's kernel (any shape: K1c, odd nz, ...)."""
         u, v, w = fields
         dims = dims_of(u)
         if pull is not None and box is not None:
             raise ValueError("a halo-pull launch covers the whole interior (no box)")
+        if gather and pull is None:
+            raise ValueError("gather needs the peer table")
         for t, n in zip(tuple(fields) + tuple(out), ("u", "v", "w", "o0", "o1", "o2")):
             _check_field(t, dims, n)
         dc = _as_device_coeffs(coeffs, u.device)
@@ -199,6 +206,12 @@ class BoundLaunch:
         L = _lib.lib()
         head = [_p(u), _p(v), _p(w), _p(out[0]), _p(out[1]), _p(out[2]), dims.nx, dims.ny,
                 dims.nz, dc.tcx, dc.tcy, _p(dc.tz[0]), _p(dc.tz[1])]
+        self._pre = None
+        if pull is not None and gather:
+            self._keep += (pull,)
+            self._pre = (L.pwadv_pull_halos_f64,
+                         [_p(u), _p(v), _p(w), dims.nx, dims.ny, dims.nz, ctypes.byref(pull)])
+            pull = None
         if pull is not None:
             self._keep += (pull,)
             pp = ctypes.byref(pull)
@@ -216,7 +229,10 @@ class BoundLaunch:
             self._args = head + [float(dt), x0, x1, y0, y1, _lib.opts_ptr(opts)]
 
     def __call__(self, stream=None) -> None:
-        _lib.check(self._fn(*self._args, _stream_handle(stream, self.device)))
+        h = _stream_handle(stream, self.device)
+        if self._pre is not None:
+            _lib.check(self._pre[0](*self._pre[1], h))
+        _lib.check(self._fn(*self._args, h))
 
 
 def event_pair(events, stream=None):
@@ -244,6 +260,17 @@ def self_peers(fields) -> _lib.Peers:
         p.u[d], p.v[d], p.w[d] = (_p(t) for t in fields)
         p.nx[d], p.ny[d] = dims.nx, dims.ny
     return p
+
+
+def pull_halos(u, v, w, peers: _lib.Peers, stream=None) -> None:
+    """K2p: this block's halo cells gathered from the neighbours' current
+    interiors (pwadv_pull_halos_f64) — the cells a two-phase periodic exchange
+    delivers (reference wrap_halos, grid.py:203-208), for any shape."""
+    dims = dims_of(u)
+    for t, n in ((u, "u"), (v, "v"), (w, "w")):
+        _check_field(t, dims, n)
+    _lib.check(_lib.lib().pwadv_pull_halos_f64(_p(u), _p(v), _p(w), dims.nx, dims.ny, dims.nz,
+                                               ctypes.byref(peers), _stream_handle(stream, u.device)))
 
 
 def advect_pull(u, v, w, coeffs, peers: _lib.Peers, out=None, *, opts: _lib.Opts | None = None,

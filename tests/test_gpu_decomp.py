@@ -345,12 +345,14 @@ def test_pull_single_block_self_peers(shape):
     assert all(torch.equal(t[0], torch.zeros_like(t[0])) for t in nxt)  # new halos untouched
 
 
-@pytest.mark.parametrize("shape", [(40, 36, 64), (64, 48, 128), (25, 23, 6)])
+@pytest.mark.parametrize("shape", [(40, 36, 64), (64, 48, 128), (25, 23, 6),
+                                   (24, 26, 63), (12, 16, 300), (9, 40, 1031)])
 @pytest.mark.parametrize("px,py", [(1, 2), (2, 1), (2, 2), (2, 4), (3, 2)])
 def test_emulated_pull_decomposition_bitwise(shape, px, py):
     """PullEvaluator on every block of a px x py decomposition (peer buffers on
     this GPU, halos NaN-poisoned): bit-identical to the undivided evaluation;
-    and a pulled forward step too."""
+    and a pulled forward step too. Blocks on the aligned X-march pull inside
+    the kernel; odd nz and deep columns (K1c) take the K2p gather kernel."""
     from paper_2010_01545_b200.decomp import LocalPeerRegistry, PullEvaluator
     gd = pw.make_grid(*shape)
     spec = pw.GeneratorSpec.baseline(9)
@@ -371,6 +373,10 @@ def test_emulated_pull_decomposition_bitwise(shape, px, py):
         _poison_halos(fs)
         evs.append((dec, PullEvaluator(dec, fs, co, reg)))
     torch.cuda.synchronize()
+    if gd.nz % 2:
+        assert all(ev.mode == "gather" for _, ev in evs)
+    elif gd.nz in (64, 128):
+        assert all(ev.mode == "fused" for _, ev in evs)
     for dec, ev in evs:  # every block published before any evaluation
         out = device.alloc_fields(dec.local_dims, "cuda")
         ev.evaluate(out)
@@ -384,6 +390,41 @@ def test_emulated_pull_decomposition_bitwise(shape, px, py):
         for o, w in zip(nxt, want_step):
             assert torch.equal(o[1:-1, 1:-1].contiguous().view(torch.int64),
                                w[1 + xo:1 + xo + bx, 1 + yo:1 + yo + by].contiguous().view(torch.int64)), dec.rank
+
+
+@pytest.mark.parametrize("shape", [(8, 8, 7), (13, 6, 64), (5, 9, 130), (1, 1, 2), (1, 7, 5)])
+def test_pull_halos_gather_kernel(shape):
+    """K2p (pwadv_pull_halos_f64): with the block as its own eight neighbours
+    it is the periodic wrap (reference wrap_halos, grid.py:203-208), every halo
+    cell incl. the corners; over a 2x3 decomposition every block's halos equal
+    the wrapped global field's."""
+    gd = pw.make_grid(*shape)
+    f = device.fill(gd, pw.GeneratorSpec.random(5))
+    want = [t.clone() for t in f]
+    device.wrap_halos(*want)
+    _poison_halos(f)
+    device.pull_halos(*f, device.self_peers(f))
+    torch.cuda.synchronize()
+    for a, b in zip(f, want):
+        assert torch.equal(a.view(torch.int64), b.view(torch.int64))
+    px, py = 2, 3
+    if gd.nx < px or gd.ny < py:
+        return
+    from paper_2010_01545_b200.decomp import LocalPeerRegistry, PullEvaluator
+    reg = LocalPeerRegistry()
+    co = pw.baseline_coefficients(5, gd.nz)
+    evs = []
+    for r in range(px * py):
+        dec = Decomposition(gd, px, py, r)
+        fs = dec.fill_local(pw.GeneratorSpec.random(5))
+        _poison_halos(fs)
+        evs.append((dec, fs, PullEvaluator(dec, fs, co, reg)))
+    for dec, fs, ev in evs:
+        device.pull_halos(*fs, ev._build_peers())
+    torch.cuda.synchronize()
+    for dec, fs, _ in evs:
+        for a, w in zip(fs, want):
+            assert torch.equal(a.view(torch.int64), dec.local_view(w).contiguous().view(torch.int64)), dec.rank
 
 
 def test_pull_rejects_shapes_off_the_aligned_xmarch():

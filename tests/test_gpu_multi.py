@@ -34,7 +34,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, px, py, q, share=False):
+def _worker(rank, world, port, px, py, q, share=False, nz=64):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         import torch.distributed as dist
@@ -48,7 +48,7 @@ def _worker(rank, world, port, px, py, q, share=False):
             dist.init_process_group("gloo", rank=rank, world_size=world)
         else:
             dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
-        gd = pw.make_grid(64, 48, 64)
+        gd = pw.make_grid(64, 48, nz)
         spec = pw.GeneratorSpec.baseline(21)
         co = pw.baseline_coefficients(21, gd.nz)
         dec = decomp.Decomposition(gd, px, py, rank)
@@ -89,6 +89,7 @@ def _worker(rank, world, port, px, py, q, share=False):
         out3 = device.alloc_fields(dec.local_dims, dev)
         ev.evaluate(out3)
         torch.cuda.synchronize()
+        ok &= ev.mode == ("fused" if nz == 64 else "gather")
         for o, w in zip(out3, want_adv):
             ok &= torch.equal(o[1:-1, 1:-1].contiguous().view(torch.int64),
                               w[1 + xo:1 + xo + bx, 1 + yo:1 + yo + by].contiguous().view(torch.int64))
@@ -119,6 +120,29 @@ def test_nccl_exchange_and_fused_ipc_step(px, py):
     for p in procs:
         p.join(timeout=120)
     assert sorted(r for r, _, _ in results) == list(range(world))
+    for r, ok, err in results:
+        assert ok, (r, err)
+
+
+@pytest.mark.skipif(NGPU < 1, reason="needs a GPU")
+@pytest.mark.parametrize("px,py,nz", [(1, 2, 63), (2, 2, 300)])
+def test_off_xmarch_blocks_across_processes(px, py, nz):
+    """Odd nz / deep columns (blocks the planner gives to the UA form or K1c):
+    the exchange, the fused push step and the pull evaluation — there the K2p
+    gather kernel reading the other processes' buffers, then the planner's
+    kernel — bitwise against the single-domain result."""
+    world = px * py
+    share = world > NGPU
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, px, py, q, share, nz)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
     for r, ok, err in results:
         assert ok, (r, err)
 

@@ -84,9 +84,11 @@ def main():
     # are the other blocks' buffers on this GPU; blocks evaluated in turn)
     from paper_2010_01545_b200.decomp import Decomposition, LocalPeerRegistry, PullEvaluator
     for n in range(max(1, a.cases // 10)):
-        nz = int(rng.choice([2, 6, 16, 64, 96, 128]))
+        # even nz on the aligned X-march pull inside K1; odd nz and deep columns
+        # (UA form, K1c) take the K2p gather kernel and the planner's kernel
+        nz = int(rng.choice([2, 6, 16, 64, 96, 128, 5, 33, 63, 127, 160, 300, 514]))
         px, py = int(rng.integers(1, 4)), int(rng.integers(1, 5))
-        nx, ny = int(rng.integers(px, 70)), int(rng.integers(py, 150))
+        nx, ny = int(rng.integers(px, 70)), int(rng.integers(py, 150 if nz <= 128 else 40))
         seed = int(rng.integers(0, 2**31))
         gd = pw.make_grid(nx, ny, nz)
         spec = pw.GeneratorSpec.baseline(seed)
