@@ -558,6 +558,37 @@ class IpcPeerRegistry:
         self._bases = {}
 
 
+def pull_mode(dims, opts, device_index: int) -> str:
+    """How a block's halo cells are pulled: "fused" into K1 / K4's own bulk
+    copies where the planner runs the block on the aligned X-march, else
+    "gather" — the K2p gather kernel (pwadv_pull_halos_f64) followed by the
+    planner's kernel (deep columns on K1c, odd nz, ...). The choice is a
+    rank's own: both forms read only the neighbours' interiors and write only
+    this block."""
+    from . import device as dv
+    try:
+        plan = dv.describe_plan(dims, None, opts, device_index)
+    except Exception:  # noqa: BLE001  (no plan report: let the fused launch decide)
+        return "fused"
+    return "fused" if plan["kernel"] == "xmarch" else "gather"
+
+
+def peer_tables(dec: "Decomposition", registry, nsets: int) -> list:
+    """One pwadv_peers table per published buffer set: the eight neighbours'
+    (u, v, w) of that set and their interior extents."""
+    from . import _lib
+    tables = []
+    nbr = neighbour_ranks(dec)
+    for set_index in range(nsets):
+        p = _lib.Peers()
+        for d, r in enumerate(nbr):
+            p.u[d], p.v[d], p.w[d] = registry.pointers(r, set_index)
+            _, nxl, _, nyl = dec.block(r)
+            p.nx[d], p.ny[d] = nxl, nyl
+        tables.append(p)
+    return tables
+
+
 class PullEvaluator:
     """PW advection of one block with the halo exchange fused into K1 (pull):
     the kernel's bulk copies load the halo cells straight from the
@@ -585,25 +616,10 @@ class PullEvaluator:
         # planner gives to another kernel (deep columns on K1c, odd nz) or
         # that the fused pull does not take. The choice is this rank's own:
         # both forms read only the neighbours' interiors and write only here.
-        self.mode = self._choose_mode()
-
-    def _choose_mode(self) -> str:
-        from . import device as dv
-        try:
-            plan = dv.describe_plan(self.dec.local_dims, None, self.opts,
-                                    self.fields[0].device.index or 0)
-        except Exception:  # noqa: BLE001  (no plan report: let the fused launch decide)
-            return "fused"
-        return "fused" if plan["kernel"] == "xmarch" else "gather"
+        self.mode = pull_mode(dec.local_dims, opts, self.fields[0].device.index or 0)
 
     def _build_peers(self):
-        from . import _lib
-        p = _lib.Peers()
-        for d, r in enumerate(neighbour_ranks(self.dec)):
-            p.u[d], p.v[d], p.w[d] = self.registry.pointers(r, 0)
-            _, nxl, _, nyl = self.dec.block(r)
-            p.nx[d], p.ny[d] = nxl, nyl
-        return p
+        return peer_tables(self.dec, self.registry, 1)[0]
 
     def evaluate(self, out, stream=None, *, sync: bool = True, dt: float | None = None,
                  events=None) -> None:
@@ -764,6 +780,90 @@ class ThreadStreamBarrier:
         return barrier
 
 
+class PullStepper:
+    """Forward-Euler steps of one block with the halo cells pulled from the
+    neighbours' current buffers every step — for ANY block shape.
+
+    Two buffer sets (ping-pong), both published; step n reads set n%2 — its
+    own interior and, for the halo cells, the neighbours' interiors of the
+    same set: inside K4's bulk copies where the block runs on the aligned
+    X-march (mode "fused", pwadv_step_pull_f64), else through the K2p gather
+    kernel followed by K4 with the planner's kernel (mode "gather": deep
+    columns on K1c, odd nz) — and writes the interior of set (n+1)%2; then
+    `barrier` (the neighbour flag handshake): before step n+1 every neighbour
+    has finished step n, so its new interior is final (RAW) and it is done
+    reading the set this rank overwrites next (WAR). No halo is ever pushed,
+    packed or sent. PushStepper (peer stores from K4's epilogue) is the
+    cheaper form where it applies; this one covers the other shapes."""
+
+    def __init__(self, dec: Decomposition, fields, coeffs, dt: float, registry, barrier, *,
+                 opts=None):
+        from . import device as dv
+        self.dec = dec
+        self.dims = dec.local_dims
+        u = fields[0]
+        self.coeffs = dv._as_device_coeffs(coeffs, u.device)
+        self.dt = float(dt)
+        self.opts = opts
+        self.sets = (tuple(fields), dv.alloc_fields(self.dims, u.device))
+        self.cur = 0
+        self.registry = registry
+        self.barrier = barrier
+        registry.publish(dec.rank, self.sets)
+        self._peers = None
+        self._launches: dict = {}
+        self.steps_done = 0
+        self.mode = pull_mode(self.dims, opts, u.device.index or 0)
+
+    @property
+    def fields(self):
+        """The current fields (halos as the last gather / wrap left them; use
+        refreshed_fields() for valid halos)."""
+        return self.sets[self.cur]
+
+    def _build_peers(self):
+        return peer_tables(self.dec, self.registry, 2)
+
+    def _launch(self, cur: int):
+        from . import device as dv
+        launch = self._launches.get(cur)
+        if launch is None:
+            launch = self._launches[cur] = dv.BoundLaunch(
+                self.sets[cur], self.coeffs, self.sets[1 - cur], opts=self.opts, dt=self.dt,
+                pull=self._peers[cur], gather=self.mode == "gather")
+        return launch
+
+    def step(self, n: int = 1, stream=None, events=None) -> None:
+        from . import _lib, device as dv
+        if self._peers is None:  # every rank published and filled its fields
+            self.barrier(stream)
+            self._peers = self._build_peers()
+        for _ in range(n):
+            ev = dv.event_pair(events, stream)
+            try:
+                self._launch(self.cur)(stream)
+            except _lib.PwadvError as exc:
+                if self.mode != "fused" or exc.code != _lib.PWADV_E_ARG:
+                    raise
+                self.mode = "gather"  # refused before anything ran: gather + the planner's kernel
+                self._launches.clear()
+                self._launch(self.cur)(stream)
+            dv.close_event_pair(ev, stream)
+            self.barrier(stream)
+            self.cur = 1 - self.cur
+            self.steps_done += 1
+
+    def refreshed_fields(self, stream=None):
+        """The current fields with their halos gathered from the neighbours (as
+        an exchange / wrap_halos would leave them)."""
+        from . import device as dv
+        if self._peers is None:
+            self.barrier(stream)
+            self._peers = self._build_peers()
+        dv.pull_halos(*self.sets[self.cur], self._peers[self.cur], stream=stream)
+        return self.sets[self.cur]
+
+
 class PushStepper:
     """Forward-Euler steps of one block with the halo exchange fused into K4.
 
@@ -792,18 +892,7 @@ class PushStepper:
         self.steps_done = 0
 
     def _build_peers(self):
-        from . import _lib
-        P = []
-        nbr = neighbour_ranks(self.dec)
-        for set_index in (0, 1):
-            p = _lib.Peers()
-            for d, r in enumerate(nbr):
-                u, v, w = self.registry.pointers(r, set_index)
-                p.u[d], p.v[d], p.w[d] = u, v, w
-                _, nxl, _, nyl = self.dec.block(r)
-                p.nx[d], p.ny[d] = nxl, nyl
-            P.append(p)
-        return P
+        return peer_tables(self.dec, self.registry, 2)
 
     def step(self, n: int = 1, stream=None, events=None) -> None:
         from . import _lib, device as dv

@@ -134,6 +134,42 @@ def test_emulated_fused_push_stepping(px, py, shape):
             assert torch.equal(f.view(torch.int64), dec.local_view(w).contiguous().view(torch.int64)), dec.rank
 
 
+@pytest.mark.parametrize("px,py,shape", [(2, 2, (25, 23, 64)), (1, 2, (30, 26, 128)), (2, 4, (48, 40, 33)),
+                                         (2, 2, (16, 24, 300)), (3, 2, (36, 30, 7)), (1, 1, (9, 8, 63)),
+                                         (2, 1, (10, 40, 1031))])
+def test_emulated_pull_stepping(px, py, shape):
+    """PullStepper (halo cells pulled every step: inside K4 on the aligned
+    X-march, through the K2p gather kernel + the planner's K4 for odd nz and
+    deep columns) == single-domain stepping, bitwise, halos included after
+    refreshed_fields()."""
+    from paper_2010_01545_b200.decomp import LocalPeerRegistry, PullStepper, ThreadStreamBarrier
+    gd = pw.make_grid(*shape)
+    spec = pw.GeneratorSpec.baseline(13)
+    co = pw.baseline_coefficients(13, gd.nz)
+    single = Stepper(device.fill(gd, spec), co, 0.1)
+    single.step(5)
+    want = single.fields
+    torch.cuda.synchronize()
+    n = px * py
+    reg = LocalPeerRegistry()
+    bar = ThreadStreamBarrier(n)
+
+    def rank(r):
+        dec = Decomposition(gd, px, py, r)
+        fs = dec.fill_local(spec)
+        _poison_halos(fs)
+        st = PullStepper(dec, fs, co, 0.1, reg, bar.bind(r))
+        assert st.mode == ("fused" if gd.nz in (64, 128) else "gather")
+        st.step(5)
+        final = st.refreshed_fields()
+        torch.cuda.current_stream().synchronize()
+        return dec, final
+
+    for dec, final in run_ranks(n, rank):
+        for f, w in zip(final, want):
+            assert torch.equal(f.view(torch.int64), dec.local_view(w).contiguous().view(torch.int64)), dec.rank
+
+
 def _misaligned_fields(dims):
     """Zeroed padded fields that are 8- but not 16-byte aligned."""
     n = dims.padded_len

@@ -93,7 +93,18 @@ def _worker(rank, world, port, px, py, q, share=False, nz=64):
         for o, w in zip(out3, want_adv):
             ok &= torch.equal(o[1:-1, 1:-1].contiguous().view(torch.int64),
                               w[1 + xo:1 + xo + bx, 1 + yo:1 + yo + by].contiguous().view(torch.int64))
+        # steps with the halo cells pulled every step (fused on the aligned
+        # X-march, K2p gather + the planner's K4 otherwise)
+        fs4 = dec.fill_local(spec, device=dev)
+        reg4 = decomp.IpcPeerRegistry(dec)
+        ps = decomp.PullStepper(dec, fs4, co, 0.1, reg4, decomp.NcclBarrier(dev))
+        ps.step(5)
+        final = ps.refreshed_fields()
+        torch.cuda.synchronize()
+        for f, w in zip(final, want_step):
+            ok &= torch.equal(f.view(torch.int64), dec.local_view(w).contiguous().view(torch.int64))
         dist.barrier()
+        reg4.close()
         reg3.close()
         reg.close()
         dist.destroy_process_group()
