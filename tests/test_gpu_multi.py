@@ -28,6 +28,23 @@ pytestmark = pytest.mark.gpu
 NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
+def _shared_gpu_ok() -> bool:
+    """Several processes may open cuda:0 (compute mode Default): the dry run
+    needs it; an exclusive-process GPU skips those cases instead of failing."""
+    import subprocess
+    try:
+        out = subprocess.run(["nvidia-smi", "--query-gpu=compute_mode", "--format=csv,noheader", "-i", "0"],
+                             capture_output=True, text=True, timeout=30).stdout.strip()
+    except Exception:  # noqa: BLE001
+        return True
+    return out in ("", "Default")
+
+
+def _skip_unless_shareable(share: bool) -> None:
+    if share and not _shared_gpu_ok():
+        pytest.skip("GPU 0 is in an exclusive compute mode: no shared-GPU dry run")
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -120,6 +137,7 @@ def test_nccl_exchange_and_fused_ipc_step(px, py):
     share = world > NGPU  # dry run: the ranks share cuda:0 (module docstring)
     if share and world > 4:
         pytest.skip(f"needs {world} GPUs (the shared-GPU dry run stops at 4 ranks)")
+    _skip_unless_shareable(share)
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -144,6 +162,7 @@ def test_off_xmarch_blocks_across_processes(px, py, nz):
     kernel — bitwise against the single-domain result."""
     world = px * py
     share = world > NGPU
+    _skip_unless_shareable(share)
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -174,6 +193,7 @@ def test_bench_under_torchrun(config):
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(root / "bench.py"),
            "--gpus", "2", "--config", config, "--steps", "10", "--warmup", "3", "--no-cpu", "--no-e2e"]
     env = dict(os.environ)
+    _skip_unless_shareable(NGPU < 2)
     if NGPU < 2:
         env["PWADV_BENCH_SHARE_GPU"] = "1"
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root, env=env)
@@ -206,6 +226,7 @@ def test_bench_ranks_fall_back_together(where, config):
            "--gpus", "2", "--config", config, "--steps", "5", "--warmup", "3", "--no-cpu", "--no-e2e",
            "--no-traffic"]
     env = dict(os.environ, PWADV_BENCH_FAIL=where)
+    _skip_unless_shareable(NGPU < 2)
     if NGPU < 2:
         env["PWADV_BENCH_SHARE_GPU"] = "1"
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root, env=env)
