@@ -314,16 +314,88 @@ def run_reference(fields, coeffs) -> SourceSet:
     gd = GridDims(dims.nx, dims.ny, dims.nz)
     u, v, w = (_host_array(f, dims) for f in (fields.u, fields.v, fields.w))
     outs = [_output_array(gd.padded_shape) for _ in range(3)]
+    planes = _slab_planes(gd)
+    from ._lib import PwadvError
+    while True:
+        try:
+            if planes >= gd.nx:
+                _advect_host(gd, (u, v, w), outs, coeffs)
+            else:
+                _advect_host_slabs(gd, (u, v, w), outs, coeffs, planes)
+            break
+        except PwadvError as exc:
+            # the device buffers did not fit beside what else lives on the
+            # GPU: halve the slab and try again (loud once one plane fails)
+            if "out of memory" not in str(exc) or planes <= 1:
+                raise
+            planes = max(1, min(planes, gd.nx) // 2)
+    return SourceSet(*(Field3D(gd, o) for o in outs))
+
+
+def _advect_host(gd, ins, outs, coeffs) -> None:
     from .device import ContextClosed
     for attempt in range(3):
         try:
-            _context(gd).advect_host(u, v, w, *outs, coeffs.tcx, coeffs.tcy, coeffs.tzc1,
-                                     coeffs.tzc2)
-            break
+            _context(gd).advect_host(*ins, *outs, coeffs.tcx, coeffs.tcy, coeffs.tzc1, coeffs.tzc2)
+            return
         except ContextClosed:  # evicted by another thread between fetch and call
             if attempt == 2:
                 raise
-    return SourceSet(*(Field3D(gd, o) for o in outs))
+
+
+# Share of the device memory the drop-in's six padded device arrays may take
+# before a grid is evaluated X slab by X slab (PWADV_DROPIN_DEVICE_BYTES
+# overrides the byte limit: tests force slabs on small grids with it).
+_DEVICE_SHARE = 0.65
+
+
+def _slab_planes(gd) -> int:
+    """Interior X planes per device-resident slab: nx when the whole grid fits."""
+    import os
+
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("run_reference needs a CUDA device: the B200 path has no CPU fallback")
+    limit = int(os.environ.get("PWADV_DROPIN_DEVICE_BYTES", "0")) or int(
+        _DEVICE_SHARE * torch.cuda.get_device_properties(torch.cuda.current_device()).total_memory)
+    per_plane = 6 * 8 * (gd.ny + 2) * gd.nz
+    if per_plane * (gd.nx + 2) <= limit:
+        return gd.nx
+    n = limit // per_plane - 2
+    if n < 1:
+        raise ValueError(f"one X plane of {gd.ny + 2} x {gd.nz} with its two halo planes "
+                         f"({3 * per_plane} bytes on the device) exceeds the limit of {limit} bytes")
+    return int(n)
+
+
+def _advect_host_slabs(gd, ins, outs, coeffs, planes: int) -> None:
+    """Out-of-core evaluation of a grid larger than the device: X slabs of
+    `planes` interior planes, each with its two neighbouring planes as halo —
+    a contiguous run of the padded host arrays, X being the slowest axis — go
+    through the slab shape's context, in and out of the same runs of the
+    caller's arrays (no staging copy of a slab). A slab's output run starts
+    one plane early, on the previous slab's last interior plane, which the
+    slab's own (zero) halo plane would overwrite: that one plane is saved and
+    put back; the plane after the run is the next slab's first, written later,
+    or the grid's halo plane. Bit-identical to the whole-grid evaluation (the
+    reference's X-slab engines, schedules.py:65-75, rest on the same
+    independence); halo planes, halo columns and level 0 are +0.0 as
+    zeros_sources leaves them (grid.py:129-130)."""
+    nx = gd.nx
+    i0 = 1
+    while i0 <= nx:
+        n = min(planes, nx + 1 - i0)
+        sd = GridDims(n, gd.ny, gd.nz)
+        keep = [o[i0 - 1].copy() for o in outs] if i0 > 1 else None
+        _advect_host(sd, [a[i0 - 1:i0 + n + 1] for a in ins], [o[i0 - 1:i0 + n + 1] for o in outs],
+                     coeffs)
+        if keep is not None:
+            for o, k in zip(outs, keep):
+                o[i0 - 1] = k
+        i0 += n
+    for o in outs:
+        o[0] = 0.0
+        o[nx + 1] = 0.0
 
 
 def _advect_point(which: int, fields, coeffs, i: int, j: int, k: int) -> float:

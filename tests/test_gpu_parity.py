@@ -68,6 +68,33 @@ def test_reference_goldens_json_through_drop_in():
     assert pw.checksum(src.sw) == g["sources"]["sw"]
 
 
+@pytest.mark.parametrize("shape,planes", [((37, 29, 64), 8), ((9, 5, 63), 1), ((20, 12, 130), 19), ((8, 8, 8), 3)])
+def test_drop_in_out_of_core_slabs(shape, planes, monkeypatch):
+    """A grid larger than the drop-in's device share is evaluated X slab by X
+    slab (forced here on small grids through PWADV_DROPIN_DEVICE_BYTES):
+    run_reference must give the whole-grid bits, halos and level 0 +0.0, for
+    even and ragged slab counts and a one-plane slab."""
+    from paper_2010_01545_b200 import stencil
+    nx, ny, nz = shape
+    dims = pw.make_grid(nx, ny, nz)
+    fields = pw.fill_fields(dims, pw.GeneratorSpec.baseline(17))
+    co = pw.baseline_coefficients(17, nz)
+    monkeypatch.delenv("PWADV_DROPIN_DEVICE_BYTES", raising=False)
+    assert stencil._slab_planes(stencil.GridDims(nx, ny, nz)) == nx
+    whole = pw.run_reference(fields, co)
+    monkeypatch.setenv("PWADV_DROPIN_DEVICE_BYTES", str((planes + 2) * 6 * 8 * (ny + 2) * nz + 7))
+    assert stencil._slab_planes(stencil.GridDims(nx, ny, nz)) == planes
+    sl = pw.run_reference(fields, co)
+    for a, b in zip((whole.su, whole.sv, whole.sw), (sl.su, sl.sv, sl.sw)):
+        assert a.data.tobytes() == b.data.tobytes()
+    want = oracle.advect(fields.u.data, fields.v.data, fields.w.data, co.tcx, co.tcy, co.tzc1, co.tzc2)
+    for got, w in zip((sl.su, sl.sv, sl.sw), want):
+        assert got.data.tobytes() == np.ascontiguousarray(w).tobytes()
+    monkeypatch.setenv("PWADV_DROPIN_DEVICE_BYTES", "1000")
+    with pytest.raises(ValueError):
+        pw.run_reference(fields, co)
+
+
 # --- device generator K5 ------------------------------------------------------
 
 @pytest.mark.parametrize("shape,seed,baseline", [((8, 8, 8), 42, False), ((64, 64, 64), 42, True),
