@@ -166,8 +166,37 @@ def test_pull_evaluator_peer_table(px, py, shape):
         # x neighbours share this block's y extent, y neighbours its x extent
         assert p.ny[_lib.NB_XM] == p.ny[_lib.NB_XP] == dec.local_dims.ny
         assert p.nx[_lib.NB_YM] == p.nx[_lib.NB_YP] == dec.local_dims.nx
+        # the corner neighbours sit on the x neighbours' rows and the y neighbours'
+        # columns (what pwadv_pull_halos_f64 requires of a peer table)
+        for c, xn, yn in ((_lib.NB_XMYM, _lib.NB_XM, _lib.NB_YM), (_lib.NB_XMYP, _lib.NB_XM, _lib.NB_YP),
+                          (_lib.NB_XPYM, _lib.NB_XP, _lib.NB_YM), (_lib.NB_XPYP, _lib.NB_XP, _lib.NB_YP)):
+            assert p.nx[c] == p.nx[xn] and p.ny[c] == p.ny[yn], (dec.rank, c)
         if px == 1:
             assert (p.u[_lib.NB_XM], p.u[_lib.NB_XP]) == (ptrs[dec.rank][0],) * 2
+
+
+def test_peer_tables_one_per_buffer_set():
+    """peer_tables (PushStepper / PullStepper): table s names the neighbours'
+    set-s buffers; extents are the same in both."""
+    from paper_2010_01545_b200 import _lib
+    from paper_2010_01545_b200.decomp import LocalPeerRegistry, peer_tables
+    gd = pw.make_grid(7, 9, 4)
+    px, py = 2, 3
+    reg = LocalPeerRegistry()
+    sets = {}
+    for r in range(px * py):
+        d = Decomposition(gd, px, py, r).local_dims
+        sets[r] = tuple(tuple(torch.zeros(d.padded_shape, dtype=torch.float64) for _ in range(3))
+                        for _ in range(2))
+        reg.publish(r, sets[r])
+    for r in range(px * py):
+        dec = Decomposition(gd, px, py, r)
+        t0, t1 = peer_tables(dec, reg, 2)
+        cx, cy = dec.coords
+        nb = dec.rank_of(cx + 1, cy)  # NB_XP
+        assert t0.u[_lib.NB_XP] == sets[nb][0][0].data_ptr()
+        assert t1.w[_lib.NB_XP] == sets[nb][1][2].data_ptr()
+        assert list(t0.nx) == list(t1.nx) and list(t0.ny) == list(t1.ny)
 
 
 @pytest.mark.parametrize("px,py", [(1, 2), (2, 2), (2, 4), (3, 2), (1, 1)])
