@@ -130,6 +130,29 @@ def _worker(rank, world, port, px, py, q, share=False, nz=64):
         q.put((rank, False, repr(e)))
 
 
+def _run_ranks(world, px, py, share, nz=64):
+    """One process per rank running _worker; (rank, ok, error) of every rank.
+    Ranks still alive at the end — a hang, a crash of their peers — are killed,
+    so none is left holding the GPU for the tests that follow."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, px, py, q, share, nz)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        results = [q.get(timeout=600) for _ in range(world)]
+        for p in procs:
+            p.join(timeout=120)
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.kill()
+    assert sorted(r for r, _, _ in results) == list(range(world))
+    return results
+
+
 @pytest.mark.skipif(NGPU < 1, reason="needs a GPU")
 @pytest.mark.parametrize("px,py", [(1, 2), (2, 1), (2, 2), (2, 4)])
 def test_nccl_exchange_and_fused_ipc_step(px, py):
@@ -138,18 +161,7 @@ def test_nccl_exchange_and_fused_ipc_step(px, py):
     if share and world > 4:
         pytest.skip(f"needs {world} GPUs (the shared-GPU dry run stops at 4 ranks)")
     _skip_unless_shareable(share)
-    import torch.multiprocessing as mp
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, px, py, q, share)) for r in range(world)]
-    for p in procs:
-        p.start()
-    results = [q.get(timeout=600) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=120)
-    assert sorted(r for r, _, _ in results) == list(range(world))
-    for r, ok, err in results:
+    for r, ok, err in _run_ranks(world, px, py, share):
         assert ok, (r, err)
 
 
@@ -163,17 +175,7 @@ def test_off_xmarch_blocks_across_processes(px, py, nz):
     world = px * py
     share = world > NGPU
     _skip_unless_shareable(share)
-    import torch.multiprocessing as mp
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, px, py, q, share, nz)) for r in range(world)]
-    for p in procs:
-        p.start()
-    results = [q.get(timeout=600) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=120)
-    for r, ok, err in results:
+    for r, ok, err in _run_ranks(world, px, py, share, nz):
         assert ok, (r, err)
 
 
