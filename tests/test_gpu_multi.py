@@ -130,6 +130,23 @@ def _worker(rank, world, port, px, py, q, share=False, nz=64):
         q.put((rank, False, repr(e)))
 
 
+def _run_torchrun(cmd, env, cwd, timeout):
+    """subprocess.run for a torchrun command in its own process group: on a
+    timeout the whole group (torchrun and its ranks) is killed, so no rank is
+    left holding the GPU."""
+    import signal
+    import subprocess
+    p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, cwd=cwd,
+                         env=env, start_new_session=True)
+    try:
+        out, err = p.communicate(timeout=timeout)
+    except subprocess.TimeoutExpired:
+        os.killpg(p.pid, signal.SIGKILL)
+        out, err = p.communicate()
+        raise AssertionError(f"timed out after {timeout} s: {err[-2000:]}")
+    return subprocess.CompletedProcess(cmd, p.returncode, out, err)
+
+
 def _run_ranks(world, px, py, share, nz=64):
     """One process per rank running _worker; (rank, ok, error) of every rank.
     Ranks still alive at the end — a hang, a crash of their peers — are killed,
@@ -198,7 +215,7 @@ def test_bench_under_torchrun(config):
     _skip_unless_shareable(NGPU < 2)
     if NGPU < 2:
         env["PWADV_BENCH_SHARE_GPU"] = "1"
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root, env=env)
+    r = _run_torchrun(cmd, env, root, 900)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
@@ -231,7 +248,7 @@ def test_bench_ranks_fall_back_together(where, config):
     _skip_unless_shareable(NGPU < 2)
     if NGPU < 2:
         env["PWADV_BENCH_SHARE_GPU"] = "1"
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root, env=env)
+    r = _run_torchrun(cmd, env, root, 240)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
